@@ -1,0 +1,152 @@
+/*
+ * psd_filter.h -- C ABI of the B200 (sm_100a) PSD-cone projection library
+ * (libpsdfilter.so) implementing the hot path of arXiv 2507.09165.
+ *
+ * Citations: "P:L<n>" is line n of the paper text (PAPER.md; Doc C, lines 337-1205,
+ * is the authority).  DESIGN.md lists every reading R<k> of the paper used here.
+ *
+ * The method (Algorithm 2, "Run-time projection algorithm"):
+ *     lambda~ = upper bound of ||X||_2          (here ||X||_F; reading R4)
+ *     X_0     = X / lambda~
+ *     X_t     = f_t(X_{t-1}),  t = 1..T
+ *     P       = lambda~ * 1/2 * X_0 (I + X_T)
+ * with f_t(x) = sum_{j=0}^{p_t} c_{t,j} x^{2j+1} odd of degree d_t = 2 p_t + 1
+ * (Eq. comp:minimax-sign P:L502-508; odd monomials P:L57).  Every stage is a chain of
+ * dense symmetric products: Y = X X; Horner in Y; one multiply by X.
+ * GEMM count = sum_t (d_t + 1)/2 (+1 for the reconstruction), P:L598 / P:L647.
+ *
+ * Conventions common to every entry point
+ *   - Matrices are dense, row-major, fp32, n x n, `batch` of them contiguous
+ *     (matrix b starts at b*n*n).  Only the UPPER triangle of X is read
+ *     (X_ij := X_min(i,j),max(i,j); reading R10).  Outputs are fully written and
+ *     exactly symmetric (mirrored stores).
+ *   - Device pointers: X, out, lambda_* live in device memory of the current
+ *     device; they are caller-owned and must be 16-byte aligned.  out == X
+ *     (in place) is allowed.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All device work is stream-ordered and asynchronous; the host never syncs
+ *     except in psd_status().
+ *   - Synchronous argument errors return PSD_EINVAL (etc.) immediately and set a
+ *     thread-local message readable through psd_last_error().  Numeric problems
+ *     found on the device (non-finite input) set the handle's status word;
+ *     psd_status() reports them.
+ *   - A handle owns its copied coefficients and a lazily grown device workspace.
+ *     One handle may be used from one host thread at a time; distinct handles are
+ *     independent.
+ */
+#ifndef PSD_FILTER_H
+#define PSD_FILTER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct psd_filter_s* psd_filter_t;
+
+typedef enum {
+    PSD_OK = 0,
+    PSD_EINVAL = 1,        /* bad argument (message in psd_last_error) */
+    PSD_ENOMEM = 2,        /* device workspace allocation failed */
+    PSD_ECUDA = 3,         /* a CUDA runtime/driver call failed */
+    PSD_ENCCL = 4,         /* reserved for the row-panel multi-GPU path */
+    PSD_ENONFINITE = 5,    /* device found a non-finite input (output is NaN) */
+    PSD_EUNSUPPORTED = 6   /* configuration not supported by this build / device */
+} psd_status_t;
+
+/* Operand precision of the tensor-core products; accumulation is always fp32.
+ * FP16: the paper's half-precision path.  BF16: same kernel, bf16 operands.
+ * TF32: kind::tf32 single pass.  TF32X3: 3-pass split hi*hi + hi*lo + lo*hi on
+ * kind::tf32, the FP32 path (the paper's FP32 / BF16x9-emulated path).
+ * Readings R11 and R17 in DESIGN.md. */
+typedef enum {
+    PSD_PREC_FP16 = 0,
+    PSD_PREC_BF16 = 1,
+    PSD_PREC_TF32 = 2,
+    PSD_PREC_TF32X3 = 3
+} psd_precision_t;
+
+/* FROBENIUS: lambda~ = ||X||_F computed on the device (default).
+ * USER: lambda~ taken from psd_project_ex's lambda_in (device, one double per matrix). */
+typedef enum {
+    PSD_BOUND_FROBENIUS = 0,
+    PSD_BOUND_USER = 1
+} psd_bound_t;
+
+/* Library version string, e.g. "psdfilter 0.1 sm_100a". Never NULL. Host only. */
+const char* psd_version(void);
+
+/* Thread-local message for the last synchronous error on this thread ("" if none). */
+const char* psd_last_error(void);
+
+/* Create a composite filter (Eq. composite-polynomial-filter).
+ *   T       number of stages, 1 <= T <= 64.
+ *   degrees T odd degrees d_t, 1 <= d_t <= 15; stage t is applied t-th (f_1 first).
+ *   coeffs  sum_t (d_t+1)/2 doubles, stage-major; within a stage c_{t,0} (of x) first,
+ *           then x^3, x^5, ...  Stabilisation factors must already be folded in
+ *           by the caller (python: paper_2507_09165_b200.filters).  All finite.
+ *   eps     design epsilon of Eq. comp:minimax-sign (0 < eps < 1); recorded only, it
+ *           does not change the map X -> P (reading R15).
+ *   out     receives the handle.
+ * Copies its inputs; makes no CUDA call (host only).  Degree-1 stages are scalar
+ * multiplies folded into the neighbouring products (0 GEMMs, reading R7).
+ * Returns PSD_EINVAL on bad arguments. */
+psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, double eps,
+                               psd_filter_t* out);
+
+/* Frees the handle and its device workspace (synchronises the device first). NULL-safe. */
+void psd_filter_destroy(psd_filter_t h);
+
+/* Operand precision (default PSD_PREC_FP16). Host only. */
+psd_status_t psd_filter_set_precision(psd_filter_t h, psd_precision_t prec);
+
+/* Bound used to normalise X (default PSD_BOUND_FROBENIUS). Host only. */
+psd_status_t psd_filter_set_bound(psd_filter_t h, psd_bound_t bound);
+
+/* Number of tensor-core products one matrix costs: sum_t (d_t+1)/2 over stages with
+ * d_t > 1, plus 1 if `for_project` (the reconstruction of P:L757).  Host only.
+ * Returns -1 for a NULL handle. */
+int psd_filter_gemm_count(psd_filter_t h, int for_project);
+
+/* Algorithm 2: out[b] = P(X[b]) for b < batch, n >= 1, batch >= 1.
+ * X, out: device fp32, see conventions.  Returns PSD_OK once all work is enqueued. */
+psd_status_t psd_project(psd_filter_t h, const float* X, int64_t n, int64_t batch,
+                         float* out, void* stream);
+
+/* Matrix sign output of the same chain: out[b] = X_T = f_T o ... o f_1 (X[b]/lambda~)
+ * (Eq. matrix-sign; the loop of Algorithm 2). */
+psd_status_t psd_sign(psd_filter_t h, const float* X, int64_t n, int64_t batch,
+                      float* out, void* stream);
+
+/* psd_project with explicit bounds.
+ *   lambda_in   device, `batch` doubles; used iff the bound is PSD_BOUND_USER (else may be NULL).
+ *   lambda_out  device, `batch` doubles receiving the lambda~ actually used; may be NULL.
+ *   want_sign   0: out = P (psd_project); 1: out = X_T (psd_sign). */
+psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t batch,
+                            float* out, const double* lambda_in, double* lambda_out,
+                            int want_sign, void* stream);
+
+/* Synchronises `stream`, then returns and clears the handle's device status word:
+ * PSD_OK or PSD_ENONFINITE (some input had a non-finite entry). */
+psd_status_t psd_status(psd_filter_t h, void* stream);
+
+/* Bytes of device workspace the handle would hold for (n, batch) at its precision. */
+int64_t psd_workspace_bytes(psd_filter_t h, int64_t n, int64_t batch);
+
+/* One symmetric product with the fused epilogue, exposed as a building block and
+ * for kernel-level tests (the products of P:L395-399 whose output is symmetric):
+ *   C = alpha * (A B) + beta * D,   A, B symmetric with A B = B A, n x n, `batch` of them.
+ *   A, B  device fp32 (upper triangle read), converted to the handle's precision first.
+ *   D     device fp32 or NULL (beta ignored); upper triangle read.
+ *   C     device fp32, fully written, mirrored from the computed upper triangle.
+ * Uses the handle's workspace; stream-ordered. */
+psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, const float* D,
+                             double alpha, double beta, int64_t n, int64_t batch, float* C,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSD_FILTER_H */

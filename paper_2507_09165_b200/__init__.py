@@ -1,0 +1,135 @@
+"""B200-native PSD-cone projection by composite polynomial filtering (arXiv 2507.09165).
+
+Thin Python binding over the C ABI of ``include/psd_filter.h`` (libpsdfilter.so).
+PyTorch supplies device memory and streams only; every step of the projection --
+the Frobenius bound, the scale/convert, the T-stage chain of fused symmetric
+products and the reconstruction -- runs in this package's sm_100a kernels.
+
+    import torch
+    from paper_2507_09165_b200 import Filter, filters
+    f = Filter(filters.half_filter(), precision="fp16")
+    P = f.project(X)            # X: (n, n) or (batch, n, n) float32 CUDA tensor
+
+Names follow the paper: ``project`` is Algorithm 2, ``sign`` returns
+X_T (the matrix-sign approximation), ``gemm_count`` the GEMM budget.
+"""
+import ctypes
+
+from . import filters  # noqa: F401
+from ._lib import BOUNDS, PRECISIONS, PsdError, check, load  # noqa: F401
+
+__all__ = ["Filter", "filters", "PsdError", "version"]
+
+
+def version():
+    return load().psd_version().decode()
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check_matrix(X):
+    import torch
+    if not isinstance(X, torch.Tensor) or not X.is_cuda or X.dtype != torch.float32:
+        raise TypeError("X must be a float32 CUDA tensor")
+    if X.dim() == 2:
+        Xb = X.unsqueeze(0)
+    elif X.dim() == 3:
+        Xb = X
+    else:
+        raise ValueError("X must be (n, n) or (batch, n, n)")
+    if Xb.shape[-1] != Xb.shape[-2]:
+        raise ValueError("X must be square")
+    if not Xb.is_contiguous():
+        raise ValueError("X must be contiguous")
+    return Xb
+
+
+class Filter:
+    """A composite polynomial filter f_T o ... o f_1 (Eq. composite-polynomial-filter).
+
+    stages    sequence of coefficient tuples (c_{t,0}, c_{t,1}, ...) of x, x^3, ...;
+              stabilisation factors already folded (see ``filters``).
+    precision 'fp16' (default, the paper's half path), 'bf16', 'tf32', 'tf32x3'.
+    bound     'frobenius' (lambda~ = ||X||_F on device) or 'user' (pass lambda_in).
+    """
+
+    def __init__(self, stages, eps=1e-3, precision="fp16", bound="frobenius"):
+        self._lib = load()
+        self.stages = [tuple(float(v) for v in c) for c in stages]
+        degrees, coeffs = filters.flatten(self.stages)
+        self.degrees = degrees
+        d = (ctypes.c_int * len(degrees))(*degrees)
+        c = (ctypes.c_double * len(coeffs))(*coeffs)
+        h = ctypes.c_void_p()
+        check(self._lib.psd_filter_create(len(degrees), d, c, float(eps), ctypes.byref(h)), "psd_filter_create")
+        self._h = h
+        self.precision = precision
+        self.bound = bound
+        check(self._lib.psd_filter_set_precision(self._h, PRECISIONS[precision]), "psd_filter_set_precision")
+        check(self._lib.psd_filter_set_bound(self._h, BOUNDS[bound]), "psd_filter_set_bound")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.psd_filter_destroy(h)
+            self._h = None
+
+    def gemm_count(self, for_project=True):
+        return self._lib.psd_filter_gemm_count(self._h, 1 if for_project else 0)
+
+    def workspace_bytes(self, n, batch=1):
+        return self._lib.psd_workspace_bytes(self._h, n, batch)
+
+    def _run(self, X, out, lambda_in, lambda_out, want_sign, stream):
+        import torch
+        Xb = _check_matrix(X)
+        if out is None:
+            out = torch.empty_like(X)
+        outb = _check_matrix(out)
+        if outb.shape != Xb.shape:
+            raise ValueError("out shape mismatch")
+        B, n = Xb.shape[0], Xb.shape[-1]
+        li = ctypes.c_void_p(lambda_in.data_ptr()) if lambda_in is not None else None
+        lo = ctypes.c_void_p(lambda_out.data_ptr()) if lambda_out is not None else None
+        check(self._lib.psd_project_ex(self._h, ctypes.c_void_p(Xb.data_ptr()), n, B,
+                                       ctypes.c_void_p(outb.data_ptr()), li, lo, 1 if want_sign else 0,
+                                       _stream_ptr(stream)), "psd_project_ex")
+        return out
+
+    def project(self, X, out=None, lambda_in=None, lambda_out=None, stream=None):
+        """P = lambda~ 1/2 X_0 (I + X_T)  (Algorithm 2).  ``lambda_out`` (float64
+        CUDA tensor of length batch) receives the lambda~ used; ``lambda_in`` is required
+        with bound='user'."""
+        return self._run(X, out, lambda_in, lambda_out, False, stream)
+
+    def sign(self, X, out=None, lambda_in=None, lambda_out=None, stream=None):
+        """S = X_T = f_T o ... o f_1 (X / lambda~)."""
+        return self._run(X, out, lambda_in, lambda_out, True, stream)
+
+    def status(self, stream=None):
+        """Synchronise and return 'PSD_OK' or 'PSD_ENONFINITE' (device numeric status)."""
+        from ._lib import STATUS_NAMES
+        code = self._lib.psd_status(self._h, _stream_ptr(stream))
+        if code not in (0, 5):
+            check(code, "psd_status")
+        return STATUS_NAMES[code]
+
+    def sym_product(self, A, B, D=None, alpha=1.0, beta=0.0, out=None, stream=None):
+        """C = alpha (A B) + beta D for commuting symmetric A, B (upper triangles read)."""
+        import torch
+        Ab, Bb = _check_matrix(A), _check_matrix(B)
+        if out is None:
+            out = torch.empty_like(A)
+        outb = _check_matrix(out)
+        Db = _check_matrix(D) if D is not None else None
+        nb, n = Ab.shape[0], Ab.shape[-1]
+        check(self._lib.psd_sym_product(self._h, ctypes.c_void_p(Ab.data_ptr()), ctypes.c_void_p(Bb.data_ptr()),
+                                        ctypes.c_void_p(Db.data_ptr()) if Db is not None else None,
+                                        float(alpha), float(beta), n, nb, ctypes.c_void_p(outb.data_ptr()),
+                                        _stream_ptr(stream)), "psd_sym_product")
+        return out

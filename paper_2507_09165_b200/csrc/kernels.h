@@ -1,0 +1,64 @@
+// kernels.h -- internal launch interface between the C-ABI driver (psd_api.cu) and the
+// sm_100a kernels.  Not part of the public ABI (include/psd_filter.h is).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace psd {
+
+enum class OpType : int { F16 = 0, BF16 = 1, TF32 = 2 };
+
+// Square output tile of the symmetric product kernel and its K block (bytes of one
+// operand row slice = one 128B swizzle atom).
+constexpr int kTile = 128;
+constexpr int kBlockKBytes = 128;
+constexpr int kPadTo = 128;   // padded matrix dimension multiple
+
+// Epilogue of one symmetric product C = alpha_eff * (A B) + beta * D over the upper
+// tiles (I <= J) of each matrix; see sym_gemm.cu for which elements go where.
+struct EpiParams {
+    float alpha;              // host factor
+    const double* alpha_dev;  // optional per-matrix factor (lambda~), multiplies alpha
+    float beta;
+    const float* D;           // optional fp32 addend, upper triangle read
+    int64_t ldD, strideD;     // row stride / matrix stride (elements)
+    int nD;                   // rows/cols of D that exist (mask)
+    void* out_op;             // operand-precision copy, full mirrored, ld = npad (or NULL)
+    float* out32;             // fp32 master, upper tiles only, ld = npad (or NULL)
+    float* outF;              // final fp32 output, full mirrored, masked to nF (or NULL)
+    int64_t ldF, strideF;
+    int nF;
+};
+
+struct GemmShape {
+    int npad;                 // padded n (multiple of kTile)
+    int batch;
+};
+
+// Host-side TMA descriptor for an operand buffer [batch*npad rows][npad cols].
+bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch);
+
+// C = alpha*(A B) + beta*D on the upper tiles; A, B given by their tensor maps.
+cudaError_t launch_sym_gemm(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                            const GemmShape& s, const EpiParams& e, cudaStream_t stream);
+
+// Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
+// x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
+int bound_blocks_per_matrix(int n);
+cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
+                                      cudaStream_t stream);
+
+// lambda[b] = sqrt(sum_k partial[b*nblk+k]) (fixed order); status |= 1 if non-finite.
+cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, double* lambda,
+                                  double* lambda_out, unsigned* status, cudaStream_t stream);
+
+// X0 = sym_upper(X) / lambda[b] (or * scale when lambda == NULL), written as
+//   op copy (full, mirrored, zero padded, ld npad)  -- if out_op
+//   fp32 master (upper 32-tiles, zero padded)       -- if out32
+//   fp32 final (full, mirrored, ld n)               -- if outF (scaled by post)
+cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
+                                 const double* lambda, double scale, void* out_op, float* out32,
+                                 float* outF, double post, cudaStream_t stream);
+
+}  // namespace psd

@@ -1,0 +1,429 @@
+// psd_api.cu -- the C ABI of include/psd_filter.h: argument validation, the stage
+// planner (Algorithm 2 as a list of fused symmetric products), the device workspace
+// and the stream-ordered launches.  Host code; kernels live in sym_gemm.cu and
+// bound_scale.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/psd_filter.h"
+#include "kernels.h"
+
+using namespace psd;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+psd_status_t fail(psd_status_t st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+psd_status_t cuda_fail(cudaError_t e, const char* where) {
+    return fail(PSD_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Operand buffers of the chain (operand precision, full mirrored, [batch][npad][npad]).
+enum Buf { B_XA = 0, B_XB, B_X0, B_Y, B_UA, B_UB, B_COUNT };
+// fp32 master buffers (upper tiles) and addend sources.
+enum Master { M_NONE = -1, M_X = 0, M_Y = 1, M_XIN = 2, M_USER = 3 };
+
+struct Step {
+    int A, B;            // operand buffers
+    double alpha;        // host factor
+    bool alpha_lambda;   // multiply alpha by lambda~[b] on the device
+    double beta;
+    int D;               // Master id of the addend (M_NONE: none)
+    int out_op;          // operand buffer written (-1: none)
+    int out32;           // master written (M_NONE / M_X / M_Y)
+    bool outF;           // final fp32 output
+};
+
+struct Workspace {
+    int npad = 0, batch = 0;
+    OpType op = OpType::F16;
+    void* op_buf[B_COUNT] = {};
+    float* master[2] = {};
+    double* partial = nullptr;
+    double* lambda = nullptr;
+    unsigned* status = nullptr;
+    CUtensorMap tmap[B_COUNT];
+    int nblk = 0;
+};
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int op_bytes(OpType t) { return t == OpType::TF32 ? 4 : 2; }
+
+}  // namespace
+
+struct psd_filter_s {
+    std::vector<int> degrees;
+    std::vector<std::vector<double>> coeffs;
+    double eps = 1e-3;
+    psd_precision_t prec = PSD_PREC_FP16;
+    psd_bound_t bound = PSD_BOUND_FROBENIUS;
+    Workspace ws;
+};
+
+namespace {
+
+OpType op_of(psd_precision_t p) {
+    switch (p) {
+        case PSD_PREC_BF16: return OpType::BF16;
+        case PSD_PREC_TF32: return OpType::TF32;
+        default: return OpType::F16;
+    }
+}
+
+void free_ws(Workspace& ws) {
+    for (auto& p : ws.op_buf) { if (p) cudaFree(p); p = nullptr; }
+    for (auto& p : ws.master) { if (p) cudaFree(p); p = nullptr; }
+    if (ws.partial) cudaFree(ws.partial);
+    if (ws.lambda) cudaFree(ws.lambda);
+    if (ws.status) cudaFree(ws.status);
+    ws.partial = nullptr;
+    ws.lambda = nullptr;
+    ws.status = nullptr;
+    ws.npad = ws.batch = 0;
+}
+
+int64_t ws_bytes(OpType op, int64_t npad, int64_t batch) {
+    const int64_t mat = npad * npad * batch;
+    return B_COUNT * mat * op_bytes(op) + 2 * mat * 4 + batch * 256 * 8 + batch * 8 + 64;
+}
+
+psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
+    Workspace& ws = h->ws;
+    const OpType op = op_of(h->prec);
+    if (ws.npad == npad && ws.batch >= batch && ws.op == op && ws.status) return PSD_OK;
+    if (ws.status) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    }
+    free_ws(ws);
+    const size_t mat = static_cast<size_t>(npad) * npad * batch;
+    for (int i = 0; i < B_COUNT; ++i) {
+        if (cudaMalloc(&ws.op_buf[i], mat * op_bytes(op)) != cudaSuccess) {
+            free_ws(ws);
+            return fail(PSD_ENOMEM, "cudaMalloc operand workspace failed");
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMalloc(&ws.master[i], mat * 4) != cudaSuccess) {
+            free_ws(ws);
+            return fail(PSD_ENOMEM, "cudaMalloc master workspace failed");
+        }
+    }
+    ws.nblk = 256;
+    if (cudaMalloc(&ws.partial, static_cast<size_t>(batch) * ws.nblk * 8) != cudaSuccess ||
+        cudaMalloc(&ws.lambda, static_cast<size_t>(batch) * 8) != cudaSuccess ||
+        cudaMalloc(&ws.status, 64) != cudaSuccess) {
+        free_ws(ws);
+        return fail(PSD_ENOMEM, "cudaMalloc small workspace failed");
+    }
+    cudaMemset(ws.status, 0, 64);
+    // Zero everything once: padded rows/cols of every operand and master must read as 0.
+    for (int i = 0; i < B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
+    for (int i = 0; i < 2; ++i) cudaMemset(ws.master[i], 0, mat * 4);
+    for (int i = 0; i < B_COUNT; ++i) {
+        if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch)) {
+            free_ws(ws);
+            return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
+        }
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        free_ws(ws);
+        return cuda_fail(e, "workspace init");
+    }
+    ws.npad = npad;
+    ws.batch = batch;
+    ws.op = op;
+    return PSD_OK;
+}
+
+// Algorithm 2's loop + return line as fused products.
+// Stage t with coefficients c_0..c_p (p >= 1), iterate Z (buffer `cur`, master M_X):
+//   Y = Z Z                                   -> Y op + Y master
+//   p == 1: Z' = c_0 Z + c_1 (Z Y)
+//   p >= 2: U  = c_p (Y Y) + c_{p-1} Y ;  U <- Y U + c_j Y (j = p-2..1) ;  Z' = c_0 Z + Z U
+// (identity-free Horner in Y = Z^2: no c*I term ever enters a low-precision operand).
+// Degree-1 stages (p = 0) and trailing scalars are carried as a pending factor s and
+// folded into the next products (f(sZ) = sum c_j s^{2j+1} Z^{2j+1}).
+std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign_only_scale) {
+    std::vector<Step> steps;
+    double s = 1.0;
+    int cur = B_X0;
+    int last_gemm_stage = -1;
+    for (size_t t = 0; t < h->coeffs.size(); ++t)
+        if (h->coeffs[t].size() > 1) last_gemm_stage = static_cast<int>(t);
+    double trailing = 1.0;
+    for (size_t t = last_gemm_stage + 1; t < h->coeffs.size(); ++t) trailing *= h->coeffs[t][0];
+
+    for (int t = 0; t <= last_gemm_stage; ++t) {
+        const std::vector<double>& c = h->coeffs[t];
+        const int p = static_cast<int>(c.size()) - 1;
+        if (p == 0) { s *= c[0]; continue; }
+        std::vector<double> cs(c.size());
+        for (int j = 0; j <= p; ++j) cs[j] = c[j] * std::pow(s, 2 * j + 1);
+        s = 1.0;
+        const int nxt = (cur == B_XA) ? B_XB : B_XA;
+        const bool last = (t == last_gemm_stage);
+        steps.push_back({cur, cur, 1.0, false, 0.0, M_NONE, B_Y, M_Y, false});
+        Step fin;
+        if (p == 1) {
+            fin = {cur, B_Y, cs[1], false, cs[0], M_X, nxt, M_X, false};
+        } else {
+            int u = B_UA;
+            steps.push_back({B_Y, B_Y, cs[p], false, cs[p - 1], M_Y, u, M_NONE, false});
+            for (int j = p - 2; j >= 1; --j) {
+                const int un = (u == B_UA) ? B_UB : B_UA;
+                steps.push_back({B_Y, u, 1.0, false, cs[j], M_Y, un, M_NONE, false});
+                u = un;
+            }
+            fin = {cur, u, 1.0, false, cs[0], M_X, nxt, M_X, false};
+        }
+        if (last && want_sign) {
+            fin.alpha *= trailing;
+            fin.beta *= trailing;
+            fin.out_op = -1;
+            fin.out32 = M_NONE;
+            fin.outF = true;
+        }
+        steps.push_back(fin);
+        cur = nxt;
+    }
+    *sign_only_scale = 0.0;
+    if (last_gemm_stage < 0) {
+        // no products in the chain: S = s * X0 with s = prod of all degree-1 coefficients
+        if (want_sign) {
+            *sign_only_scale = trailing;
+        } else {
+            steps.push_back({B_X0, B_X0, 0.5 * trailing, true, 0.5, M_XIN, -1, M_NONE, true});
+        }
+        return steps;
+    }
+    if (!want_sign) {
+        // P = 1/2 X + 1/2 lambda~ (X_0 S)  ==  lambda~ 1/2 X_0 (I + X_T)   (reading R5)
+        steps.push_back({B_X0, cur, 0.5 * trailing, true, 0.5, M_XIN, -1, M_NONE, true});
+    }
+    return steps;
+}
+
+psd_status_t check_args(psd_filter_t h, const void* X, int64_t n, int64_t batch, const void* out) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (!X || !out) return fail(PSD_EINVAL, "null X or out");
+    if (n < 1 || batch < 1) return fail(PSD_EINVAL, "n and batch must be >= 1");
+    if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+        return fail(PSD_EINVAL, "X and out must be 16-byte aligned");
+    if (n > 65536) return fail(PSD_EUNSUPPORTED, "n > 65536");
+    if (h->prec == PSD_PREC_TF32X3) return fail(PSD_EUNSUPPORTED, "TF32X3 not built yet");
+    return PSD_OK;
+}
+
+psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
+                 const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
+    psd_status_t rc = check_args(h, X, n64, batch64, out);
+    if (rc != PSD_OK) return rc;
+    if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
+    const int n = static_cast<int>(n64), batch = static_cast<int>(batch64);
+    const int npad = static_cast<int>(round_up(n, kPadTo));
+    rc = ensure_ws(h, npad, batch);
+    if (rc != PSD_OK) return rc;
+    Workspace& ws = h->ws;
+    cudaError_t e;
+
+    // (a1) bound
+    const double* lam = nullptr;
+    if (h->bound == PSD_BOUND_FROBENIUS) {
+        const int nblk = bound_blocks_per_matrix(n);
+        e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
+        if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
+        e = launch_finalize_bound(ws.partial, nblk, batch, ws.lambda, lambda_out, ws.status, st);
+        if (e != cudaSuccess) return cuda_fail(e, "finalize_bound");
+        lam = ws.lambda;
+    } else {
+        lam = lambda_in;
+        if (lambda_out && lambda_out != lambda_in) {
+            e = cudaMemcpyAsync(lambda_out, lambda_in, batch * sizeof(double), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "lambda copy");
+        }
+    }
+    double sign_only = 0.0;
+    std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
+    // (a2) scale + convert; the products-free sign chain finishes here
+    e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], ws.master[M_X],
+                             (want_sign && steps.empty()) ? out : nullptr, sign_only, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
+    // (a3-a6) products
+    GemmShape shape{npad, batch};
+    for (const Step& s : steps) {
+        EpiParams ep{};
+        ep.alpha = static_cast<float>(s.alpha);
+        ep.alpha_dev = s.alpha_lambda ? lam : nullptr;
+        ep.beta = static_cast<float>(s.beta);
+        if (s.D == M_X || s.D == M_Y) {
+            ep.D = ws.master[s.D];
+            ep.ldD = npad;
+            ep.strideD = static_cast<int64_t>(npad) * npad;
+            ep.nD = npad;
+        } else if (s.D == M_XIN) {
+            ep.D = X;
+            ep.ldD = n;
+            ep.strideD = static_cast<int64_t>(n) * n;
+            ep.nD = n;
+        }
+        ep.out_op = s.out_op >= 0 ? ws.op_buf[s.out_op] : nullptr;
+        ep.out32 = (s.out32 == M_X || s.out32 == M_Y) ? ws.master[s.out32] : nullptr;
+        if (s.outF) {
+            ep.outF = out;
+            ep.ldF = n;
+            ep.strideF = static_cast<int64_t>(n) * n;
+            ep.nF = n;
+        }
+        e = launch_sym_gemm(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st);
+        if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
+    }
+    return PSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psd_version(void) { return "psdfilter 0.1 sm_100a"; }
+
+const char* psd_last_error(void) { return g_last_error.c_str(); }
+
+psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, double eps, psd_filter_t* out) {
+    if (!out) return fail(PSD_EINVAL, "null out");
+    *out = nullptr;
+    if (T < 1 || T > 64) return fail(PSD_EINVAL, "T must be in [1, 64]");
+    if (!degrees || !coeffs) return fail(PSD_EINVAL, "null degrees or coeffs");
+    if (!(eps > 0.0 && eps < 1.0)) return fail(PSD_EINVAL, "eps must be in (0, 1)");
+    auto* h = new psd_filter_s();
+    h->eps = eps;
+    const double* c = coeffs;
+    for (int t = 0; t < T; ++t) {
+        const int d = degrees[t];
+        if (d < 1 || d > 15 || (d % 2) == 0) {
+            delete h;
+            return fail(PSD_EINVAL, "stage " + std::to_string(t) + ": degree must be odd in [1, 15]");
+        }
+        std::vector<double> cc(c, c + (d + 1) / 2);
+        for (double v : cc) {
+            if (!std::isfinite(v)) {
+                delete h;
+                return fail(PSD_EINVAL, "stage " + std::to_string(t) + ": non-finite coefficient");
+            }
+        }
+        c += (d + 1) / 2;
+        h->degrees.push_back(d);
+        h->coeffs.push_back(cc);
+    }
+    *out = h;
+    g_last_error.clear();
+    return PSD_OK;
+}
+
+void psd_filter_destroy(psd_filter_t h) {
+    if (!h) return;
+    if (h->ws.status) {
+        cudaDeviceSynchronize();
+        free_ws(h->ws);
+    }
+    delete h;
+}
+
+psd_status_t psd_filter_set_precision(psd_filter_t h, psd_precision_t prec) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (prec < PSD_PREC_FP16 || prec > PSD_PREC_TF32X3) return fail(PSD_EINVAL, "unknown precision");
+    h->prec = prec;
+    return PSD_OK;
+}
+
+psd_status_t psd_filter_set_bound(psd_filter_t h, psd_bound_t bound) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (bound != PSD_BOUND_FROBENIUS && bound != PSD_BOUND_USER) return fail(PSD_EINVAL, "unknown bound");
+    h->bound = bound;
+    return PSD_OK;
+}
+
+int psd_filter_gemm_count(psd_filter_t h, int for_project) {
+    if (!h) return -1;
+    int g = 0;
+    for (int d : h->degrees) g += d > 1 ? (d + 1) / 2 : 0;
+    return g + (for_project ? 1 : 0);
+}
+
+int64_t psd_workspace_bytes(psd_filter_t h, int64_t n, int64_t batch) {
+    if (!h || n < 1 || batch < 1) return -1;
+    return ws_bytes(op_of(h->prec), round_up(n, kPadTo), batch);
+}
+
+psd_status_t psd_project(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out, void* stream) {
+    if (h && h->bound == PSD_BOUND_USER) return fail(PSD_EINVAL, "PSD_BOUND_USER: use psd_project_ex");
+    return run(h, X, n, batch, out, nullptr, nullptr, false, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_sign(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out, void* stream) {
+    if (h && h->bound == PSD_BOUND_USER) return fail(PSD_EINVAL, "PSD_BOUND_USER: use psd_project_ex");
+    return run(h, X, n, batch, out, nullptr, nullptr, true, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out,
+                            const double* lambda_in, double* lambda_out, int want_sign, void* stream) {
+    return run(h, X, n, batch, out, lambda_in, lambda_out, want_sign != 0, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_status(psd_filter_t h, void* stream) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (!h->ws.status) return PSD_OK;
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    unsigned v = 0;
+    e = cudaMemcpy(&v, h->ws.status, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "status readback");
+    cudaMemset(h->ws.status, 0, sizeof(unsigned));
+    return v ? PSD_ENONFINITE : PSD_OK;
+}
+
+psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, const float* D, double alpha,
+                             double beta, int64_t n64, int64_t batch64, float* C, void* stream) {
+    psd_status_t rc = check_args(h, A, n64, batch64, C);
+    if (rc != PSD_OK) return rc;
+    if (!B) return fail(PSD_EINVAL, "null B");
+    const int n = static_cast<int>(n64), batch = static_cast<int>(batch64);
+    const int npad = static_cast<int>(round_up(n, kPadTo));
+    rc = ensure_ws(h, npad, batch);
+    if (rc != PSD_OK) return rc;
+    Workspace& ws = h->ws;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = launch_scale_convert(ws.op, A, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XA], nullptr,
+                                         nullptr, 0.0, st);
+    if (e == cudaSuccess)
+        e = launch_scale_convert(ws.op, B, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XB], nullptr, nullptr, 0.0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
+    EpiParams ep{};
+    ep.alpha = static_cast<float>(alpha);
+    ep.beta = static_cast<float>(beta);
+    if (D) {
+        ep.D = D;
+        ep.ldD = n;
+        ep.strideD = static_cast<int64_t>(n) * n;
+        ep.nD = n;
+    }
+    ep.outF = C;
+    ep.ldF = n;
+    ep.strideF = static_cast<int64_t>(n) * n;
+    ep.nF = n;
+    e = launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st);
+    if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
+    return PSD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,310 @@
+// sym_gemm.cu -- symmetric product C = alpha * (A B) + beta * D on sm_100a tensor cores.
+//
+// Every product of the composite filter (Algorithm 2) multiplies two
+// commuting symmetric matrices (powers/polynomials of the same X), so
+// C is symmetric: only upper tiles (I <= J) are computed and each is stored twice
+// (direct + transposed), which halves the MMA work and makes C exactly symmetric.
+// A and B are symmetric, so both operands are read as row panels ("K-major"):
+// A tile = rows I*128.., B^T tile = rows J*128.. of B (B^T = B).
+//
+// Pipeline per CTA (one 128x128 upper tile):
+//   warp 0 / 1 elected lane : TMA producer  -> kStages-deep smem ring (mbarrier full/empty)
+//   warp 1 / 1 elected lane : tcgen05.mma.cta_group::1 (M=128, N=128) into TMEM
+//   warps 0-3               : epilogue  tcgen05.ld -> alpha*acc + beta*D -> mirrored stores
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace psd {
+
+namespace {
+
+template <OpType T> struct OpTraits;
+template <> struct OpTraits<OpType::F16> {
+    using type = __half;
+    static constexpr int kBytes = 2;
+    static constexpr uint32_t kFmt = 0;
+    __device__ static type cvt(float v) { return __float2half_rn(v); }
+};
+template <> struct OpTraits<OpType::BF16> {
+    using type = __nv_bfloat16;
+    static constexpr int kBytes = 2;
+    static constexpr uint32_t kFmt = 1;
+    __device__ static type cvt(float v) { return __float2bfloat16_rn(v); }
+};
+template <> struct OpTraits<OpType::TF32> {
+    using type = float;
+    static constexpr int kBytes = 4;
+    static constexpr uint32_t kFmt = 2;
+    __device__ static type cvt(float v) {
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+        return __uint_as_float(r);
+    }
+};
+
+constexpr int kStages = 4;
+constexpr int kThreads = 128;
+constexpr int kTileBytes = kTile * kBlockKBytes;                 // 16 KB per operand tile
+constexpr int kSmemBytes = 2 * kStages * kTileBytes + 1024 + 256; // ring + align slack + barriers
+
+__device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J) {
+    // row-major enumeration of {(I, J): 0 <= I <= J < nt}
+    int i = 0;
+    int rem = t;
+    while (rem >= nt - i) { rem -= nt - i; ++i; }
+    I = i;
+    J = i + rem;
+}
+
+template <OpType T>
+__global__ void __launch_bounds__(kThreads, 1)
+sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmShape s, const EpiParams e) {
+    using Tr = OpTraits<T>;
+    using op_t = typename Tr::type;
+    constexpr int kBK = kBlockKBytes / Tr::kBytes;     // K elements per block (64 f16 / 32 tf32)
+    constexpr int kUmmaK = 32 / Tr::kBytes;            // K per tcgen05.mma (16 f16 / 8 tf32)
+    constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, kTile);
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kTileBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * kTileBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* accum_full = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nt = s.npad / kTile;
+    const int b = blockIdx.y;
+    int I, J;
+    upper_tile_coords(blockIdx.x, nt, I, J);
+
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            ptx::tma_prefetch_desc(&tmA);
+            ptx::tma_prefetch_desc(&tmB);
+            for (int i = 0; i < kStages; ++i) {
+                ptx::mbar_init(&full[i], 1);
+                ptx::mbar_init(&empty[i], 1);
+            }
+            ptx::mbar_init(accum_full, 1);
+            ptx::fence_barrier_init();
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        ptx::tmem_alloc<kTile>(tmem_slot);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_kb = s.npad / kBK;
+    const int rowA = b * s.npad + I * kTile;
+    const int rowB = b * s.npad + J * kTile;
+
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            const uint64_t pol = ptx::policy_evict_last();
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int st = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[st], 2 * kTileBytes);
+                ptx::tma_load_2d(sA + st * kTileBytes, &tmA, &full[st], kb * kBK, rowA, pol);
+                ptx::tma_load_2d(sB + st * kTileBytes, &tmB, &full[st], kb * kBK, rowB, pol);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (ptx::elect_one()) {
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int st = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                ptx::mbar_wait(&full[st], ph);
+                ptx::tc_fence_after();
+                const uint64_t adesc = ptx::smem_desc_sw128_kmajor(ptx::smem_u32(sA + st * kTileBytes));
+                const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(ptx::smem_u32(sB + st * kTileBytes));
+#pragma unroll
+                for (int k = 0; k < kBK / kUmmaK; ++k) {
+                    const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);   // 32 B per K step
+                    if constexpr (T == OpType::TF32)
+                        ptx::mma_tf32(tmem_base, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                    else
+                        ptx::mma_f16(tmem_base, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                }
+                ptx::mma_commit(&empty[st]);
+            }
+            ptx::mma_commit(accum_full);
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------------------------------ epilogue
+    ptx::mbar_wait(accum_full, 0);
+    ptx::tc_fence_after();
+
+    const int r = warp * 32 + lane;                 // tile row == TMEM lane
+    const int gi = I * kTile + r;                   // global row
+    const bool diag = (I == J);
+    float alpha = e.alpha;
+    if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
+    const float beta = e.beta;
+    op_t* out_op = reinterpret_cast<op_t*>(e.out_op);
+    const int64_t opBase = static_cast<int64_t>(b) * s.npad * s.npad;
+
+#pragma unroll 1
+    for (int c0 = 0; c0 < kTile; c0 += 32) {
+        uint32_t raw[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
+        ptx::tmem_ld_wait();
+        const int gj0 = J * kTile + c0;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
+        if (e.D) {
+            const float* drow = e.D + static_cast<int64_t>(b) * e.strideD + static_cast<int64_t>(gi) * e.ldD;
+            const bool row_ok = gi < e.nD;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                const bool ok = row_ok && gj < e.nD && gj >= gi;
+                v[i] += ok ? beta * drow[gj] : 0.0f;
+            }
+        }
+        // operand copy: direct (row gi) + transposed (row gj), mirrored
+        if (out_op) {
+            op_t* orow = out_op + opBase + static_cast<int64_t>(gi) * s.npad;
+            if (!diag) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
+                if constexpr (Tr::kBytes == 2) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            op_t lo = Tr::cvt(v[q * 8 + 2 * h]);
+                            op_t hi = Tr::cvt(v[q * 8 + 2 * h + 1]);
+                            w[h] = static_cast<uint32_t>(*reinterpret_cast<uint16_t*>(&lo)) |
+                                   (static_cast<uint32_t>(*reinterpret_cast<uint16_t*>(&hi)) << 16);
+                        }
+                        dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        dst[q] = make_uint4(__float_as_uint(Tr::cvt(v[4 * q])), __float_as_uint(Tr::cvt(v[4 * q + 1])),
+                                            __float_as_uint(Tr::cvt(v[4 * q + 2])), __float_as_uint(Tr::cvt(v[4 * q + 3])));
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                if (diag && gj < gi) continue;
+                const op_t cv = Tr::cvt(v[i]);
+                if (diag) orow[gj] = cv;
+                if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * s.npad + gi] = cv;
+            }
+        }
+        if (e.out32) {
+            float* mrow = e.out32 + opBase + static_cast<int64_t>(gi) * s.npad;
+            if (!diag) {
+                float4* dst = reinterpret_cast<float4*>(mrow + gj0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (gj0 + i >= gi) mrow[gj0 + i] = v[i];
+            }
+        }
+        if (e.outF && gi < e.nF) {
+            float* F = e.outF + static_cast<int64_t>(b) * e.strideF;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                if (gj >= e.nF || gj < gi) continue;     // upper part of this tile only
+                F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
+                if (gj != gi) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<kTile>(tmem_base);
+    }
+}
+
+template <OpType T>
+cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s,
+                     const EpiParams& e, cudaStream_t stream) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (err != cudaSuccess) return err;
+        attr_set = true;
+    }
+    const int nt = s.npad / kTile;
+    dim3 grid(nt * (nt + 1) / 2, s.batch);
+    sym_gemm_kernel<T><<<grid, kThreads, kSmemBytes, stream>>>(tmA, tmB, s, e);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_sym_gemm(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                            const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
+    switch (t) {
+        case OpType::F16: return launch_t<OpType::F16>(tmA, tmB, s, e, stream);
+        case OpType::BF16: return launch_t<OpType::BF16>(tmA, tmB, s, e, stream);
+        case OpType::TF32: return launch_t<OpType::TF32>(tmA, tmB, s, e, stream);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+}  // namespace
+
+bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    const int bytes = (t == OpType::TF32) ? 4 : 2;
+    const CUtensorMapDataType dt = (t == OpType::F16) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                 : (t == OpType::BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(npad), static_cast<cuuint64_t>(npad) * batch};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(npad) * bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockKBytes / bytes), static_cast<cuuint32_t>(kTile)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace psd
