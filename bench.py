@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the PSD-cone projection hot path (arXiv 2507.09165, Algorithm 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+
+Metric (BASELINE.json): PSD projections/sec and achieved tensor TFLOPS vs peak at n=4096.
+Default workload = config c4 of BASELINE.json: a global batch of 32 SDP-shaped symmetric
+n=4096 matrices, f~*_half with the P:L727 stabilisation folded (T=7, d=5, 22 products),
+fp16 operands / fp32 accumulation; for N > 1 (torchrun) the 32 matrices are sharded over
+the ranks (no collective on the data path; fixed total work -> "scaling": "strong").
+
+One step = one psd_project call over this rank's shard (bound + scale/convert + 21 chain
+products + the reconstruction product), inputs resident in HBM (2.1 GB > L2, so no L2
+flush is needed between steps).  Device time by CUDA events on the launching stream,
+barrier + synchronize around the timed region, max over ranks.
+
+--impl reference times the float64 CPU oracle (oracle/) on this host's cores on a bounded
+sample of the same workload (the tier's reference arm); rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c4": dict(n=4096, batch=32, family="sdp_shaped", filter="half",
+               workload="c4: batch 32 x n=4096 SDP-shaped symmetric iterates, f~*_half+kappa (T=7, d=5), "
+                        "global batch sharded over GPUs"),
+    "c3": dict(n=1024, batch=1, family="goe", filter="c3",
+               workload="c3: single n=1024 symmetric matrix, Remez filter T=6 d=5"),
+    "c2": dict(n=64, batch=4096, family="goe", filter="c2",
+               workload="c2: batch 4096 x 64x64 symmetric, Remez T=4 d=7"),
+    "c5": dict(n=16384, batch=1, family="goe", filter="half",
+               workload="c5: single n=16384 symmetric matrix (1 GPU here)"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def product_filter(name):
+    from paper_2507_09165_b200 import filters
+    return {"half": filters.half_filter, "single": filters.single_filter,
+            "c3": lambda: filters.remez_half_prefix(6), "c2": filters.c2_filter}[name]()
+
+
+def make_inputs(cfg, first, count, seed_base):
+    """Seeded synthetic inputs (synth/): matrix g of the global batch uses seed seed_base + g."""
+    import numpy as np
+    import torch
+
+    import synth
+    n = cfg["n"]
+    host = torch.empty((count, n, n), dtype=torch.float32, pin_memory=True)
+
+    def one(b):
+        host[b].copy_(torch.from_numpy(synth.make(cfg["family"], n, seed_base + first + b).astype(np.float32)))
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        list(ex.map(one, range(count)))
+    return host
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(cfg, stages_oracle, kappas, seconds_cap=30.0):
+    """Time the float64 oracle (as it stands) on a bounded sample of the workload.
+
+    Sample: one matrix of the config; stages of Algorithm 2 are run one at a time until
+    ~seconds_cap is spent (at least one stage); the per-matrix time is extrapolated by the
+    GEMM count (each oracle stage costs (d+1)/2 matmuls, the return line one more)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    import synth
+    from oracle import chain
+    n = cfg["n"]
+    X = synth.make(cfg["family"], n, synth.SEED_BASE)
+    t0 = time.perf_counter()
+    lam = chain.frobenius_bound(X)
+    Z = X / lam
+    done_gemms = 0
+    stages_run = 0
+    for t, c in enumerate(stages_oracle):
+        Z = chain.odd_poly_matrix(Z, c)
+        if kappas is not None:
+            Z = kappas[t] * Z
+        done_gemms += len(c) if len(c) > 1 else 0
+        stages_run += 1
+        if time.perf_counter() - t0 > seconds_cap:
+            break
+    if stages_run == len(stages_oracle):
+        P = lam * 0.5 * (X / lam @ (np.eye(n) + Z))
+        done_gemms += 1
+        del P
+    el = time.perf_counter() - t0
+    total_gemms = chain.gemm_count([2 * len(c) - 1 for c in stages_oracle])
+    per_matrix = el * total_gemms / max(done_gemms, 1)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    sample = (f"oracle/chain.py float64 on 1 of the {cfg['batch']} matrices (n={n}), {stages_run} of "
+              f"{len(stages_oracle)} stages = {done_gemms} of {total_gemms} numpy matmuls in {el:.1f} s, "
+              f"extrapolated by GEMM count")
+    return 1.0 / per_matrix, threads, sample
+
+
+def oracle_filter(name):
+    from oracle import tables
+    from paper_2507_09165_b200 import filters as pf
+    if name == "half":
+        return tables.F_HALF_REFINED, tables.half_kappas(7)
+    if name == "single":
+        return tables.F_SINGLE_REFINED, tables.single_kappas(10)
+    if name == "c3":
+        return tables.F_HALF[:6], None
+    return pf.c2_filter(), None
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    st, kap = oracle_filter(cfg["filter"])
+    per_step = max(5.0, 100.0 / max(args.steps + args.warmup, 1))
+    vals = []
+    threads, sample = 1, ""
+    for i in range(args.warmup + args.steps):
+        v, threads, sample = cpu_oracle_sample(cfg, st, kap, seconds_cap=per_step)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": cfg["n"], "global_batch": cfg["batch"],
+                   "family": cfg["family"]},
+        "cpu_baseline": {"value": value, "unit": "matrices/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "matrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import synth
+    from paper_2507_09165_b200 import Filter
+    n, gb = cfg["n"], cfg["batch"]
+    if gb % world:
+        raise SystemExit(f"global batch {gb} not divisible by {world} GPUs")
+    count = gb // world
+    first = rank * count
+
+    stages = product_filter(cfg["filter"])
+    f = Filter(stages, precision=args.precision)
+    G = f.gemm_count(True)
+
+    host_in = make_inputs(cfg, first, count, synth.SEED_BASE)
+    X = host_in.to(dev, non_blocking=False)
+    out = torch.empty_like(X)
+    stream = torch.cuda.current_stream(dev)
+
+    # warm-up (also allocates the workspace)
+    for _ in range(args.warmup):
+        f.project(X, out=out)
+    torch.cuda.synchronize(dev)
+    f.profile_read()  # reset counters
+    f.profile(True)
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            f.project(X, out=out)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prod_ms, prod_launches, kernel_launches = f.profile_read()
+    f.profile(False)
+    assert f.status() == "PSD_OK"
+
+    # e2e through the public API with pinned host buffers (H2D of the inputs and D2H of
+    # the projected matrices inside the timed region, every step)
+    e2e_ms = None
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 3))
+        f.project(X, out=out)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            X.copy_(host_in, non_blocking=True)
+            f.project(X, out=out)
+            host_out.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+
+    t = torch.tensor([ms, e2e_ms or 0.0, prod_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms_max, prod_ms_max = t.tolist()
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        ms_step = ms / args.steps
+        value = gb * args.steps / (ms / 1000.0)
+        # algorithmic work of one symmetric product: n(n+1)/2 independent outputs x 2n flops
+        alg_flops_product = float(n) * n * (n + 1)
+        dense_flops_matrix = 2.0 * n ** 3 * G
+        launch_ms = prod_ms_max / max(prod_launches, 1) if prod_launches else None
+        achieved = (alg_flops_product * count / (launch_ms / 1000.0) / 1e12) if launch_ms else None
+        peak_bf16 = peaks.get("bf16_tflops", 1590.0)
+        if args.precision in ("fp16", "bf16"):
+            peak = peak_bf16
+            peak_note = f"{peak_src} bf16 burst (fp16 = bf16 rate)"
+        else:
+            peak = peak_bf16 / 2.0
+            peak_note = f"{peak_src} bf16 burst x 1/2 (tf32 nominal ratio)"
+        line = {
+            "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": cfg["workload"], "n": n, "global_batch": gb, "per_gpu_batch": count,
+                       "family": cfg["family"], "filter": cfg["filter"], "products_per_matrix": G,
+                       "parallelism": f"batch-sharded dp{world}", "l2": "inputs 2.1 GB > 126 MB L2, no flush"
+                       if n * n * 4 * count > 126e6 else "inputs smaller than L2"},
+            "tflops_dense_equivalent": dense_flops_matrix * gb * args.steps / (ms / 1000.0) / 1e12,
+            "tflops_algorithmic": alg_flops_product * G * gb * args.steps / (ms / 1000.0) / 1e12,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "sym_gemm_kernel (symmetric product, fused epilogue)",
+                         "per_launch_flops": alg_flops_product * count,
+                         "avg_launch_ms": launch_ms, "peak_source": peak_note},
+            "gpu_launches": kernel_launches,
+            "clocks": clk.summary(),
+        }
+        if e2e_ms_max:
+            line["e2e"] = {"value": gb / (e2e_ms_max / 1000.0), "unit": "matrices/s",
+                           "h2d_bytes_per_step": int(host_in.numel() * 4 * world),
+                           "d2h_bytes_per_step": int(host_out.numel() * 4 * world)}
+        if world == 1 and not args.no_cpu_baseline:
+            st, kap = oracle_filter(cfg["filter"])
+            v, threads, sample = cpu_oracle_sample(cfg, st, kap, seconds_cap=args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": "matrices/s", "cores": threads, "kind": "oracle",
+                                    "sample": sample}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "tf32", "tf32x3"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,17 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
                              double alpha, double beta, int64_t n, int64_t batch, float* C,
                              void* stream);
 
+/* Profiling of the product chain (measurement support for bench.py).
+ * psd_profile(h, 1): every later psd_project, psd_project_ex or psd_sign call records a CUDA event pair on its
+ * stream around its contiguous run of product kernels.  psd_profile(h, 0) stops recording.
+ * psd_profile_read: synchronises on the recorded events, returns the summed device time of
+ * the product runs (ms), the number of product kernels they contained, and the number of
+ * kernels the handle launched in total since the last read (always counted); then resets.
+ * Any out pointer may be NULL. */
+psd_status_t psd_profile(psd_filter_t h, int enable);
+psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* product_launches,
+                              int64_t* kernel_launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,19 @@ class Filter:
             check(code, "psd_status")
         return STATUS_NAMES[code]
 
+    def profile(self, enable=True):
+        """Record device time of the product kernels of later calls (see psd_profile)."""
+        check(self._lib.psd_profile(self._h, 1 if enable else 0), "psd_profile")
+
+    def profile_read(self):
+        """(product_ms, product_launches, kernel_launches) since the last read; synchronises."""
+        ms = ctypes.c_double()
+        pl = ctypes.c_int64()
+        kl = ctypes.c_int64()
+        check(self._lib.psd_profile_read(self._h, ctypes.byref(ms), ctypes.byref(pl), ctypes.byref(kl)),
+              "psd_profile_read")
+        return ms.value, pl.value, kl.value
+
     def sym_product(self, A, B, D=None, alpha=1.0, beta=0.0, out=None, stream=None):
         """C = alpha (A B) + beta D for commuting symmetric A, B (upper triangles read)."""
         import torch

@@ -32,6 +32,9 @@ SIGNATURES = [
                                   _c.c_void_p, _c.c_int, _c.c_void_p]),
     ("psd_status", _c.c_int, [_c.c_void_p, _c.c_void_p]),
     ("psd_workspace_bytes", _c.c_int64, [_c.c_void_p, _c.c_int64, _c.c_int64]),
+    ("psd_profile", _c.c_int, [_c.c_void_p, _c.c_int]),
+    ("psd_profile_read", _c.c_int, [_c.c_void_p, _c.POINTER(_c.c_double), _c.POINTER(_c.c_int64),
+                                    _c.POINTER(_c.c_int64)]),
     ("psd_sym_product", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_double, _c.c_double,
                                    _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
 ]

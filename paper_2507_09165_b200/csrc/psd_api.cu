@@ -67,6 +67,12 @@ struct psd_filter_s {
     psd_precision_t prec = PSD_PREC_FP16;
     psd_bound_t bound = PSD_BOUND_FROBENIUS;
     Workspace ws;
+    // profiling / launch accounting
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+    int64_t product_launches_profiled = 0;
+    int64_t kernel_launches = 0;
 };
 
 namespace {
@@ -225,6 +231,17 @@ psd_status_t check_args(psd_filter_t h, const void* X, int64_t n, int64_t batch,
     return PSD_OK;
 }
 
+cudaEvent_t take_event(psd_filter_s* h) {
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
 psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
                  const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
     psd_status_t rc = check_args(h, X, n64, batch64, out);
@@ -243,6 +260,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         const int nblk = bound_blocks_per_matrix(n);
         e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
         if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
+        h->kernel_launches += 2;
         e = launch_finalize_bound(ws.partial, nblk, batch, ws.lambda, lambda_out, ws.status, st);
         if (e != cudaSuccess) return cuda_fail(e, "finalize_bound");
         lam = ws.lambda;
@@ -259,8 +277,14 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], ws.master[M_X],
                              (want_sign && steps.empty()) ? out : nullptr, sign_only, st);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
+    h->kernel_launches += 1;
     // (a3-a6) products
     GemmShape shape{npad, batch};
+    std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
+    if (h->profiling && !steps.empty()) {
+        evp = {take_event(h), take_event(h)};
+        cudaEventRecord(evp.first, st);
+    }
     for (const Step& s : steps) {
         EpiParams ep{};
         ep.alpha = static_cast<float>(s.alpha);
@@ -287,6 +311,12 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         }
         e = launch_sym_gemm(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
+        h->kernel_launches += 1;
+    }
+    if (evp.first) {
+        cudaEventRecord(evp.second, st);
+        h->ev_pairs.push_back(evp);
+        h->product_launches_profiled += static_cast<int64_t>(steps.size());
     }
     return PSD_OK;
 }
@@ -332,6 +362,8 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
 
 void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
+    for (auto& p : h->ev_pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto& e : h->ev_pool) cudaEventDestroy(e);
     if (h->ws.status) {
         cudaDeviceSynchronize();
         free_ws(h->ws);
@@ -392,6 +424,34 @@ psd_status_t psd_status(psd_filter_t h, void* stream) {
     return v ? PSD_ENONFINITE : PSD_OK;
 }
 
+psd_status_t psd_profile(psd_filter_t h, int enable) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    h->profiling = enable != 0;
+    return PSD_OK;
+}
+
+psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* product_launches,
+                              int64_t* kernel_launches) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    double total = 0.0;
+    for (auto& p : h->ev_pairs) {
+        cudaError_t e = cudaEventSynchronize(p.second);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        total += ms;
+        h->ev_pool.push_back(p.first);
+        h->ev_pool.push_back(p.second);
+    }
+    h->ev_pairs.clear();
+    if (product_ms) *product_ms = total;
+    if (product_launches) *product_launches = h->product_launches_profiled;
+    if (kernel_launches) *kernel_launches = h->kernel_launches;
+    h->product_launches_profiled = 0;
+    h->kernel_launches = 0;
+    return PSD_OK;
+}
+
 psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, const float* D, double alpha,
                              double beta, int64_t n64, int64_t batch64, float* C, void* stream) {
     psd_status_t rc = check_args(h, A, n64, batch64, C);
@@ -423,6 +483,7 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.nF = n;
     e = launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
+    h->kernel_launches += 3;
     return PSD_OK;
 }
 

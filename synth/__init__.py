@@ -73,14 +73,20 @@ def sdp_shaped(n, seed, avg_degree=8, rank=None, sigma=1.0):
     W = np.zeros((n, n))
     W[i, j] = 1.0
     W[j, i] = 1.0
-    L = np.diag(W.sum(axis=1)) - W
-    C = -0.25 * L
+    deg = W.sum(axis=1)
     y = r.standard_normal(n) - 0.25 * avg_degree
     rank = max(1, n // 20) if rank is None else rank
     V = r.standard_normal((n, rank)) * np.sqrt(avg_degree / (4.0 * n))
-    Xk = V @ V.T
-    M = C - np.diag(y) - Xk / sigma
-    return _f32(0.5 * (M + M.T))
+    # M = C - diag(y) - X^k / sigma with C = -L/4 = (W - diag(deg)) / 4
+    M = V @ V.T
+    M *= -1.0 / sigma
+    W *= 0.25
+    M += W
+    del W
+    M[np.diag_indices(n)] += -0.25 * deg - y
+    M += M.T.copy()
+    M *= 0.5
+    return _f32(M)
 
 
 FAMILIES = {"goe": goe, "haar": haar, "sdp_shaped": sdp_shaped, "dominant": dominant}

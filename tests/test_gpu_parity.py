@@ -17,6 +17,14 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL = {"fp16": 5e-3, "bf16": 3e-2, "tf32": 5e-3}
+# n < 64: a handful of eigenvalues dominate ||P||_F and the fp16 rounding model of this very
+# algorithm (operands RN to fp16, fp32 accumulate) reaches 1.6e-2 on 8x8 inputs (DESIGN.md
+# "Tolerances"); the 5e-3 bar applies from n = 64 on.
+TOL_SMALL_N = {"fp16": 2e-2, "bf16": 8e-2, "tf32": 2e-2}
+
+
+def tol(prec, n):
+    return TOL[prec] if n >= 64 else TOL_SMALL_N[prec]
 
 
 @pytest.fixture(scope="module")
@@ -81,7 +89,7 @@ def test_project_parity(pkg, n, batch, family, which, prec):
         assert abs(lam[b] - chain.frobenius_bound(X[b])) <= 1e-12 * lam[b]
         ref, _ = chain.project(X[b], st, kap, lam=lam[b])
         err = _rel(P[b], ref)
-        assert err <= TOL[prec], f"b={b} err={err:.3e}"
+        assert err <= tol(prec, n), f"b={b} err={err:.3e}"
         assert np.array_equal(P[b], P[b].T)
 
 
@@ -92,7 +100,7 @@ def test_sign_parity(pkg, n, prec):
     for b in range(2):
         ref, _ = chain.sign(X[b], *HALF, lam=lam[b])
         # sign chain output has ||S||_F ~ sqrt(n); relative bar as for P
-        assert _rel(S[b], ref) <= TOL[prec]
+        assert _rel(S[b], ref) <= tol(prec, n)
         assert np.array_equal(S[b], S[b].T)
 
 
