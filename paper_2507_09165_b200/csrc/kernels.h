@@ -43,6 +43,13 @@ bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, i
 cudaError_t launch_sym_gemm(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                             const GemmShape& s, const EpiParams& e, cudaStream_t stream);
 
+// Same product, persistent CTA-pair kernel with 256 x 256 tiles (npad multiple of 256).
+cudaError_t launch_sym_gemm_2cta(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                 const GemmShape& s, const EpiParams& e, cudaStream_t stream);
+// Whether (n, batch) runs on the CTA-pair kernel, and the padded size it needs.
+bool use_pair_kernel(int64_t n, int64_t batch);
+int64_t padded_n(int64_t n, int64_t batch);
+
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
 int bound_blocks_per_matrix(int n);

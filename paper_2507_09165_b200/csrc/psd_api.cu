@@ -54,7 +54,6 @@ struct Workspace {
     int nblk = 0;
 };
 
-int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 int op_bytes(OpType t) { return t == OpType::TF32 ? 4 : 2; }
 
@@ -248,7 +247,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     if (rc != PSD_OK) return rc;
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
     const int n = static_cast<int>(n64), batch = static_cast<int>(batch64);
-    const int npad = static_cast<int>(round_up(n, kPadTo));
+    const int npad = static_cast<int>(padded_n(n, batch));
     rc = ensure_ws(h, npad, batch);
     if (rc != PSD_OK) return rc;
     Workspace& ws = h->ws;
@@ -309,7 +308,9 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             ep.strideF = static_cast<int64_t>(n) * n;
             ep.nF = n;
         }
-        e = launch_sym_gemm(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st);
+        e = (npad % 256 == 0 && use_pair_kernel(n, batch))
+                ? launch_sym_gemm_2cta(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st)
+                : launch_sym_gemm(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
     }
@@ -394,7 +395,7 @@ int psd_filter_gemm_count(psd_filter_t h, int for_project) {
 
 int64_t psd_workspace_bytes(psd_filter_t h, int64_t n, int64_t batch) {
     if (!h || n < 1 || batch < 1) return -1;
-    return ws_bytes(op_of(h->prec), round_up(n, kPadTo), batch);
+    return ws_bytes(op_of(h->prec), padded_n(n, batch), batch);
 }
 
 psd_status_t psd_project(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out, void* stream) {
@@ -458,7 +459,7 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     if (rc != PSD_OK) return rc;
     if (!B) return fail(PSD_EINVAL, "null B");
     const int n = static_cast<int>(n64), batch = static_cast<int>(batch64);
-    const int npad = static_cast<int>(round_up(n, kPadTo));
+    const int npad = static_cast<int>(padded_n(n, batch));
     rc = ensure_ws(h, npad, batch);
     if (rc != PSD_OK) return rc;
     Workspace& ws = h->ws;
@@ -481,7 +482,9 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.ldF = n;
     ep.strideF = static_cast<int64_t>(n) * n;
     ep.nF = n;
-    e = launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st);
+    e = (npad % 256 == 0 && use_pair_kernel(n, batch))
+            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st)
+            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
     return PSD_OK;

@@ -14,36 +14,14 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "epilogue.cuh"
 #include "kernels.h"
+#include "optraits.cuh"
 #include "ptx.cuh"
 
 namespace psd {
 
 namespace {
-
-template <OpType T> struct OpTraits;
-template <> struct OpTraits<OpType::F16> {
-    using type = __half;
-    static constexpr int kBytes = 2;
-    static constexpr uint32_t kFmt = 0;
-    __device__ static type cvt(float v) { return __float2half_rn(v); }
-};
-template <> struct OpTraits<OpType::BF16> {
-    using type = __nv_bfloat16;
-    static constexpr int kBytes = 2;
-    static constexpr uint32_t kFmt = 1;
-    __device__ static type cvt(float v) { return __float2bfloat16_rn(v); }
-};
-template <> struct OpTraits<OpType::TF32> {
-    using type = float;
-    static constexpr int kBytes = 4;
-    static constexpr uint32_t kFmt = 2;
-    __device__ static type cvt(float v) {
-        uint32_t r;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-        return __uint_as_float(r);
-    }
-};
 
 constexpr int kStages = 4;
 constexpr int kThreads = 128;
@@ -64,7 +42,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
-    using op_t = typename Tr::type;
     constexpr int kBK = kBlockKBytes / Tr::kBytes;     // K elements per block (64 f16 / 32 tf32)
     constexpr int kUmmaK = 32 / Tr::kBytes;            // K per tcgen05.mma (16 f16 / 8 tf32)
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, kTile);
@@ -155,86 +132,13 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const bool diag = (I == J);
     float alpha = e.alpha;
     if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
-    const float beta = e.beta;
-    op_t* out_op = reinterpret_cast<op_t*>(e.out_op);
-    const int64_t opBase = static_cast<int64_t>(b) * s.npad * s.npad;
 
 #pragma unroll 1
     for (int c0 = 0; c0 < kTile; c0 += 32) {
         uint32_t raw[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
         ptx::tmem_ld_wait();
-        const int gj0 = J * kTile + c0;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
-        if (e.D) {
-            const float* drow = e.D + static_cast<int64_t>(b) * e.strideD + static_cast<int64_t>(gi) * e.ldD;
-            const bool row_ok = gi < e.nD;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                const bool ok = row_ok && gj < e.nD && gj >= gi;
-                v[i] += ok ? beta * drow[gj] : 0.0f;
-            }
-        }
-        // operand copy: direct (row gi) + transposed (row gj), mirrored
-        if (out_op) {
-            op_t* orow = out_op + opBase + static_cast<int64_t>(gi) * s.npad;
-            if (!diag) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
-                if constexpr (Tr::kBytes == 2) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint32_t w[4];
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            op_t lo = Tr::cvt(v[q * 8 + 2 * h]);
-                            op_t hi = Tr::cvt(v[q * 8 + 2 * h + 1]);
-                            w[h] = static_cast<uint32_t>(*reinterpret_cast<uint16_t*>(&lo)) |
-                                   (static_cast<uint32_t>(*reinterpret_cast<uint16_t*>(&hi)) << 16);
-                        }
-                        dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        dst[q] = make_uint4(__float_as_uint(Tr::cvt(v[4 * q])), __float_as_uint(Tr::cvt(v[4 * q + 1])),
-                                            __float_as_uint(Tr::cvt(v[4 * q + 2])), __float_as_uint(Tr::cvt(v[4 * q + 3])));
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                if (diag && gj < gi) continue;
-                const op_t cv = Tr::cvt(v[i]);
-                if (diag) orow[gj] = cv;
-                if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * s.npad + gi] = cv;
-            }
-        }
-        if (e.out32) {
-            float* mrow = e.out32 + opBase + static_cast<int64_t>(gi) * s.npad;
-            if (!diag) {
-                float4* dst = reinterpret_cast<float4*>(mrow + gj0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (gj0 + i >= gi) mrow[gj0 + i] = v[i];
-            }
-        }
-        if (e.outF && gi < e.nF) {
-            float* F = e.outF + static_cast<int64_t>(b) * e.strideF;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                if (gj >= e.nF || gj < gi) continue;     // upper part of this tile only
-                F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
-                if (gj != gi) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
-            }
-        }
+        epilogue_chunk<T>(e, alpha, b, s.npad, gi, J * kTile + c0, diag, raw);
     }
 
     ptx::tc_fence_before();

@@ -1,0 +1,236 @@
+// sym_gemm_2cta.cu -- persistent CTA-pair (cta_group::2) symmetric product for large n.
+//
+// Same product and epilogue as sym_gemm.cu (C = alpha A B + beta D over upper tiles,
+// mirrored stores; Algorithm 2's products), re-tiled for full tensor-core
+// rate on sm_100a:
+//   * a cluster of 2 CTAs (one TPC) owns a 256 x 256 upper output tile; tcgen05.mma
+//     .cta_group::2 with M = 256, N = 256, K = 16: CTA r holds A rows [r*128, r*128+128)
+//     and B^T rows [r*128, r*128+128) of the tile in its smem, and the accumulator rows
+//     [r*128, +128) x 256 columns in its TMEM -- half the operand bytes per CTA of a 1-SM
+//     tile of the same size (64 B/clk/SM of L2->SMEM traffic at full MMA rate);
+//   * persistent: grid = 2 x (#SMs / 2); cluster c walks tiles c, c + #clusters, ...;
+//   * warp roles: w0 TMA producer, w1 MMA issuer (leader CTA only), w2 TMEM allocator,
+//     w4..w7 epilogue (one TMEM lane quadrant each);
+//   * TMEM holds two 256-column fp32 accumulators (all 512 columns), so the epilogue of
+//     tile i overlaps the mainloop of tile i+1;
+//   * kStages-deep smem ring, 32 KB per stage per CTA (A 16 KB + B 16 KB, SW128 K-major).
+#include "epilogue.cuh"
+#include "kernels.h"
+#include "optraits.cuh"
+#include "ptx.cuh"
+
+namespace psd {
+
+namespace {
+
+constexpr int kT2 = 256;                       // output tile edge per CTA pair
+constexpr int kRowsPerCta = 128;
+constexpr int kStages2 = 6;
+constexpr int kThreads2 = 256;                 // 8 warps
+constexpr int kStageBytes = 2 * kRowsPerCta * kBlockKBytes;   // 32 KB (A + B half)
+constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512;
+constexpr uint32_t kTmemCols = 512;            // 2 accumulators x 256 fp32 columns
+
+__device__ __forceinline__ void decode_tile(int t, int nt, int tiles_per_matrix, int& b, int& I, int& J) {
+    b = t / tiles_per_matrix;
+    int rem = t - b * tiles_per_matrix;
+    int i = 0;
+    while (rem >= nt - i) { rem -= nt - i; ++i; }
+    I = i;
+    J = i + rem;
+}
+
+template <OpType T>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmShape s, const EpiParams e) {
+    using Tr = OpTraits<T>;
+    constexpr int kBK = kBlockKBytes / Tr::kBytes;
+    constexpr int kUmmaK = 32 / Tr::kBytes;
+    constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kT2, kT2);
+    constexpr int kTileBytes1 = kRowsPerCta * kBlockKBytes;   // 16 KB
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring = smem;                                       // stage st: A at +0, B at +16 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tmem_full = empty + kStages2;                     // [2]
+    uint64_t* tmem_empty = tmem_full + 2;                       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = (rank == 0);
+    const int cluster_id = blockIdx.x >> 1;
+    const int num_clusters = gridDim.x >> 1;
+    const int nt = s.npad / kT2;
+    const int tiles_per_matrix = nt * (nt + 1) / 2;
+    const int total_tiles = tiles_per_matrix * s.batch;
+    const int num_kb = s.npad / kBK;
+
+    if (warp == 0 && ptx::elect_one()) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int i = 0; i < kStages2; ++i) {
+            ptx::mbar_init(&full[i], 2);          // leader arrive.expect_tx + peer arrive
+            ptx::mbar_init(&empty[i], 1);         // one multicast MMA commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);     // one multicast MMA commit
+            ptx::mbar_init(&tmem_empty[i], 2 * 128);   // every epilogue thread of both CTAs
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (ptx::elect_one()) {
+            const uint64_t pol = ptx::policy_evict_last();
+            int st = 0;
+            uint32_t ph = 0;
+            for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+                int b, I, J;
+                decode_tile(t, nt, tiles_per_matrix, b, I, J);
+                const int rowA = b * s.npad + I * kT2 + rank * kRowsPerCta;
+                const int rowB = b * s.npad + J * kT2 + rank * kRowsPerCta;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[st], ph ^ 1);
+                    const uint32_t full_leader = ptx::mapa_shared(ptx::smem_u32(&full[st]), 0);
+                    uint8_t* sa = ring + st * kStageBytes;
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
+                    else ptx::mbar_arrive_remote(full_leader);
+                    ptx::tma_load_2d_pair(sa, &tmA, full_leader, kb * kBK, rowA, pol);
+                    ptx::tma_load_2d_pair(sa + kTileBytes1, &tmB, full_leader, kb * kBK, rowB, pol);
+                    if (++st == kStages2) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer (leader)
+        if (leader && ptx::elect_one()) {
+            int st = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_ph = (it >> 1) & 1;
+                ptx::mbar_wait_cluster(&tmem_empty[acc], acc_ph ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kT2;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait_cluster(&full[st], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
+                    const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
+                    const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + kTileBytes1);
+#pragma unroll
+                    for (int k = 0; k < kBK / kUmmaK; ++k) {
+                        const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
+                        if constexpr (T == OpType::TF32)
+                            ptx::mma_tf32_pair(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                        else
+                            ptx::mma_f16_pair(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                    }
+                    ptx::mma_commit_pair(&empty[st], 0x3);
+                    if (kb == num_kb - 1) ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                    if (++st == kStages2) { st = 0; ph ^= 1; }
+                }
+            }
+            // drain: the last commits must land before the pair tears down
+            if (it > 0) {
+                const int last = it - 1;
+                ptx::mbar_wait_cluster(&tmem_empty[last & 1], (last >> 1) & 1);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;                        // TMEM lane quadrant
+        const int r = q * 32 + lane;                   // row within this CTA's 128 rows
+        const uint32_t tmem_empty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[0]), 0);
+        const uint32_t tmem_empty_leader1 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[1]), 0);
+        int it = 0;
+        for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+            int b, I, J;
+            decode_tile(t, nt, tiles_per_matrix, b, I, J);
+            const int acc = it & 1;
+            ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
+            ptx::tc_fence_after();
+            const int gi = I * kT2 + rank * kRowsPerCta + r;
+            const bool diag = (I == J);
+            float alpha = e.alpha;
+            if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
+            const uint32_t tbase = tmem_base + acc * kT2 + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+            for (int c0 = 0; c0 < kT2; c0 += 32) {
+                const int gj0 = J * kT2 + c0;
+                // a 32-column chunk strictly below the diagonal for every lane of this warp: skip
+                if (diag && gj0 + 31 < I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32) continue;
+                uint32_t raw[32];
+                ptx::tmem_ld_32x32b_x32(tbase + c0, raw);
+                ptx::tmem_ld_wait();
+                epilogue_chunk<T>(e, alpha, b, s.npad, gi, gj0, diag, raw);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_remote(acc ? tmem_empty_leader1 : tmem_empty_leader0);
+        }
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair<kTmemCols>(tmem_base);
+    }
+}
+
+template <OpType T>
+cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s, const EpiParams& e,
+                      cudaStream_t stream) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_2cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+        if (err != cudaSuccess) return err;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int nt = s.npad / kT2;
+    const int total = nt * (nt + 1) / 2 * s.batch;
+    int clusters = num_sms / 2;
+    if (clusters > total) clusters = total;
+    sym_gemm_2cta_kernel<T><<<2 * clusters, kThreads2, kSmem2, stream>>>(tmA, tmB, s, e);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool use_pair_kernel(int64_t n, int64_t batch) {
+    const int64_t nt = (n + kT2 - 1) / kT2;
+    return n >= 1024 && nt * (nt + 1) / 2 * batch >= 74;
+}
+
+int64_t padded_n(int64_t n, int64_t batch) {
+    const int64_t m = use_pair_kernel(n, batch) ? kT2 : kTile;
+    return (n + m - 1) / m * m;
+}
+
+cudaError_t launch_sym_gemm_2cta(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s,
+                                 const EpiParams& e, cudaStream_t stream) {
+    switch (t) {
+        case OpType::F16: return launch2_t<OpType::F16>(tmA, tmB, s, e, stream);
+        case OpType::BF16: return launch2_t<OpType::BF16>(tmA, tmB, s, e, stream);
+        case OpType::TF32: return launch2_t<OpType::TF32>(tmA, tmB, s, e, stream);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace psd

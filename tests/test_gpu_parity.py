@@ -157,3 +157,41 @@ def test_psd_and_exact_projection_accuracy(pkg):
     P, lam, _ = _gpu(pkg, _product_filter("half", pkg), X, "fp16")
     err = spectral.rel_error(P[0], spectral.eig_project(X[0]))
     assert err < 5e-3
+
+
+@pytest.mark.parametrize("n,batch,family,prec", [
+    (1024, 8, "goe", "fp16"),          # 80 pair tiles: CTA-pair (cta_group::2) kernel
+    (2048, 3, "sdp_shaped", "fp16"),   # 108 pair tiles
+    (1280, 6, "haar", "bf16"),         # ragged for 256-tiles (1280 = 5 x 256), bf16
+    (1024, 8, "goe", "tf32"),
+])
+def test_pair_kernel_parity(pkg, n, batch, family, prec):
+    """Large-n path (persistent CTA-pair kernel, 256x256 tiles): sampled matrices vs oracle."""
+    X = synth.batch(family, n, batch, synth.SEED_BASE + 3 * n)
+    P, lam, f = _gpu(pkg, _product_filter("half", pkg), X, prec)
+    assert f.status() == "PSD_OK"
+    for b in sorted({0, batch - 1}):
+        ref, _ = chain.project(X[b], *HALF, lam=lam[b])
+        assert _rel(P[b], ref) <= tol(prec, n), (b, _rel(P[b], ref))
+    for b in range(batch):
+        assert np.array_equal(P[b], P[b].T)
+
+
+def test_c4_full_size_structured(pkg):
+    """Config c4 in bench.py's launch configuration (batch 32 x n=4096, fp16, f~*_half+kappa):
+    every output exactly symmetric; sampled outputs vs the exact structured oracle
+    P(H B H^T) = H P(B) H^T (oracle/spectral.py) with the GPU's lambda~."""
+    n, batch = 4096, 32
+    mats, blocks = [], []
+    for b in range(batch):
+        Xb, bl = synth.structured(n, synth.SEED_BASE + 17 * b, block=64, family="goe" if b % 2 else "sdp_shaped")
+        mats.append(Xb)
+        blocks.append(bl)
+    X = np.stack(mats)
+    P, lam, f = _gpu(pkg, _product_filter("half", pkg), X, "fp16")
+    assert f.status() == "PSD_OK"
+    for b in range(batch):
+        assert np.array_equal(P[b], P[b].T)
+    for b in [0, 1, 17, 31]:
+        ref = spectral.structured_project(blocks[b], *HALF, lam[b])
+        assert _rel(P[b], ref) <= TOL["fp16"], (b, _rel(P[b], ref))
