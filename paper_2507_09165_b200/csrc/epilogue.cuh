@@ -1,31 +1,77 @@
 // epilogue.cuh -- fused symmetric epilogue shared by the product kernels.
 //
-// One thread owns one output row gi of an upper tile (I <= J) and processes 32 consecutive
-// accumulator columns gj0..gj0+31 at a time (one tcgen05.ld 32x32b.x32):
-//     v = alpha * acc + beta * D[gi][gj]          (D: fp32 master / input, upper triangle)
-//     operand copy  : out_op[gi][gj] = v and out_op[gj][gi] = v   (mirrored, exact symmetry)
-//     fp32 master   : out32[gi][gj] = v                            (upper part only)
-//     final output  : outF[gi][gj] = outF[gj][gi] = v              (masked to n)
-// On a diagonal tile only gj >= gi is valid; the mirror provides the rest.  This is where
-// the polynomial's axpy terms (c_j Y, c_0 X) and the reconstruction 1/2 X + 1/2 lambda~ X_0 S
-// of Algorithm 2 are fused: no separate elementwise pass touches HBM.
+// One warp owns 32 consecutive output rows gi0..gi0+31 of an upper tile (I <= J); lane l
+// holds row gi = gi0 + l and processes 32 accumulator columns gj0..gj0+31 at a time (one
+// tcgen05.ld 32x32b.x32):
+//     v = alpha * acc + beta * D[gi][gj]         D: the operand-precision copy of the addend
+//                                                (Z or Y, upper triangle) or, for the
+//                                                reconstruction, the fp32 input X
+//     operand copy: out_op[gi][gj] = out_op[gj][gi] = v   (mirrored -> exactly symmetric)
+//     final output: outF[gi][gj]  = outF[gj][gi]  = v     (fp32, masked to n)
+// The mirrored half goes through a per-warp 32x32 smem transpose so that both halves are
+// written as 16-byte row segments.  On a diagonal tile only gj >= gi is valid (scalar path).
+// This is where the polynomial's axpy terms (c_j Y, c_0 Z) and the reconstruction
+// 1/2 X + 1/2 lambda~ X_0 S of Algorithm 2 are fused: no separate
+// elementwise pass touches HBM.
 #pragma once
 #include "kernels.h"
 #include "optraits.cuh"
 
 namespace psd {
 
+// per-warp staging: 32 rows x (32 + 4) fp32 words (row stride 144 B keeps LDS.128 of
+// 8-lane phases conflict-free); reused as 32 x 40 fp16 (row stride 80 B)
+constexpr int kEpiWarpSmemBytes = 32 * 36 * 4;
+
 template <OpType T>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi, int gj0,
-                                               bool diag, const uint32_t (&raw)[32]) {
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
+                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
+    const int lane = threadIdx.x & 31;
+    const int gi = gi0 + lane;
+    const int64_t opBase = static_cast<int64_t>(b) * npad * npad;
     float v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
-    if (e.D) {
-        const float* drow = e.D + static_cast<int64_t>(b) * e.strideD + static_cast<int64_t>(gi) * e.ldD;
-        if (!diag && gi < e.nD && gj0 + 32 <= e.nD && (e.ldD & 3) == 0) {
+
+    if (e.Dop) {                                     // addend in operand precision, ld npad
+        const op_t* drow = reinterpret_cast<const op_t*>(e.Dop) + opBase + static_cast<int64_t>(gi) * npad;
+        if (!diag) {
+            if constexpr (Tr::kBytes == 2) {
+                const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 d = d4[q];
+                    const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        float lo, hi;
+                        Tr::unpack2(w[h], lo, hi);
+                        v[q * 8 + 2 * h] += e.beta * lo;
+                        v[q * 8 + 2 * h + 1] += e.beta * hi;
+                    }
+                }
+            } else {
+                const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 d = d4[q];
+                    v[4 * q] += e.beta * d.x;
+                    v[4 * q + 1] += e.beta * d.y;
+                    v[4 * q + 2] += e.beta * d.z;
+                    v[4 * q + 3] += e.beta * d.w;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (gj0 + i >= gi) v[i] += e.beta * Tr::to_float(drow[gj0 + i]);
+        }
+    }
+    if (e.Df) {                                      // fp32 addend (the input X), masked to nDf
+        const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
+        if (!diag && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
             const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -36,22 +82,22 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 v[4 * q + 3] += e.beta * d.w;
             }
         } else {
-            const bool row_ok = gi < e.nD;
+            const bool row_ok = gi < e.nDf;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int gj = gj0 + i;
-                const bool ok = row_ok && gj < e.nD && gj >= gi;
-                v[i] += ok ? e.beta * drow[gj] : 0.0f;
+                v[i] += (row_ok && gj < e.nDf && gj >= gi) ? e.beta * drow[gj] : 0.0f;
             }
         }
     }
-    const int64_t opBase = static_cast<int64_t>(b) * npad * npad;
+
     if (e.out_op) {
         op_t* out_op = reinterpret_cast<op_t*>(e.out_op);
         op_t* orow = out_op + opBase + static_cast<int64_t>(gi) * npad;
         if (!diag) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
+            // direct half: 32 contiguous elements of row gi
             if constexpr (Tr::kBytes == 2) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint32_t w[4];
@@ -59,42 +105,71 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                     for (int h = 0; h < 4; ++h) w[h] = Tr::pack2(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
                     dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
                 }
+                // mirrored half: transpose the warp's 32x32 block through smem (row stride 80 B)
+                uint16_t* S = reinterpret_cast<uint16_t*>(wsmem);
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const op_t cv = Tr::cvt(v[c]);
+                    S[c * 40 + lane] = *reinterpret_cast<const uint16_t*>(&cv);
+                }
+                __syncwarp();
+                const uint4* src = reinterpret_cast<const uint4*>(S + lane * 40);
+                uint4* tdst = reinterpret_cast<uint4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tdst[q] = src[q];
             } else {
+                float4* dst = reinterpret_cast<float4*>(orow + gj0);
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
-                    dst[q] = make_uint4(__float_as_uint(Tr::cvt(v[4 * q])), __float_as_uint(Tr::cvt(v[4 * q + 1])),
-                                        __float_as_uint(Tr::cvt(v[4 * q + 2])), __float_as_uint(Tr::cvt(v[4 * q + 3])));
+                    dst[q] = make_float4(Tr::cvt(v[4 * q]), Tr::cvt(v[4 * q + 1]), Tr::cvt(v[4 * q + 2]),
+                                         Tr::cvt(v[4 * q + 3]));
+                float* S = reinterpret_cast<float*>(wsmem);
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) S[c * 36 + lane] = Tr::cvt(v[c]);
+                __syncwarp();
+                const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+                float4* tdst = reinterpret_cast<float4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) tdst[q] = src[q];
             }
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int gj = gj0 + i;
-            if (diag && gj < gi) continue;
-            const op_t cv = Tr::cvt(v[i]);
-            if (diag) orow[gj] = cv;
-            if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * npad + gi] = cv;
-        }
-    }
-    if (e.out32) {
-        float* mrow = e.out32 + opBase + static_cast<int64_t>(gi) * npad;
-        if (!diag) {
-            float4* dst = reinterpret_cast<float4*>(mrow + gj0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (gj0 + i >= gi) mrow[gj0 + i] = v[i];
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                if (gj < gi) continue;
+                const op_t cv = Tr::cvt(v[i]);
+                orow[gj] = cv;
+                if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * npad + gi] = cv;
+            }
         }
     }
-    if (e.outF && gi < e.nF) {
+
+    if (e.outF) {
         float* F = e.outF + static_cast<int64_t>(b) * e.strideF;
+        const bool fast = !diag && (e.ldF & 3) == 0 && gi0 + 32 <= e.nF && gj0 + 32 <= e.nF;
+        if (fast) {
+            float4* dst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gi) * e.ldF + gj0);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int gj = gj0 + i;
-            if (gj >= e.nF || gj < gi) continue;     // upper part of this tile only
-            F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
-            if (gj != gi) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
+            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            float* S = reinterpret_cast<float*>(wsmem);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
+            __syncwarp();
+            const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+            float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * e.ldF + gi0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tdst[q] = src[q];
+        } else if (gi < e.nF) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                if (gj >= e.nF || gj < gi) continue;     // upper part of this tile only
+                F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
+                if (gj != gi) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
+            }
         }
     }
 }

@@ -21,11 +21,11 @@ struct EpiParams {
     float alpha;              // host factor
     const double* alpha_dev;  // optional per-matrix factor (lambda~), multiplies alpha
     float beta;
-    const float* D;           // optional fp32 addend, upper triangle read
-    int64_t ldD, strideD;     // row stride / matrix stride (elements)
-    int nD;                   // rows/cols of D that exist (mask)
+    const void* Dop;          // optional addend in operand precision, upper triangle, ld npad
+    const float* Df;          // optional fp32 addend (the input X), upper triangle read
+    int64_t ldDf, strideDf;   // row stride / matrix stride (elements)
+    int nDf;                  // rows/cols of Df that exist (mask)
     void* out_op;             // operand-precision copy, full mirrored, ld = npad (or NULL)
-    float* out32;             // fp32 master, upper tiles only, ld = npad (or NULL)
     float* outF;              // final fp32 output, full mirrored, masked to nF (or NULL)
     int64_t ldF, strideF;
     int nF;

@@ -28,17 +28,16 @@ psd_status_t cuda_fail(cudaError_t e, const char* where) {
 
 // Operand buffers of the chain (operand precision, full mirrored, [batch][npad][npad]).
 enum Buf { B_XA = 0, B_XB, B_X0, B_Y, B_UA, B_UB, B_COUNT };
-// fp32 master buffers (upper tiles) and addend sources.
-enum Master { M_NONE = -1, M_X = 0, M_Y = 1, M_XIN = 2, M_USER = 3 };
+// Addend sources: an operand buffer (>= 0), none, or the fp32 input X.
+enum Addend { D_NONE = -1, D_XIN = -2 };
 
 struct Step {
     int A, B;            // operand buffers
     double alpha;        // host factor
     bool alpha_lambda;   // multiply alpha by lambda~[b] on the device
     double beta;
-    int D;               // Master id of the addend (M_NONE: none)
+    int D;               // addend: operand buffer id, D_NONE or D_XIN
     int out_op;          // operand buffer written (-1: none)
-    int out32;           // master written (M_NONE / M_X / M_Y)
     bool outF;           // final fp32 output
 };
 
@@ -46,7 +45,6 @@ struct Workspace {
     int npad = 0, batch = 0;
     OpType op = OpType::F16;
     void* op_buf[B_COUNT] = {};
-    float* master[2] = {};
     double* partial = nullptr;
     double* lambda = nullptr;
     unsigned* status = nullptr;
@@ -86,7 +84,6 @@ OpType op_of(psd_precision_t p) {
 
 void free_ws(Workspace& ws) {
     for (auto& p : ws.op_buf) { if (p) cudaFree(p); p = nullptr; }
-    for (auto& p : ws.master) { if (p) cudaFree(p); p = nullptr; }
     if (ws.partial) cudaFree(ws.partial);
     if (ws.lambda) cudaFree(ws.lambda);
     if (ws.status) cudaFree(ws.status);
@@ -98,7 +95,7 @@ void free_ws(Workspace& ws) {
 
 int64_t ws_bytes(OpType op, int64_t npad, int64_t batch) {
     const int64_t mat = npad * npad * batch;
-    return B_COUNT * mat * op_bytes(op) + 2 * mat * 4 + batch * 256 * 8 + batch * 8 + 64;
+    return B_COUNT * mat * op_bytes(op) + batch * 256 * 8 + batch * 8 + 64;
 }
 
 psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
@@ -117,12 +114,6 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
             return fail(PSD_ENOMEM, "cudaMalloc operand workspace failed");
         }
     }
-    for (int i = 0; i < 2; ++i) {
-        if (cudaMalloc(&ws.master[i], mat * 4) != cudaSuccess) {
-            free_ws(ws);
-            return fail(PSD_ENOMEM, "cudaMalloc master workspace failed");
-        }
-    }
     ws.nblk = 256;
     if (cudaMalloc(&ws.partial, static_cast<size_t>(batch) * ws.nblk * 8) != cudaSuccess ||
         cudaMalloc(&ws.lambda, static_cast<size_t>(batch) * 8) != cudaSuccess ||
@@ -131,9 +122,8 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
         return fail(PSD_ENOMEM, "cudaMalloc small workspace failed");
     }
     cudaMemset(ws.status, 0, 64);
-    // Zero everything once: padded rows/cols of every operand and master must read as 0.
+    // Zero everything once: padded rows/cols of every operand buffer must read as 0.
     for (int i = 0; i < B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
-    for (int i = 0; i < 2; ++i) cudaMemset(ws.master[i], 0, mat * 4);
     for (int i = 0; i < B_COUNT; ++i) {
         if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch)) {
             free_ws(ws);
@@ -152,11 +142,14 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
 }
 
 // Algorithm 2's loop + return line as fused products.
-// Stage t with coefficients c_0..c_p (p >= 1), iterate Z (buffer `cur`, master M_X):
-//   Y = Z Z                                   -> Y op + Y master
+// Stage t with coefficients c_0..c_p (p >= 1) on the iterate Z (operand buffer `cur`):
+//   Y = Z Z
 //   p == 1: Z' = c_0 Z + c_1 (Z Y)
 //   p >= 2: U  = c_p (Y Y) + c_{p-1} Y ;  U <- Y U + c_j Y (j = p-2..1) ;  Z' = c_0 Z + Z U
-// (identity-free Horner in Y = Z^2: no c*I term ever enters a low-precision operand).
+// (identity-free Horner in Y = Z^2: no c*I term ever enters a low-precision operand).  The
+// addends c_j Y and c_0 Z are read from the SAME rounded operand copies the tensor cores
+// multiply, so every stage is exactly f_t of one rounded Z (DESIGN.md "consistent rounding":
+// fp32 masters of Z, Y measured 2x less accurate in the rounding model).
 // Degree-1 stages (p = 0) and trailing scalars are carried as a pending factor s and
 // folded into the next products (f(sZ) = sum c_j s^{2j+1} Z^{2j+1}).
 std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign_only_scale) {
@@ -178,25 +171,24 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
         s = 1.0;
         const int nxt = (cur == B_XA) ? B_XB : B_XA;
         const bool last = (t == last_gemm_stage);
-        steps.push_back({cur, cur, 1.0, false, 0.0, M_NONE, B_Y, M_Y, false});
+        steps.push_back({cur, cur, 1.0, false, 0.0, D_NONE, B_Y, false});
         Step fin;
         if (p == 1) {
-            fin = {cur, B_Y, cs[1], false, cs[0], M_X, nxt, M_X, false};
+            fin = {cur, B_Y, cs[1], false, cs[0], cur, nxt, false};
         } else {
             int u = B_UA;
-            steps.push_back({B_Y, B_Y, cs[p], false, cs[p - 1], M_Y, u, M_NONE, false});
+            steps.push_back({B_Y, B_Y, cs[p], false, cs[p - 1], B_Y, u, false});
             for (int j = p - 2; j >= 1; --j) {
                 const int un = (u == B_UA) ? B_UB : B_UA;
-                steps.push_back({B_Y, u, 1.0, false, cs[j], M_Y, un, M_NONE, false});
+                steps.push_back({B_Y, u, 1.0, false, cs[j], B_Y, un, false});
                 u = un;
             }
-            fin = {cur, u, 1.0, false, cs[0], M_X, nxt, M_X, false};
+            fin = {cur, u, 1.0, false, cs[0], cur, nxt, false};
         }
         if (last && want_sign) {
             fin.alpha *= trailing;
             fin.beta *= trailing;
             fin.out_op = -1;
-            fin.out32 = M_NONE;
             fin.outF = true;
         }
         steps.push_back(fin);
@@ -208,13 +200,13 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
         if (want_sign) {
             *sign_only_scale = trailing;
         } else {
-            steps.push_back({B_X0, B_X0, 0.5 * trailing, true, 0.5, M_XIN, -1, M_NONE, true});
+            steps.push_back({B_X0, B_X0, 0.5 * trailing, true, 0.5, D_XIN, -1, true});
         }
         return steps;
     }
     if (!want_sign) {
         // P = 1/2 X + 1/2 lambda~ (X_0 S)  ==  lambda~ 1/2 X_0 (I + X_T)   (reading R5)
-        steps.push_back({B_X0, cur, 0.5 * trailing, true, 0.5, M_XIN, -1, M_NONE, true});
+        steps.push_back({B_X0, cur, 0.5 * trailing, true, 0.5, D_XIN, -1, true});
     }
     return steps;
 }
@@ -273,7 +265,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     double sign_only = 0.0;
     std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
     // (a2) scale + convert; the products-free sign chain finishes here
-    e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], ws.master[M_X],
+    e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr,
                              (want_sign && steps.empty()) ? out : nullptr, sign_only, st);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
@@ -289,19 +281,15 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         ep.alpha = static_cast<float>(s.alpha);
         ep.alpha_dev = s.alpha_lambda ? lam : nullptr;
         ep.beta = static_cast<float>(s.beta);
-        if (s.D == M_X || s.D == M_Y) {
-            ep.D = ws.master[s.D];
-            ep.ldD = npad;
-            ep.strideD = static_cast<int64_t>(npad) * npad;
-            ep.nD = npad;
-        } else if (s.D == M_XIN) {
-            ep.D = X;
-            ep.ldD = n;
-            ep.strideD = static_cast<int64_t>(n) * n;
-            ep.nD = n;
+        if (s.D >= 0) {
+            ep.Dop = ws.op_buf[s.D];
+        } else if (s.D == D_XIN) {
+            ep.Df = X;
+            ep.ldDf = n;
+            ep.strideDf = static_cast<int64_t>(n) * n;
+            ep.nDf = n;
         }
         ep.out_op = s.out_op >= 0 ? ws.op_buf[s.out_op] : nullptr;
-        ep.out32 = (s.out32 == M_X || s.out32 == M_Y) ? ws.master[s.out32] : nullptr;
         if (s.outF) {
             ep.outF = out;
             ep.ldF = n;
@@ -473,10 +461,10 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.alpha = static_cast<float>(alpha);
     ep.beta = static_cast<float>(beta);
     if (D) {
-        ep.D = D;
-        ep.ldD = n;
-        ep.strideD = static_cast<int64_t>(n) * n;
-        ep.nD = n;
+        ep.Df = D;
+        ep.ldDf = n;
+        ep.strideDf = static_cast<int64_t>(n) * n;
+        ep.nDf = n;
     }
     ep.outF = C;
     ep.ldF = n;

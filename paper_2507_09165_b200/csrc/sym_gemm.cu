@@ -26,7 +26,7 @@ namespace {
 constexpr int kStages = 4;
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTile * kBlockKBytes;                 // 16 KB per operand tile
-constexpr int kSmemBytes = 2 * kStages * kTileBytes + 1024 + 256; // ring + align slack + barriers
+constexpr int kSmemBytes = 2 * kStages * kTileBytes + 1024 + 256 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers, staging
 
 __device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J) {
     // row-major enumeration of {(I, J): 0 <= I <= J < nt}
@@ -54,9 +54,9 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint64_t* empty = full + kStages;
     uint64_t* accum_full = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+    uint8_t* epi_smem = smem + 2 * kStages * kTileBytes + 256;     // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
     const int nt = s.npad / kTile;
     const int b = blockIdx.y;
     int I, J;
@@ -127,18 +127,20 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     ptx::mbar_wait(accum_full, 0);
     ptx::tc_fence_after();
 
-    const int r = warp * 32 + lane;                 // tile row == TMEM lane
-    const int gi = I * kTile + r;                   // global row
+    const int gi0 = I * kTile + warp * 32;          // this warp's first row (TMEM lanes 32w..)
     const bool diag = (I == J);
     float alpha = e.alpha;
     if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
+    uint8_t* wsmem = epi_smem + warp * kEpiWarpSmemBytes;
 
 #pragma unroll 1
     for (int c0 = 0; c0 < kTile; c0 += 32) {
+        const int gj0 = J * kTile + c0;
+        if (diag && gj0 + 31 < gi0) continue;       // chunk below the diagonal for the whole warp
         uint32_t raw[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
         ptx::tmem_ld_wait();
-        epilogue_chunk<T>(e, alpha, b, s.npad, gi, J * kTile + c0, diag, raw);
+        epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
     }
 
     ptx::tc_fence_before();

@@ -28,7 +28,7 @@ constexpr int kRowsPerCta = 128;
 constexpr int kStages2 = 6;
 constexpr int kThreads2 = 256;                 // 8 warps
 constexpr int kStageBytes = 2 * kRowsPerCta * kBlockKBytes;   // 32 KB (A + B half)
-constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512;
+constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;
 constexpr uint32_t kTmemCols = 512;            // 2 accumulators x 256 fp32 columns
 
 __device__ __forceinline__ void decode_tile(int t, int nt, int tiles_per_matrix, int& b, int& I, int& J) {
@@ -58,9 +58,9 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint64_t* tmem_full = empty + kStages2;                     // [2]
     uint64_t* tmem_empty = tmem_full + 2;                       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint8_t* epi_smem = smem + kStages2 * kStageBytes + 512;    // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = (rank == 0);
     const int cluster_id = blockIdx.x >> 1;
@@ -122,11 +122,11 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_ph = (it >> 1) & 1;
-                ptx::mbar_wait_cluster(&tmem_empty[acc], acc_ph ^ 1);
+                ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kT2;
                 for (int kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait_cluster(&full[st], ph);
+                    ptx::mbar_wait(&full[st], ph);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
                     const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
@@ -147,14 +147,14 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             // drain: the last commits must land before the pair tears down
             if (it > 0) {
                 const int last = it - 1;
-                ptx::mbar_wait_cluster(&tmem_empty[last & 1], (last >> 1) & 1);
+                ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
             }
         }
         __syncwarp();
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;                        // TMEM lane quadrant
-        const int r = q * 32 + lane;                   // row within this CTA's 128 rows
+        uint8_t* wsmem = epi_smem + q * kEpiWarpSmemBytes;
         const uint32_t tmem_empty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[0]), 0);
         const uint32_t tmem_empty_leader1 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[1]), 0);
         int it = 0;
@@ -164,7 +164,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             const int acc = it & 1;
             ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
             ptx::tc_fence_after();
-            const int gi = I * kT2 + rank * kRowsPerCta + r;
+            const int gi0 = I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32;
             const bool diag = (I == J);
             float alpha = e.alpha;
             if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
@@ -172,12 +172,11 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 #pragma unroll 1
             for (int c0 = 0; c0 < kT2; c0 += 32) {
                 const int gj0 = J * kT2 + c0;
-                // a 32-column chunk strictly below the diagonal for every lane of this warp: skip
-                if (diag && gj0 + 31 < I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32) continue;
+                if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
                 uint32_t raw[32];
                 ptx::tmem_ld_32x32b_x32(tbase + c0, raw);
                 ptx::tmem_ld_wait();
-                epilogue_chunk<T>(e, alpha, b, s.npad, gi, gj0, diag, raw);
+                epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive_remote(acc ? tmem_empty_leader1 : tmem_empty_leader0);
