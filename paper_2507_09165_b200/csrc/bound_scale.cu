@@ -81,7 +81,7 @@ template <> struct Cvt<OpType::TF32> {
     }
 };
 
-constexpr int kST = 32;   // scale tile
+constexpr int kST = 64;   // scale tile (64 x 64, 256 threads)
 
 __device__ __forceinline__ void upper_coords(int t, int nt, int& I, int& J) {
     // closed form for row-major upper-triangle enumeration, with a fix-up step
@@ -94,8 +94,11 @@ __device__ __forceinline__ void upper_coords(int t, int nt, int& I, int& J) {
     J = i + (t - start(i));
 }
 
+// One block per upper 64x64 tile pair (I <= J) of the padded matrix: reads tile (I, J) of X
+// once (upper triangle; on a diagonal tile the lower half mirrors the upper), writes the
+// operand copy of tiles (I, J) and (J, I), zero in the padding.
 template <OpType T>
-__global__ void __launch_bounds__(kST * 8)
+__global__ void __launch_bounds__(256)
 scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double* __restrict__ lambda,
                      double scale, typename Cvt<T>::type* __restrict__ out_op, float* __restrict__ out32,
                      float* __restrict__ outF, double post) {
@@ -105,7 +108,7 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
     const int ntile = npad / kST;
     int I, J;
     upper_coords(blockIdx.x, ntile, I, J);
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tid = threadIdx.x;
     const float* Xb = X + static_cast<int64_t>(b) * n * n;
 
     double inv = scale;
@@ -113,32 +116,65 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
         const double lam = lambda[b];
         inv = (lam > 0.0) ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);   // NaN stays NaN; 0 -> zeros
     }
-    for (int r = ty; r < kST; r += 8) {
-        const int gi = I * kST + r, gj = J * kST + tx;
-        float x = 0.0f;
-        if (gi < n && gj < n) x = Xb[static_cast<int64_t>(gi) * n + gj];
-        S[r][tx] = static_cast<float>(static_cast<double>(x) * inv);
+    const int r0 = I * kST, c0 = J * kST;
+    if ((n & 3) == 0 && r0 + kST <= n && c0 + kST <= n) {
+        // 64 rows x 16 float4; 4 per thread, coalesced
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int idx = tid + 256 * k;
+            const int r = idx >> 4, q = idx & 15;
+            const float4 x = __ldcs(reinterpret_cast<const float4*>(Xb + static_cast<int64_t>(r0 + r) * n + c0) + q);
+            S[r][4 * q] = static_cast<float>(static_cast<double>(x.x) * inv);
+            S[r][4 * q + 1] = static_cast<float>(static_cast<double>(x.y) * inv);
+            S[r][4 * q + 2] = static_cast<float>(static_cast<double>(x.z) * inv);
+            S[r][4 * q + 3] = static_cast<float>(static_cast<double>(x.w) * inv);
+        }
+    } else {
+        for (int idx = tid; idx < kST * kST; idx += 256) {
+            const int r = idx >> 6, c = idx & 63;
+            const int gi = r0 + r, gj = c0 + c;
+            const float x = (gi < n && gj < n) ? Xb[static_cast<int64_t>(gi) * n + gj] : 0.0f;
+            S[r][c] = static_cast<float>(static_cast<double>(x) * inv);
+        }
     }
     __syncthreads();
     const int64_t base = static_cast<int64_t>(b) * npad * npad;
-    for (int r = ty; r < kST; r += 8) {
-        // direct tile (I, J): element (r, tx); on the diagonal tile the lower half mirrors
-        const float vd = (I == J && tx < r) ? S[tx][r] : S[r][tx];
-        const int64_t od = base + static_cast<int64_t>(I * kST + r) * npad + J * kST + tx;
-        if (out_op) out_op[od] = Cvt<T>::f(vd);
-        if (out32) out32[od] = vd;
-        // transposed tile (J, I): element (r, tx) = S[tx][r]
-        if (I != J) {
-            const float vt = S[tx][r];
-            const int64_t ot = base + static_cast<int64_t>(J * kST + r) * npad + I * kST + tx;
-            if (out_op) out_op[ot] = Cvt<T>::f(vt);
+    // each thread: one row segment of 16 elements of the direct tile and of the mirrored tile
+    const int r = tid >> 2, cs = (tid & 3) * 16;
+    if (out_op) {
+        __align__(16) op_t vd[16];
+        __align__(16) op_t vt[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int c = cs + i;
+            vd[i] = Cvt<T>::f((I == J && c < r) ? S[c][r] : S[r][c]);
+            vt[i] = Cvt<T>::f(S[c][r]);
         }
-        if (outF) {
-            float* F = outF + static_cast<int64_t>(b) * n * n;
-            const int gi = I * kST + r, gj = J * kST + tx;
+        constexpr int kVec = 16 / sizeof(op_t);   // elements per 16-byte store
+        uint4* od = reinterpret_cast<uint4*>(out_op + base + static_cast<int64_t>(r0 + r) * npad + c0 + cs);
+#pragma unroll
+        for (int q = 0; q < 16 / kVec; ++q) od[q] = *reinterpret_cast<const uint4*>(vd + q * kVec);
+        if (I != J) {
+            uint4* ot = reinterpret_cast<uint4*>(out_op + base + static_cast<int64_t>(c0 + r) * npad + r0 + cs);
+#pragma unroll
+            for (int q = 0; q < 16 / kVec; ++q) ot[q] = *reinterpret_cast<const uint4*>(vt + q * kVec);
+        }
+    }
+    if (out32) {
+        for (int i = 0; i < 16; ++i) {
+            const int c = cs + i;
+            out32[base + static_cast<int64_t>(r0 + r) * npad + c0 + c] = (I == J && c < r) ? S[c][r] : S[r][c];
+        }
+    }
+    if (outF) {
+        float* F = outF + static_cast<int64_t>(b) * n * n;
+        for (int i = 0; i < 16; ++i) {
+            const int c = cs + i;
+            const float vd = (I == J && c < r) ? S[c][r] : S[r][c];
+            const int gi = r0 + r, gj = c0 + c;
             if (gi < n && gj < n) F[static_cast<int64_t>(gi) * n + gj] = static_cast<float>(vd * post);
-            const int ti = J * kST + r, tj = I * kST + tx;
-            if (I != J && ti < n && tj < n) F[static_cast<int64_t>(ti) * n + tj] = static_cast<float>(S[tx][r] * post);
+            const int ti = c0 + r, tj = r0 + c;
+            if (I != J && ti < n && tj < n) F[static_cast<int64_t>(ti) * n + tj] = static_cast<float>(S[c][r] * post);
         }
     }
 }
@@ -170,15 +206,15 @@ cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int 
     dim3 grid(nt * (nt + 1) / 2, batch);
     switch (t) {
         case OpType::F16:
-            scale_convert_kernel<OpType::F16><<<grid, kST * 8, 0, stream>>>(
+            scale_convert_kernel<OpType::F16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__half*>(out_op), out32, outF, post);
             break;
         case OpType::BF16:
-            scale_convert_kernel<OpType::BF16><<<grid, kST * 8, 0, stream>>>(
+            scale_convert_kernel<OpType::BF16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__nv_bfloat16*>(out_op), out32, outF, post);
             break;
         case OpType::TF32:
-            scale_convert_kernel<OpType::TF32><<<grid, kST * 8, 0, stream>>>(
+            scale_convert_kernel<OpType::TF32><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<float*>(out_op), out32, outF, post);
             break;
     }

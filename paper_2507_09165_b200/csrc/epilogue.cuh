@@ -42,7 +42,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 d = d4[q];
+                    const uint4 d = __ldcs(d4 + q);
                     const uint32_t w[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
@@ -56,7 +56,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const float4 d = d4[q];
+                    const float4 d = __ldcs(d4 + q);
                     v[4 * q] += e.beta * d.x;
                     v[4 * q + 1] += e.beta * d.y;
                     v[4 * q + 2] += e.beta * d.z;
@@ -75,7 +75,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const float4 d = d4[q];
+                const float4 d = __ldcs(d4 + q);
                 v[4 * q] += e.beta * d.x;
                 v[4 * q + 1] += e.beta * d.y;
                 v[4 * q + 2] += e.beta * d.z;
@@ -103,7 +103,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                     uint32_t w[4];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) w[h] = Tr::pack2(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
-                    dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+                    __stcs(dst + q, make_uint4(w[0], w[1], w[2], w[3]));
                 }
                 // mirrored half: transpose the warp's 32x32 block through smem (row stride 80 B)
                 uint16_t* S = reinterpret_cast<uint16_t*>(wsmem);
@@ -117,13 +117,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const uint4* src = reinterpret_cast<const uint4*>(S + lane * 40);
                 uint4* tdst = reinterpret_cast<uint4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) tdst[q] = src[q];
+                for (int q = 0; q < 4; ++q) __stcs(tdst + q, src[q]);
             } else {
                 float4* dst = reinterpret_cast<float4*>(orow + gj0);
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
-                    dst[q] = make_float4(Tr::cvt(v[4 * q]), Tr::cvt(v[4 * q + 1]), Tr::cvt(v[4 * q + 2]),
-                                         Tr::cvt(v[4 * q + 3]));
+                    __stcs(dst + q, make_float4(Tr::cvt(v[4 * q]), Tr::cvt(v[4 * q + 1]), Tr::cvt(v[4 * q + 2]),
+                                                Tr::cvt(v[4 * q + 3])));
                 float* S = reinterpret_cast<float*>(wsmem);
                 __syncwarp();
 #pragma unroll
@@ -132,7 +132,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
                 float4* tdst = reinterpret_cast<float4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) tdst[q] = src[q];
+                for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
             }
         } else {
 #pragma unroll
@@ -152,7 +152,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         if (fast) {
             float4* dst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gi) * e.ldF + gj0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
             float* S = reinterpret_cast<float*>(wsmem);
             __syncwarp();
 #pragma unroll
@@ -161,7 +161,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
             float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * e.ldF + gi0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) tdst[q] = src[q];
+            for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
         } else if (gi < e.nF) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {

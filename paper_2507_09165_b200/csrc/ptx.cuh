@@ -207,6 +207,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
            "r"(x), "r"(y), "l"(cache_hint)
         : "memory");
 }
+// Same, default L2 policy.
+__device__ __forceinline__ void tma_load_2d_pair_nohint(void* smem_dst, const CUtensorMap* m, uint32_t leader_bar_cluster,
+                                                        int32_t x, int32_t y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];"
+        :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar_cluster),
+           "r"(x), "r"(y)
+        : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_result) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"

@@ -92,7 +92,6 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (ptx::elect_one()) {
-            const uint64_t pol = ptx::policy_evict_last();
             int st = 0;
             uint32_t ph = 0;
             for (int t = cluster_id; t < total_tiles; t += num_clusters) {
@@ -106,8 +105,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     uint8_t* sa = ring + st * kStageBytes;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
-                    ptx::tma_load_2d_pair(sa, &tmA, full_leader, kb * kBK, rowA, pol);
-                    ptx::tma_load_2d_pair(sa + kTileBytes1, &tmB, full_leader, kb * kBK, rowB, pol);
+                    ptx::tma_load_2d_pair_nohint(sa, &tmA, full_leader, kb * kBK, rowA);
+                    ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tmB, full_leader, kb * kBK, rowB);
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
             }
