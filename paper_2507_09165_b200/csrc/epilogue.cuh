@@ -42,7 +42,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 d = __ldcs(d4 + q);
+                    const uint4 d = d4[q];
                     const uint32_t w[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
@@ -56,7 +56,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const float4 d = __ldcs(d4 + q);
+                    const float4 d = d4[q];
                     v[4 * q] += e.beta * d.x;
                     v[4 * q + 1] += e.beta * d.y;
                     v[4 * q + 2] += e.beta * d.z;
@@ -75,7 +75,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const float4 d = __ldcs(d4 + q);
+                const float4 d = d4[q];
                 v[4 * q] += e.beta * d.x;
                 v[4 * q + 1] += e.beta * d.y;
                 v[4 * q + 2] += e.beta * d.z;

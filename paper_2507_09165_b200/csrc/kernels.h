@@ -34,7 +34,13 @@ struct EpiParams {
 struct GemmShape {
     int npad;                 // padded n (multiple of kTile)
     int batch;
+    const uint32_t* tiles;    // CTA-pair kernel: upper-tile visiting order, (I << 16) | J, one matrix
+    int tiles_per_matrix;     // = nt (nt + 1) / 2 for nt = npad / 256
 };
+
+// Visiting order of the upper 256-tiles of one matrix (host side), by name:
+// "row" (row-major), "col" (column-major), "grouped<G>" (G x G super-tiles, row-major).
+void make_tile_order(int nt, const char* order, uint32_t* out);
 
 // Host-side TMA descriptor for an operand buffer [batch*npad rows][npad cols].
 bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch);

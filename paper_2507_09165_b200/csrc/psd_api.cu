@@ -4,6 +4,7 @@
 // bound_scale.cu.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -50,6 +51,8 @@ struct Workspace {
     unsigned* status = nullptr;
     CUtensorMap tmap[B_COUNT];
     int nblk = 0;
+    uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
+    int tiles_per_matrix = 0;
 };
 
 
@@ -87,6 +90,8 @@ void free_ws(Workspace& ws) {
     if (ws.partial) cudaFree(ws.partial);
     if (ws.lambda) cudaFree(ws.lambda);
     if (ws.status) cudaFree(ws.status);
+    if (ws.tiles) cudaFree(ws.tiles);
+    ws.tiles = nullptr;
     ws.partial = nullptr;
     ws.lambda = nullptr;
     ws.status = nullptr;
@@ -128,6 +133,19 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
         if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch)) {
             free_ws(ws);
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
+        }
+    }
+    {
+        const int nt = npad / 256;
+        ws.tiles_per_matrix = nt * (nt + 1) / 2;
+        if (ws.tiles_per_matrix > 0) {
+            std::vector<uint32_t> order(ws.tiles_per_matrix);
+            make_tile_order(nt, std::getenv("PSD_TILE_ORDER"), order.data());
+            if (cudaMalloc(&ws.tiles, order.size() * 4) != cudaSuccess) {
+                free_ws(ws);
+                return fail(PSD_ENOMEM, "cudaMalloc tile order failed");
+            }
+            cudaMemcpy(ws.tiles, order.data(), order.size() * 4, cudaMemcpyHostToDevice);
         }
     }
     cudaError_t e = cudaDeviceSynchronize();
@@ -270,7 +288,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
     // (a3-a6) products
-    GemmShape shape{npad, batch};
+    GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix};
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
     if (h->profiling && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
@@ -471,8 +489,8 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.strideF = static_cast<int64_t>(n) * n;
     ep.nF = n;
     e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st)
-            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch}, ep, st);
+            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch, ws.tiles, ws.tiles_per_matrix}, ep, st)
+            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch, ws.tiles, ws.tiles_per_matrix}, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
     return PSD_OK;

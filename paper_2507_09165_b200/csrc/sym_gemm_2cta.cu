@@ -19,6 +19,10 @@
 #include "optraits.cuh"
 #include "ptx.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 namespace psd {
 
 namespace {
@@ -31,13 +35,11 @@ constexpr int kStageBytes = 2 * kRowsPerCta * kBlockKBytes;   // 32 KB (A + B ha
 constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;
 constexpr uint32_t kTmemCols = 512;            // 2 accumulators x 256 fp32 columns
 
-__device__ __forceinline__ void decode_tile(int t, int nt, int tiles_per_matrix, int& b, int& I, int& J) {
-    b = t / tiles_per_matrix;
-    int rem = t - b * tiles_per_matrix;
-    int i = 0;
-    while (rem >= nt - i) { rem -= nt - i; ++i; }
-    I = i;
-    J = i + rem;
+__device__ __forceinline__ void decode_tile(int t, const GemmShape& s, int& b, int& I, int& J) {
+    b = t / s.tiles_per_matrix;
+    const uint32_t code = __ldg(s.tiles + (t - b * s.tiles_per_matrix));
+    I = static_cast<int>(code >> 16);
+    J = static_cast<int>(code & 0xFFFFu);
 }
 
 template <OpType T>
@@ -65,9 +67,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const bool leader = (rank == 0);
     const int cluster_id = blockIdx.x >> 1;
     const int num_clusters = gridDim.x >> 1;
-    const int nt = s.npad / kT2;
-    const int tiles_per_matrix = nt * (nt + 1) / 2;
-    const int total_tiles = tiles_per_matrix * s.batch;
+    const int total_tiles = s.tiles_per_matrix * s.batch;
     const int num_kb = s.npad / kBK;
 
     if (warp == 0 && ptx::elect_one()) {
@@ -96,7 +96,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             uint32_t ph = 0;
             for (int t = cluster_id; t < total_tiles; t += num_clusters) {
                 int b, I, J;
-                decode_tile(t, nt, tiles_per_matrix, b, I, J);
+                decode_tile(t, s, b, I, J);
                 const int rowA = b * s.npad + I * kT2 + rank * kRowsPerCta;
                 const int rowB = b * s.npad + J * kT2 + rank * kRowsPerCta;
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -159,7 +159,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         int it = 0;
         for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
             int b, I, J;
-            decode_tile(t, nt, tiles_per_matrix, b, I, J);
+            decode_tile(t, s, b, I, J);
             const int acc = it & 1;
             ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
             ptx::tc_fence_after();
@@ -201,8 +201,7 @@ cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gemm
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int nt = s.npad / kT2;
-    const int total = nt * (nt + 1) / 2 * s.batch;
+    const int total = s.tiles_per_matrix * s.batch;
     int clusters = num_sms / 2;
     if (clusters > total) clusters = total;
     sym_gemm_2cta_kernel<T><<<2 * clusters, kThreads2, kSmem2, stream>>>(tmA, tmB, s, e);
@@ -210,6 +209,28 @@ cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gemm
 }
 
 }  // namespace
+
+void make_tile_order(int nt, const char* order, uint32_t* out) {
+    int k = 0;
+    auto put = [&](int I, int J) { out[k++] = (static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(J); };
+    const std::string o = order ? order : "row";
+    if (o == "col") {
+        for (int J = 0; J < nt; ++J)
+            for (int I = 0; I <= J; ++I) put(I, J);
+    } else if (o.rfind("grouped", 0) == 0) {
+        int G = std::atoi(o.c_str() + 7);
+        if (G < 1) G = 4;
+        const int nb = (nt + G - 1) / G;
+        for (int BI = 0; BI < nb; ++BI)
+            for (int BJ = BI; BJ < nb; ++BJ)
+                for (int I = BI * G; I < std::min(nt, BI * G + G); ++I)
+                    for (int J = BJ * G; J < std::min(nt, BJ * G + G); ++J)
+                        if (I <= J) put(I, J);
+    } else {
+        for (int I = 0; I < nt; ++I)
+            for (int J = I; J < nt; ++J) put(I, J);
+    }
+}
 
 bool use_pair_kernel(int64_t n, int64_t batch) {
     const int64_t nt = (n + kT2 - 1) / kT2;
