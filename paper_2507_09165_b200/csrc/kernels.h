@@ -36,6 +36,7 @@ struct GemmShape {
     int batch;
     const uint32_t* tiles;    // CTA-pair kernel: upper-tile visiting order, (I << 16) | J, one matrix
     int tiles_per_matrix;     // = nt (nt + 1) / 2 for nt = npad / 256
+    int* counter;             // CTA-pair kernel: zeroed global tile counter (dynamic scheduler)
 };
 
 // Visiting order of the upper 256-tiles of one matrix (host side), by name:

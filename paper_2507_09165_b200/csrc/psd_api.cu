@@ -53,7 +53,10 @@ struct Workspace {
     int nblk = 0;
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
+    int* counters = nullptr;       // per-product tile counters of the dynamic scheduler
 };
+
+constexpr int kMaxSteps = 1024;
 
 
 int op_bytes(OpType t) { return t == OpType::TF32 ? 4 : 2; }
@@ -91,7 +94,9 @@ void free_ws(Workspace& ws) {
     if (ws.lambda) cudaFree(ws.lambda);
     if (ws.status) cudaFree(ws.status);
     if (ws.tiles) cudaFree(ws.tiles);
+    if (ws.counters) cudaFree(ws.counters);
     ws.tiles = nullptr;
+    ws.counters = nullptr;
     ws.partial = nullptr;
     ws.lambda = nullptr;
     ws.status = nullptr;
@@ -146,6 +151,10 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
                 return fail(PSD_ENOMEM, "cudaMalloc tile order failed");
             }
             cudaMemcpy(ws.tiles, order.data(), order.size() * 4, cudaMemcpyHostToDevice);
+        }
+        if (cudaMalloc(&ws.counters, kMaxSteps * sizeof(int)) != cudaSuccess) {
+            free_ws(ws);
+            return fail(PSD_ENOMEM, "cudaMalloc counters failed");
         }
     }
     cudaError_t e = cudaDeviceSynchronize();
@@ -288,13 +297,18 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
     // (a3-a6) products
-    GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix};
+    if (steps.size() > static_cast<size_t>(kMaxSteps)) return fail(PSD_EUNSUPPORTED, "too many products");
+    e = cudaMemsetAsync(ws.counters, 0, steps.size() * sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
     if (h->profiling && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
     }
-    for (const Step& s : steps) {
+    for (size_t si = 0; si < steps.size(); ++si) {
+        const Step& s = steps[si];
+        shape.counter = ws.counters + si;
         EpiParams ep{};
         ep.alpha = static_cast<float>(s.alpha);
         ep.alpha_dev = s.alpha_lambda ? lam : nullptr;
@@ -488,9 +502,12 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.ldF = n;
     ep.strideF = static_cast<int64_t>(n) * n;
     ep.nF = n;
+    e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    const GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
     e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch, ws.tiles, ws.tiles_per_matrix}, ep, st)
-            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], GemmShape{npad, batch, ws.tiles, ws.tiles_per_matrix}, ep, st);
+            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], shape, ep, st)
+            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], shape, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
     return PSD_OK;

@@ -32,7 +32,7 @@ constexpr int kRowsPerCta = 128;
 constexpr int kStages2 = 6;
 constexpr int kThreads2 = 256;                 // 8 warps
 constexpr int kStageBytes = 2 * kRowsPerCta * kBlockKBytes;   // 32 KB (A + B half)
-constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;
+constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers+ids, staging
 constexpr uint32_t kTmemCols = 512;            // 2 accumulators x 256 fp32 columns
 
 __device__ __forceinline__ void decode_tile(int t, const GemmShape& s, int& b, int& I, int& J) {
@@ -51,6 +51,10 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     constexpr int kUmmaK = 32 / Tr::kBytes;
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kT2, kT2);
     constexpr int kTileBytes1 = kRowsPerCta * kBlockKBytes;   // 16 KB
+    constexpr int kRing = 4;                                  // tile-id ring depth
+    // consumers of each tile id that release a ring slot (arrivals on the leader's tile_empty):
+    // leader MMA thread, 4 leader epilogue warps, peer producer, 4 peer epilogue warps
+    constexpr uint32_t kTileConsumers = 10;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -59,14 +63,15 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint64_t* empty = full + kStages2;
     uint64_t* tmem_full = empty + kStages2;                     // [2]
     uint64_t* tmem_empty = tmem_full + 2;                       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* tile_full = tmem_empty + 2;                       // [kRing]
+    uint64_t* tile_empty = tile_full + kRing;                   // [kRing]
+    uint32_t* tile_id = reinterpret_cast<uint32_t*>(tile_empty + kRing);   // [kRing]
+    uint32_t* tmem_slot = tile_id + kRing;
     uint8_t* epi_smem = smem + kStages2 * kStageBytes + 512;    // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = (rank == 0);
-    const int cluster_id = blockIdx.x >> 1;
-    const int num_clusters = gridDim.x >> 1;
     const int total_tiles = s.tiles_per_matrix * s.batch;
     const int num_kb = s.npad / kBK;
 
@@ -81,6 +86,10 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             ptx::mbar_init(&tmem_full[i], 1);     // one multicast MMA commit
             ptx::mbar_init(&tmem_empty[i], 2 * 128);   // every epilogue thread of both CTAs
         }
+        for (int i = 0; i < kRing; ++i) {
+            ptx::mbar_init(&tile_full[i], 1);     // the fetcher's (local or remote) arrive
+            ptx::mbar_init(&tile_empty[i], kTileConsumers);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -88,20 +97,49 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tile_empty_leader = ptx::mapa_shared(ptx::smem_u32(tile_empty), 0);
+
+    // Tile ids come from a global counter (dynamic scheduling keeps the tiles in flight a
+    // contiguous window of the visiting order, so the operand panels they share stay in L2).
+    // The leader's producer fetches; everybody else reads the id from its CTA's ring.
+    auto next_tile = [&](int i) -> int {
+        const int slot = i & (kRing - 1);
+        ptx::mbar_wait_cluster(&tile_full[slot], (i / kRing) & 1);
+        return static_cast<int>(tile_id[slot]);
+    };
+    auto release_tile = [&](int i) {
+        ptx::mbar_arrive_remote(tile_empty_leader + 8u * static_cast<uint32_t>(i & (kRing - 1)));
+    };
 
     if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer
+        // ------------------------------------------------------------ TMA producer (+ fetcher)
         if (ptx::elect_one()) {
             int st = 0;
             uint32_t ph = 0;
-            for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+            const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(full), 0);
+            for (int i = 0;; ++i) {
+                int t;
+                if (leader) {
+                    const int slot = i & (kRing - 1);
+                    ptx::mbar_wait(&tile_empty[slot], ((i / kRing) & 1) ^ 1);
+                    t = atomicAdd(s.counter, 1);
+                    if (t > total_tiles) t = total_tiles;
+                    tile_id[slot] = static_cast<uint32_t>(t);
+                    ptx::st_shared_cluster_u32(ptx::mapa_shared(ptx::smem_u32(&tile_id[slot]), 1), static_cast<uint32_t>(t));
+                    ptx::mbar_arrive_remote_release(ptx::mapa_shared(ptx::smem_u32(&tile_full[slot]), 1));
+                    ptx::mbar_arrive_remote_release(ptx::mapa_shared(ptx::smem_u32(&tile_full[slot]), 0));
+                } else {
+                    t = next_tile(i);
+                    release_tile(i);
+                }
+                if (t >= total_tiles) break;
                 int b, I, J;
                 decode_tile(t, s, b, I, J);
                 const int rowA = b * s.npad + I * kT2 + rank * kRowsPerCta;
                 const int rowB = b * s.npad + J * kT2 + rank * kRowsPerCta;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[st], ph ^ 1);
-                    const uint32_t full_leader = ptx::mapa_shared(ptx::smem_u32(&full[st]), 0);
+                    const uint32_t full_leader = full_leader0 + 8u * static_cast<uint32_t>(st);
                     uint8_t* sa = ring + st * kStageBytes;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
@@ -118,7 +156,10 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             int st = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+            for (;; ++it) {
+                const int t = next_tile(it);
+                release_tile(it);
+                if (t >= total_tiles) break;
                 const int acc = it & 1;
                 const uint32_t acc_ph = (it >> 1) & 1;
                 ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
@@ -143,11 +184,9 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
             }
-            // drain: the last commits must land before the pair tears down
-            if (it > 0) {
-                const int last = it - 1;
-                ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
-            }
+            // drain: the last accumulators must be read out before the pair tears down
+            for (int last = it - 2; last < it; ++last)
+                if (last >= 0) ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
         }
         __syncwarp();
     } else if (warp >= 4) {
@@ -156,8 +195,12 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         uint8_t* wsmem = epi_smem + q * kEpiWarpSmemBytes;
         const uint32_t tmem_empty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[0]), 0);
         const uint32_t tmem_empty_leader1 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[1]), 0);
-        int it = 0;
-        for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+        for (int it = 0;; ++it) {
+            const int t = next_tile(it);
+            __syncwarp();
+            if (ptx::elect_one()) release_tile(it);
+            __syncwarp();
+            if (t >= total_tiles) break;
             int b, I, J;
             decode_tile(t, s, b, I, J);
             const int acc = it & 1;
