@@ -51,6 +51,19 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def load_traffic(cfg):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/ncu_latest.json, written by tools/summarize_ncu.py from `ncu --set full`)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as f:
+            d = json.load(f)
+        if cfg["n"] == 4096 and "sym_gemm" in d.get("kernel", ""):
+            return d["dram_bytes_per_launch"], d.get("source")
+    except (OSError, ValueError, KeyError):
+        pass
+    return None, None
+
+
 def product_filter(name):
     from paper_2507_09165_b200 import filters
     return {"half": filters.half_filter, "single": filters.single_filter,
@@ -301,6 +314,7 @@ def run_ours(args, cfg):
         else:
             peak = peak_bf16 / 2.0
             peak_note = f"{peak_src} bf16 burst x 1/2 (tf32 nominal ratio)"
+        traffic, traffic_src = load_traffic(cfg)
         line = {
             "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -312,8 +326,10 @@ def run_ours(args, cfg):
             "tflops_dense_equivalent": dense_flops_matrix * gb * args.steps / (ms / 1000.0) / 1e12,
             "tflops_algorithmic": alg_flops_product * G * gb * args.steps / (ms / 1000.0) / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
-                         "kernel": "sym_gemm_kernel (symmetric product, fused epilogue)",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "kernel": "sym_gemm_2cta_kernel (CTA-pair tcgen05 symmetric product, fused epilogue)"
+                         if n >= 1024 else "sym_gemm_kernel (tcgen05 symmetric product, fused epilogue)",
                          "per_launch_flops": alg_flops_product * count,
                          "avg_launch_ms": launch_ms, "peak_source": peak_note},
             "gpu_launches": kernel_launches,
@@ -336,7 +352,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
