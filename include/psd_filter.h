@@ -57,14 +57,20 @@ typedef enum {
 
 /* Operand precision of the tensor-core products; accumulation is always fp32.
  * FP16: the paper's half-precision path.  BF16: same kernel, bf16 operands.
- * TF32: kind::tf32 single pass.  TF32X3: 3-pass split hi*hi + hi*lo + lo*hi on
- * kind::tf32, the FP32 path (the paper's FP32 / BF16x9-emulated path).
- * Readings R11 and R17 in DESIGN.md. */
+ * TF32: kind::tf32 single pass.
+ * *X3 (split precision, the FP32-class path standing in for the paper's FP32 /
+ * BF16x9-emulated products): every operand is stored as hi + lo in the
+ * operand type (fp16 with a per-buffer power-of-two scale that keeps lo in the normal
+ * range) and each product is hi*hi + hi*lo + lo*hi, three tcgen05.mma passes into one fp32
+ * accumulator.  FP16X3 runs at the fp16 rate (3 passes), TF32X3 at the tf32 rate.
+ * Readings R11, R17, R19 in DESIGN.md. */
 typedef enum {
     PSD_PREC_FP16 = 0,
     PSD_PREC_BF16 = 1,
     PSD_PREC_TF32 = 2,
-    PSD_PREC_TF32X3 = 3
+    PSD_PREC_TF32X3 = 3,
+    PSD_PREC_FP16X3 = 4,
+    PSD_PREC_BF16X3 = 5
 } psd_precision_t;
 
 /* FROBENIUS: lambda~ = ||X||_F computed on the device (default).

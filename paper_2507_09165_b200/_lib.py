@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libpsdfilter.so")
 PSD_OK, PSD_EINVAL, PSD_ENOMEM, PSD_ECUDA, PSD_ENCCL, PSD_ENONFINITE, PSD_EUNSUPPORTED = range(7)
 STATUS_NAMES = {0: "PSD_OK", 1: "PSD_EINVAL", 2: "PSD_ENOMEM", 3: "PSD_ECUDA", 4: "PSD_ENCCL",
                 5: "PSD_ENONFINITE", 6: "PSD_EUNSUPPORTED"}
-PRECISIONS = {"fp16": 0, "bf16": 1, "tf32": 2, "tf32x3": 3}
+PRECISIONS = {"fp16": 0, "bf16": 1, "tf32": 2, "tf32x3": 3, "fp16x3": 4, "bf16x3": 5}
 BOUNDS = {"frobenius": 0, "user": 1}
 
 # (name, restype, argtypes) for every symbol include/psd_filter.h declares.

@@ -67,10 +67,12 @@ template <OpType T> struct Cvt;
 template <> struct Cvt<OpType::F16> {
     using type = __half;
     __device__ static type f(float v) { return __float2half_rn(v); }
+    __device__ static float back(type v) { return __half2float(v); }
 };
 template <> struct Cvt<OpType::BF16> {
     using type = __nv_bfloat16;
     __device__ static type f(float v) { return __float2bfloat16_rn(v); }
+    __device__ static float back(type v) { return __bfloat162float(v); }
 };
 template <> struct Cvt<OpType::TF32> {
     using type = float;
@@ -79,6 +81,7 @@ template <> struct Cvt<OpType::TF32> {
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
         return __uint_as_float(r);
     }
+    __device__ static float back(type v) { return v; }
 };
 
 constexpr int kST = 64;   // scale tile (64 x 64, 256 threads)
@@ -100,8 +103,8 @@ __device__ __forceinline__ void upper_coords(int t, int nt, int& I, int& J) {
 template <OpType T>
 __global__ void __launch_bounds__(256)
 scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double* __restrict__ lambda,
-                     double scale, typename Cvt<T>::type* __restrict__ out_op, float* __restrict__ out32,
-                     float* __restrict__ outF, double post) {
+                     double scale, typename Cvt<T>::type* __restrict__ out_op, typename Cvt<T>::type* __restrict__ out_lo,
+                     float op_scale, float* __restrict__ outF, double post) {
     using op_t = typename Cvt<T>::type;
     __shared__ float S[kST][kST + 1];
     const int b = blockIdx.y;
@@ -142,28 +145,29 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
     // each thread: one row segment of 16 elements of the direct tile and of the mirrored tile
     const int r = tid >> 2, cs = (tid & 3) * 16;
     if (out_op) {
-        __align__(16) op_t vd[16];
-        __align__(16) op_t vt[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int c = cs + i;
-            vd[i] = Cvt<T>::f((I == J && c < r) ? S[c][r] : S[r][c]);
-            vt[i] = Cvt<T>::f(S[c][r]);
-        }
         constexpr int kVec = 16 / sizeof(op_t);   // elements per 16-byte store
-        uint4* od = reinterpret_cast<uint4*>(out_op + base + static_cast<int64_t>(r0 + r) * npad + c0 + cs);
+        for (int part = 0; part < (out_lo ? 2 : 1); ++part) {
+            __align__(16) op_t vd[16];
+            __align__(16) op_t vt[16];
 #pragma unroll
-        for (int q = 0; q < 16 / kVec; ++q) od[q] = *reinterpret_cast<const uint4*>(vd + q * kVec);
-        if (I != J) {
-            uint4* ot = reinterpret_cast<uint4*>(out_op + base + static_cast<int64_t>(c0 + r) * npad + r0 + cs);
+            for (int i = 0; i < 16; ++i) {
+                const int c = cs + i;
+                const float xd = ((I == J && c < r) ? S[c][r] : S[r][c]) * op_scale;
+                const float xt = S[c][r] * op_scale;
+                const op_t hd = Cvt<T>::f(xd), ht = Cvt<T>::f(xt);
+                // part 0: hi = rn(x s); part 1: lo = rn(x s - hi)
+                vd[i] = part == 0 ? hd : Cvt<T>::f(xd - Cvt<T>::back(hd));
+                vt[i] = part == 0 ? ht : Cvt<T>::f(xt - Cvt<T>::back(ht));
+            }
+            op_t* dstb = part == 0 ? out_op : out_lo;
+            uint4* od = reinterpret_cast<uint4*>(dstb + base + static_cast<int64_t>(r0 + r) * npad + c0 + cs);
 #pragma unroll
-            for (int q = 0; q < 16 / kVec; ++q) ot[q] = *reinterpret_cast<const uint4*>(vt + q * kVec);
-        }
-    }
-    if (out32) {
-        for (int i = 0; i < 16; ++i) {
-            const int c = cs + i;
-            out32[base + static_cast<int64_t>(r0 + r) * npad + c0 + c] = (I == J && c < r) ? S[c][r] : S[r][c];
+            for (int q = 0; q < 16 / kVec; ++q) od[q] = *reinterpret_cast<const uint4*>(vd + q * kVec);
+            if (I != J) {
+                uint4* ot = reinterpret_cast<uint4*>(dstb + base + static_cast<int64_t>(c0 + r) * npad + r0 + cs);
+#pragma unroll
+                for (int q = 0; q < 16 / kVec; ++q) ot[q] = *reinterpret_cast<const uint4*>(vt + q * kVec);
+            }
         }
     }
     if (outF) {
@@ -200,22 +204,25 @@ cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, do
 }
 
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
-                                 const double* lambda, double scale, void* out_op, float* out32,
-                                 float* outF, double post, cudaStream_t stream) {
+                                 const double* lambda, double scale, void* out_op, void* out_lo,
+                                 double op_scale, float* outF, double post, cudaStream_t stream) {
     const int nt = npad / kST;
     dim3 grid(nt * (nt + 1) / 2, batch);
     switch (t) {
         case OpType::F16:
             scale_convert_kernel<OpType::F16><<<grid, 256, 0, stream>>>(
-                X, n, npad, lambda, scale, static_cast<__half*>(out_op), out32, outF, post);
+                X, n, npad, lambda, scale, static_cast<__half*>(out_op), static_cast<__half*>(out_lo),
+                static_cast<float>(op_scale), outF, post);
             break;
         case OpType::BF16:
             scale_convert_kernel<OpType::BF16><<<grid, 256, 0, stream>>>(
-                X, n, npad, lambda, scale, static_cast<__nv_bfloat16*>(out_op), out32, outF, post);
+                X, n, npad, lambda, scale, static_cast<__nv_bfloat16*>(out_op),
+                static_cast<__nv_bfloat16*>(out_lo), static_cast<float>(op_scale), outF, post);
             break;
         case OpType::TF32:
             scale_convert_kernel<OpType::TF32><<<grid, 256, 0, stream>>>(
-                X, n, npad, lambda, scale, static_cast<float*>(out_op), out32, outF, post);
+                X, n, npad, lambda, scale, static_cast<float*>(out_op), static_cast<float*>(out_lo),
+                static_cast<float>(op_scale), outF, post);
             break;
     }
     return cudaGetLastError();

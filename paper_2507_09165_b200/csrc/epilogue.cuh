@@ -24,75 +24,14 @@ namespace psd {
 constexpr int kEpiWarpSmemBytes = 32 * 36 * 4;
 
 template <OpType T>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
-                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem) {
+__device__ __forceinline__ void store_op_mirrored(void* out, int64_t opBase, int npad, int gi0, int gj0, bool diag,
+                                                  const float (&v)[32], uint8_t* wsmem) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     const int lane = threadIdx.x & 31;
     const int gi = gi0 + lane;
-    const int64_t opBase = static_cast<int64_t>(b) * npad * npad;
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
-
-    if (e.Dop) {                                     // addend in operand precision, ld npad
-        const op_t* drow = reinterpret_cast<const op_t*>(e.Dop) + opBase + static_cast<int64_t>(gi) * npad;
-        if (!diag) {
-            if constexpr (Tr::kBytes == 2) {
-                const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint4 d = d4[q];
-                    const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        float lo, hi;
-                        Tr::unpack2(w[h], lo, hi);
-                        v[q * 8 + 2 * h] += e.beta * lo;
-                        v[q * 8 + 2 * h + 1] += e.beta * hi;
-                    }
-                }
-            } else {
-                const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 d = d4[q];
-                    v[4 * q] += e.beta * d.x;
-                    v[4 * q + 1] += e.beta * d.y;
-                    v[4 * q + 2] += e.beta * d.z;
-                    v[4 * q + 3] += e.beta * d.w;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (gj0 + i >= gi) v[i] += e.beta * Tr::to_float(drow[gj0 + i]);
-        }
-    }
-    if (e.Df) {                                      // fp32 addend (the input X), masked to nDf
-        const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
-        if (!diag && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
-            const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float4 d = d4[q];
-                v[4 * q] += e.beta * d.x;
-                v[4 * q + 1] += e.beta * d.y;
-                v[4 * q + 2] += e.beta * d.z;
-                v[4 * q + 3] += e.beta * d.w;
-            }
-        } else {
-            const bool row_ok = gi < e.nDf;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                v[i] += (row_ok && gj < e.nDf && gj >= gi) ? e.beta * drow[gj] : 0.0f;
-            }
-        }
-    }
-
-    if (e.out_op) {
-        op_t* out_op = reinterpret_cast<op_t*>(e.out_op);
+    {
+        op_t* out_op = reinterpret_cast<op_t*>(out);
         op_t* orow = out_op + opBase + static_cast<int64_t>(gi) * npad;
         if (!diag) {
             // direct half: 32 contiguous elements of row gi
@@ -144,6 +83,124 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * npad + gi] = cv;
             }
         }
+    }
+}
+
+template <OpType T>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
+                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem) {
+    using Tr = OpTraits<T>;
+    using op_t = typename Tr::type;
+    const int lane = threadIdx.x & 31;
+    const int gi = gi0 + lane;
+    const int64_t opBase = static_cast<int64_t>(b) * npad * npad;
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
+
+    if (e.Dop) {                                     // addend in operand precision, ld npad
+        const op_t* drow = reinterpret_cast<const op_t*>(e.Dop) + opBase + static_cast<int64_t>(gi) * npad;
+        if (!diag) {
+            if constexpr (Tr::kBytes == 2) {
+                const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 d = d4[q];
+                    const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        float lo, hi;
+                        Tr::unpack2(w[h], lo, hi);
+                        v[q * 8 + 2 * h] += e.beta * lo;
+                        v[q * 8 + 2 * h + 1] += e.beta * hi;
+                    }
+                }
+                if (e.Dop_lo) {
+                    const uint4* l4 = reinterpret_cast<const uint4*>(
+                        reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad + gj0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 d = l4[q];
+                        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            float lo, hi;
+                            Tr::unpack2(w[h], lo, hi);
+                            v[q * 8 + 2 * h] += e.beta * lo;
+                            v[q * 8 + 2 * h + 1] += e.beta * hi;
+                        }
+                    }
+                }
+            } else {
+                const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 d = d4[q];
+                    v[4 * q] += e.beta * d.x;
+                    v[4 * q + 1] += e.beta * d.y;
+                    v[4 * q + 2] += e.beta * d.z;
+                    v[4 * q + 3] += e.beta * d.w;
+                }
+                if (e.Dop_lo) {
+                    const float4* l4 = reinterpret_cast<const float4*>(
+                        reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad + gj0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 d = l4[q];
+                        v[4 * q] += e.beta * d.x;
+                        v[4 * q + 1] += e.beta * d.y;
+                        v[4 * q + 2] += e.beta * d.z;
+                        v[4 * q + 3] += e.beta * d.w;
+                    }
+                }
+            }
+        } else {
+            const op_t* lrow = e.Dop_lo ? reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad
+                                        : nullptr;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (gj0 + i >= gi)
+                    v[i] += e.beta * (Tr::to_float(drow[gj0 + i]) + (lrow ? Tr::to_float(lrow[gj0 + i]) : 0.0f));
+        }
+    }
+    if (e.Df) {                                      // fp32 addend (the input X), masked to nDf
+        const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
+        if (!diag && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
+            const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float4 d = d4[q];
+                v[4 * q] += e.beta * d.x;
+                v[4 * q + 1] += e.beta * d.y;
+                v[4 * q + 2] += e.beta * d.z;
+                v[4 * q + 3] += e.beta * d.w;
+            }
+        } else {
+            const bool row_ok = gi < e.nDf;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int gj = gj0 + i;
+                v[i] += (row_ok && gj < e.nDf && gj >= gi) ? e.beta * drow[gj] : 0.0f;
+            }
+        }
+    }
+
+    if (e.out_op) {
+        float w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w[i] = v[i] * e.out_scale;
+        if (e.out_lo) {
+            // split precision: hi = rn(w), lo = rn(w - hi); both stored mirrored
+            float lo[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float h = Tr::to_float(Tr::cvt(w[i]));
+                lo[i] = w[i] - h;
+                w[i] = h;
+            }
+            store_op_mirrored<T>(e.out_lo, opBase, npad, gi0, gj0, diag, lo, wsmem);
+        }
+        store_op_mirrored<T>(e.out_op, opBase, npad, gi0, gj0, diag, w, wsmem);
     }
 
     if (e.outF) {

@@ -18,10 +18,13 @@ constexpr int kPadTo = 128;   // padded matrix dimension multiple
 // Epilogue of one symmetric product C = alpha_eff * (A B) + beta * D over the upper
 // tiles (I <= J) of each matrix; see sym_gemm.cu for which elements go where.
 struct EpiParams {
-    float alpha;              // host factor
+    float alpha;              // host factor (already divided by the operands' scales)
     const double* alpha_dev;  // optional per-matrix factor (lambda~), multiplies alpha
-    float beta;
+    float beta;               // (already divided by the addend's scale)
     const void* Dop;          // optional addend in operand precision, upper triangle, ld npad
+    const void* Dop_lo;       // split precision: low part of the addend (added to Dop)
+    void* out_lo;             // split precision: low part of the output copy
+    float out_scale;          // the output copy stores v * out_scale (power of two)
     const float* Df;          // optional fp32 addend (the input X), upper triangle read
     int64_t ldDf, strideDf;   // row stride / matrix stride (elements)
     int nDf;                  // rows/cols of Df that exist (mask)
@@ -46,13 +49,19 @@ void make_tile_order(int nt, const char* order, uint32_t* out);
 // Host-side TMA descriptor for an operand buffer [batch*npad rows][npad cols].
 bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch);
 
-// C = alpha*(A B) + beta*D on the upper tiles; A, B given by their tensor maps.
-cudaError_t launch_sym_gemm(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                            const GemmShape& s, const EpiParams& e, cudaStream_t stream);
+// Operand tensor maps of one product: A, B (high parts) and, for split precision, their
+// low parts (A*B ~= Ahi Bhi + Ahi Blo + Alo Bhi, three tcgen05.mma passes, one accumulator).
+struct OperandMaps {
+    CUtensorMap a, b, a_lo, b_lo;
+};
+
+// C = alpha*(A B) + beta*D on the upper tiles.
+cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
+                            cudaStream_t stream);
 
 // Same product, persistent CTA-pair kernel with 256 x 256 tiles (npad multiple of 256).
-cudaError_t launch_sym_gemm_2cta(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                                 const GemmShape& s, const EpiParams& e, cudaStream_t stream);
+cudaError_t launch_sym_gemm_2cta(OpType t, bool split, const OperandMaps& m, const GemmShape& s,
+                                 const EpiParams& e, cudaStream_t stream);
 // Whether (n, batch) runs on the CTA-pair kernel, and the padded size it needs.
 bool use_pair_kernel(int64_t n, int64_t batch);
 int64_t padded_n(int64_t n, int64_t batch);
@@ -71,8 +80,9 @@ cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, do
 //   op copy (full, mirrored, zero padded, ld npad)  -- if out_op
 //   fp32 master (upper 32-tiles, zero padded)       -- if out32
 //   fp32 final (full, mirrored, ld n)               -- if outF (scaled by post)
+// With out_lo (split precision): out_op = cvt(x0 * op_scale), out_lo = cvt(x0 * op_scale - out_op).
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
-                                 const double* lambda, double scale, void* out_op, float* out32,
-                                 float* outF, double post, cudaStream_t stream);
+                                 const double* lambda, double scale, void* out_op, void* out_lo,
+                                 double op_scale, float* outF, double post, cudaStream_t stream);
 
 }  // namespace psd

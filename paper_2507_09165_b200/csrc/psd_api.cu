@@ -2,6 +2,7 @@
 // planner (Algorithm 2 as a list of fused symmetric products), the device workspace
 // and the stream-ordered launches.  Host code; kernels live in sym_gemm.cu and
 // bound_scale.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -45,11 +46,12 @@ struct Step {
 struct Workspace {
     int npad = 0, batch = 0;
     OpType op = OpType::F16;
-    void* op_buf[B_COUNT] = {};
+    bool split = false;
+    void* op_buf[2 * B_COUNT] = {};          // [B_COUNT..2 B_COUNT): low parts (split precision)
     double* partial = nullptr;
     double* lambda = nullptr;
     unsigned* status = nullptr;
-    CUtensorMap tmap[B_COUNT];
+    CUtensorMap tmap[2 * B_COUNT];
     int nblk = 0;
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
@@ -70,6 +72,8 @@ struct psd_filter_s {
     psd_precision_t prec = PSD_PREC_FP16;
     psd_bound_t bound = PSD_BOUND_FROBENIUS;
     Workspace ws;
+    // power-of-two operand scales of the fp16 split path: Z iterates, Y = Z^2, Horner U
+    double s_z = 1.0, s_y = 1.0, s_u = 1.0;
     // profiling / launch accounting
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -82,13 +86,61 @@ namespace {
 
 OpType op_of(psd_precision_t p) {
     switch (p) {
-        case PSD_PREC_BF16: return OpType::BF16;
-        case PSD_PREC_TF32: return OpType::TF32;
+        case PSD_PREC_BF16:
+        case PSD_PREC_BF16X3: return OpType::BF16;
+        case PSD_PREC_TF32:
+        case PSD_PREC_TF32X3: return OpType::TF32;
         default: return OpType::F16;
     }
 }
 
+bool split_of(psd_precision_t p) {
+    return p == PSD_PREC_TF32X3 || p == PSD_PREC_FP16X3 || p == PSD_PREC_BF16X3;
+}
+
+// Bounds of |Z|, |Y|, |U| over the whole chain for spectra in [-1, 1] (||X_0||_2 <= 1 by the
+// Frobenius normalisation; matrix entries are bounded by the spectral norm), evaluated on the
+// scalar chain exactly as the planner folds it; each scale puts 1.25 x bound at <= 2^14.
+void compute_scales(psd_filter_s* h) {
+    const int N = 40001;
+    std::vector<double> z(N);
+    for (int i = 0; i < N; ++i) z[i] = -1.0 + 2.0 * i / (N - 1);
+    double bz = 1.0, by = 0.0, bu = 0.0, s = 1.0;
+    for (const auto& c : h->coeffs) {
+        const int p = static_cast<int>(c.size()) - 1;
+        if (p == 0) { s *= c[0]; continue; }
+        std::vector<double> cs(c.size());
+        for (int j = 0; j <= p; ++j) cs[j] = c[j] * std::pow(s, 2 * j + 1);
+        s = 1.0;
+        for (int i = 0; i < N; ++i) {
+            const double y = z[i] * z[i];
+            by = std::max(by, std::fabs(y));
+            double u;
+            if (p == 1) {
+                u = cs[1] * y;
+            } else {
+                u = cs[p] * y * y + cs[p - 1] * y;
+                bu = std::max(bu, std::fabs(u));
+                for (int j = p - 2; j >= 1; --j) {
+                    u = y * u + cs[j] * y;
+                    bu = std::max(bu, std::fabs(u));
+                }
+            }
+            z[i] = cs[0] * z[i] + z[i] * u;
+            bz = std::max(bz, std::fabs(z[i]));
+        }
+    }
+    auto scale_for = [](double b) {
+        if (!(b > 0.0) || !std::isfinite(b)) return 1.0;
+        return std::pow(2.0, std::floor(std::log2(16384.0 / (1.25 * b))));
+    };
+    h->s_z = scale_for(bz);
+    h->s_y = scale_for(by);
+    h->s_u = scale_for(bu);
+}
+
 void free_ws(Workspace& ws) {
+    for (int i = B_COUNT; i < 2 * B_COUNT; ++i) { if (ws.op_buf[i]) cudaFree(ws.op_buf[i]); ws.op_buf[i] = nullptr; }
     for (auto& p : ws.op_buf) { if (p) cudaFree(p); p = nullptr; }
     if (ws.partial) cudaFree(ws.partial);
     if (ws.lambda) cudaFree(ws.lambda);
@@ -103,22 +155,23 @@ void free_ws(Workspace& ws) {
     ws.npad = ws.batch = 0;
 }
 
-int64_t ws_bytes(OpType op, int64_t npad, int64_t batch) {
+int64_t ws_bytes(OpType op, bool split, int64_t npad, int64_t batch) {
     const int64_t mat = npad * npad * batch;
-    return B_COUNT * mat * op_bytes(op) + batch * 256 * 8 + batch * 8 + 64;
+    return (split ? 2 : 1) * B_COUNT * mat * op_bytes(op) + batch * 256 * 8 + batch * 8 + 64;
 }
 
 psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     Workspace& ws = h->ws;
     const OpType op = op_of(h->prec);
-    if (ws.npad == npad && ws.batch >= batch && ws.op == op && ws.status) return PSD_OK;
+    const bool split = split_of(h->prec);
+    if (ws.npad == npad && ws.batch >= batch && ws.op == op && ws.split == split && ws.status) return PSD_OK;
     if (ws.status) {
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
     }
     free_ws(ws);
     const size_t mat = static_cast<size_t>(npad) * npad * batch;
-    for (int i = 0; i < B_COUNT; ++i) {
+    for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
         if (cudaMalloc(&ws.op_buf[i], mat * op_bytes(op)) != cudaSuccess) {
             free_ws(ws);
             return fail(PSD_ENOMEM, "cudaMalloc operand workspace failed");
@@ -133,8 +186,8 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     }
     cudaMemset(ws.status, 0, 64);
     // Zero everything once: padded rows/cols of every operand buffer must read as 0.
-    for (int i = 0; i < B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
-    for (int i = 0; i < B_COUNT; ++i) {
+    for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
+    for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
         if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch)) {
             free_ws(ws);
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
@@ -165,6 +218,7 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     ws.npad = npad;
     ws.batch = batch;
     ws.op = op;
+    ws.split = split;
     return PSD_OK;
 }
 
@@ -245,7 +299,6 @@ psd_status_t check_args(psd_filter_t h, const void* X, int64_t n, int64_t batch,
     if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
         return fail(PSD_EINVAL, "X and out must be 16-byte aligned");
     if (n > 65536) return fail(PSD_EUNSUPPORTED, "n > 65536");
-    if (h->prec == PSD_PREC_TF32X3) return fail(PSD_EUNSUPPORTED, "TF32X3 not built yet");
     return PSD_OK;
 }
 
@@ -291,8 +344,25 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     }
     double sign_only = 0.0;
     std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
+    const bool split = ws.split;
+    double sc[B_COUNT];
+    for (int i = 0; i < B_COUNT; ++i) sc[i] = 1.0;
+    if (split && ws.op == OpType::F16) {
+        sc[B_X0] = sc[B_XA] = sc[B_XB] = h->s_z;
+        sc[B_Y] = h->s_y;
+        sc[B_UA] = sc[B_UB] = h->s_u;
+    }
+    auto maps = [&](int A, int B) {
+        OperandMaps m;
+        m.a = ws.tmap[A];
+        m.b = ws.tmap[B];
+        m.a_lo = ws.tmap[split ? A + B_COUNT : A];
+        m.b_lo = ws.tmap[split ? B + B_COUNT : B];
+        return m;
+    };
     // (a2) scale + convert; the products-free sign chain finishes here
-    e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr,
+    e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0],
+                             split ? ws.op_buf[B_X0 + B_COUNT] : nullptr, sc[B_X0],
                              (want_sign && steps.empty()) ? out : nullptr, sign_only, st);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
@@ -310,11 +380,13 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         const Step& s = steps[si];
         shape.counter = ws.counters + si;
         EpiParams ep{};
-        ep.alpha = static_cast<float>(s.alpha);
+        ep.alpha = static_cast<float>(s.alpha / (sc[s.A] * sc[s.B]));
         ep.alpha_dev = s.alpha_lambda ? lam : nullptr;
-        ep.beta = static_cast<float>(s.beta);
+        ep.beta = static_cast<float>(s.D >= 0 ? s.beta / sc[s.D] : s.beta);
+        ep.out_scale = s.out_op >= 0 ? static_cast<float>(sc[s.out_op]) : 1.0f;
         if (s.D >= 0) {
             ep.Dop = ws.op_buf[s.D];
+            ep.Dop_lo = split ? ws.op_buf[s.D + B_COUNT] : nullptr;
         } else if (s.D == D_XIN) {
             ep.Df = X;
             ep.ldDf = n;
@@ -322,6 +394,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             ep.nDf = n;
         }
         ep.out_op = s.out_op >= 0 ? ws.op_buf[s.out_op] : nullptr;
+        ep.out_lo = (s.out_op >= 0 && split) ? ws.op_buf[s.out_op + B_COUNT] : nullptr;
         if (s.outF) {
             ep.outF = out;
             ep.ldF = n;
@@ -329,8 +402,8 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             ep.nF = n;
         }
         e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-                ? launch_sym_gemm_2cta(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st)
-                : launch_sym_gemm(ws.op, ws.tmap[s.A], ws.tmap[s.B], shape, ep, st);
+                ? launch_sym_gemm_2cta(ws.op, split, maps(s.A, s.B), shape, ep, st)
+                : launch_sym_gemm(ws.op, split, maps(s.A, s.B), shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
     }
@@ -376,6 +449,7 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
         h->degrees.push_back(d);
         h->coeffs.push_back(cc);
     }
+    compute_scales(h);
     *out = h;
     g_last_error.clear();
     return PSD_OK;
@@ -394,7 +468,7 @@ void psd_filter_destroy(psd_filter_t h) {
 
 psd_status_t psd_filter_set_precision(psd_filter_t h, psd_precision_t prec) {
     if (!h) return fail(PSD_EINVAL, "null handle");
-    if (prec < PSD_PREC_FP16 || prec > PSD_PREC_TF32X3) return fail(PSD_EINVAL, "unknown precision");
+    if (prec < PSD_PREC_FP16 || prec > PSD_PREC_BF16X3) return fail(PSD_EINVAL, "unknown precision");
     h->prec = prec;
     return PSD_OK;
 }
@@ -415,7 +489,7 @@ int psd_filter_gemm_count(psd_filter_t h, int for_project) {
 
 int64_t psd_workspace_bytes(psd_filter_t h, int64_t n, int64_t batch) {
     if (!h || n < 1 || batch < 1) return -1;
-    return ws_bytes(op_of(h->prec), padded_n(n, batch), batch);
+    return ws_bytes(op_of(h->prec), split_of(h->prec), padded_n(n, batch), batch);
 }
 
 psd_status_t psd_project(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out, void* stream) {
@@ -484,14 +558,17 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     if (rc != PSD_OK) return rc;
     Workspace& ws = h->ws;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = launch_scale_convert(ws.op, A, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XA], nullptr,
-                                         nullptr, 0.0, st);
+    const bool split = ws.split;
+    cudaError_t e = launch_scale_convert(ws.op, A, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XA],
+                                         split ? ws.op_buf[B_XA + B_COUNT] : nullptr, 1.0, nullptr, 0.0, st);
     if (e == cudaSuccess)
-        e = launch_scale_convert(ws.op, B, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XB], nullptr, nullptr, 0.0, st);
+        e = launch_scale_convert(ws.op, B, n, npad, batch, nullptr, 1.0, ws.op_buf[B_XB],
+                                 split ? ws.op_buf[B_XB + B_COUNT] : nullptr, 1.0, nullptr, 0.0, st);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     EpiParams ep{};
     ep.alpha = static_cast<float>(alpha);
     ep.beta = static_cast<float>(beta);
+    ep.out_scale = 1.0f;
     if (D) {
         ep.Df = D;
         ep.ldDf = n;
@@ -505,9 +582,14 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     const GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
+    OperandMaps m;
+    m.a = ws.tmap[B_XA];
+    m.b = ws.tmap[B_XB];
+    m.a_lo = ws.tmap[split ? B_XA + B_COUNT : B_XA];
+    m.b_lo = ws.tmap[split ? B_XB + B_COUNT : B_XB];
     e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-            ? launch_sym_gemm_2cta(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], shape, ep, st)
-            : launch_sym_gemm(ws.op, ws.tmap[B_XA], ws.tmap[B_XB], shape, ep, st);
+            ? launch_sym_gemm_2cta(ws.op, split, m, shape, ep, st)
+            : launch_sym_gemm(ws.op, split, m, shape, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
     return PSD_OK;

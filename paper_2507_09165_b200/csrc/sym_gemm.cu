@@ -23,10 +23,14 @@ namespace psd {
 
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTile * kBlockKBytes;                 // 16 KB per operand tile
-constexpr int kSmemBytes = 2 * kStages * kTileBytes + 1024 + 256 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers, staging
+constexpr int kRingBytes1 = 128 * 1024;
+template <bool kSplit> struct Ring1 {
+    static constexpr int kStageBytes = (kSplit ? 4 : 2) * kTileBytes;   // A, B (+ A_lo, B_lo)
+    static constexpr int kStages = kRingBytes1 / kStageBytes;           // 4 or 2
+};
+constexpr int kSmemBytes = kRingBytes1 + 1024 + 256 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers, staging
 
 __device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J) {
     // row-major enumeration of {(I, J): 0 <= I <= J < nt}
@@ -37,24 +41,24 @@ __device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J)
     J = i + rem;
 }
 
-template <OpType T>
+template <OpType T, bool kSplit>
 __global__ void __launch_bounds__(kThreads, 1)
-sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmShape s, const EpiParams e) {
+sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
+    constexpr int kStages = Ring1<kSplit>::kStages;
+    constexpr int kStageBytes = Ring1<kSplit>::kStageBytes;
     constexpr int kBK = kBlockKBytes / Tr::kBytes;     // K elements per block (64 f16 / 32 tf32)
     constexpr int kUmmaK = 32 / Tr::kBytes;            // K per tcgen05.mma (16 f16 / 8 tf32)
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, kTile);
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * kTileBytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * kTileBytes);
+    uint8_t* ring = smem;                                         // stage: A | B | A_lo | B_lo
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes1);
     uint64_t* empty = full + kStages;
     uint64_t* accum_full = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
-    uint8_t* epi_smem = smem + 2 * kStages * kTileBytes + 256;     // 4 x kEpiWarpSmemBytes
+    uint8_t* epi_smem = smem + kRingBytes1 + 256;                   // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
     const int nt = s.npad / kTile;
@@ -64,8 +68,8 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     if (warp == 0) {
         if (ptx::elect_one()) {
-            ptx::tma_prefetch_desc(&tmA);
-            ptx::tma_prefetch_desc(&tmB);
+            ptx::tma_prefetch_desc(&tm.a);
+            ptx::tma_prefetch_desc(&tm.b);
             for (int i = 0; i < kStages; ++i) {
                 ptx::mbar_init(&full[i], 1);
                 ptx::mbar_init(&empty[i], 1);
@@ -93,9 +97,14 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int st = kb % kStages;
                 const uint32_t ph = (kb / kStages) & 1;
                 ptx::mbar_wait(&empty[st], ph ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[st], 2 * kTileBytes);
-                ptx::tma_load_2d(sA + st * kTileBytes, &tmA, &full[st], kb * kBK, rowA, pol);
-                ptx::tma_load_2d(sB + st * kTileBytes, &tmB, &full[st], kb * kBK, rowB, pol);
+                uint8_t* sa = ring + st * kStageBytes;
+                ptx::mbar_arrive_expect_tx(&full[st], kStageBytes);
+                ptx::tma_load_2d(sa, &tm.a, &full[st], kb * kBK, rowA, pol);
+                ptx::tma_load_2d(sa + kTileBytes, &tm.b, &full[st], kb * kBK, rowB, pol);
+                if constexpr (kSplit) {
+                    ptx::tma_load_2d(sa + 2 * kTileBytes, &tm.a_lo, &full[st], kb * kBK, rowA, pol);
+                    ptx::tma_load_2d(sa + 3 * kTileBytes, &tm.b_lo, &full[st], kb * kBK, rowB, pol);
+                }
             }
         }
         __syncwarp();
@@ -106,15 +115,25 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const uint32_t ph = (kb / kStages) & 1;
                 ptx::mbar_wait(&full[st], ph);
                 ptx::tc_fence_after();
-                const uint64_t adesc = ptx::smem_desc_sw128_kmajor(ptx::smem_u32(sA + st * kTileBytes));
-                const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(ptx::smem_u32(sB + st * kTileBytes));
+                const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
+                const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
+                const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + kTileBytes);
+                auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
+                    if constexpr (T == OpType::TF32)
+                        ptx::mma_tf32(tmem_base, a, bb, kIdesc, accumulate);
+                    else
+                        ptx::mma_f16(tmem_base, a, bb, kIdesc, accumulate);
+                };
 #pragma unroll
                 for (int k = 0; k < kBK / kUmmaK; ++k) {
                     const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);   // 32 B per K step
-                    if constexpr (T == OpType::TF32)
-                        ptx::mma_tf32(tmem_base, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
-                    else
-                        ptx::mma_f16(tmem_base, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                    mma(adesc + koff, bdesc + koff, (kb | k) != 0);
+                    if constexpr (kSplit) {
+                        const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes);
+                        const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes);
+                        mma(adesc + koff, blo + koff, 1u);            // A_hi B_lo
+                        mma(alo + koff, bdesc + koff, 1u);            // A_lo B_hi
+                    }
                 }
                 ptx::mma_commit(&empty[st]);
             }
@@ -151,29 +170,31 @@ sym_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 }
 
-template <OpType T>
-cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s,
-                     const EpiParams& e, cudaStream_t stream) {
+template <OpType T, bool kSplit>
+cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
     const int nt = s.npad / kTile;
     dim3 grid(nt * (nt + 1) / 2, s.batch);
-    sym_gemm_kernel<T><<<grid, kThreads, kSmemBytes, stream>>>(tmA, tmB, s, e);
+    sym_gemm_kernel<T, kSplit><<<grid, kThreads, kSmemBytes, stream>>>(m, s, e);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_sym_gemm(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                            const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
+cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
+                            cudaStream_t stream) {
     switch (t) {
-        case OpType::F16: return launch_t<OpType::F16>(tmA, tmB, s, e, stream);
-        case OpType::BF16: return launch_t<OpType::BF16>(tmA, tmB, s, e, stream);
-        case OpType::TF32: return launch_t<OpType::TF32>(tmA, tmB, s, e, stream);
+        case OpType::F16: return split ? launch_t<OpType::F16, true>(m, s, e, stream)
+                                       : launch_t<OpType::F16, false>(m, s, e, stream);
+        case OpType::BF16: return split ? launch_t<OpType::BF16, true>(m, s, e, stream)
+                                        : launch_t<OpType::BF16, false>(m, s, e, stream);
+        case OpType::TF32: return split ? launch_t<OpType::TF32, true>(m, s, e, stream)
+                                        : launch_t<OpType::TF32, false>(m, s, e, stream);
     }
     return cudaErrorInvalidValue;
 }

@@ -29,10 +29,14 @@ namespace {
 
 constexpr int kT2 = 256;                       // output tile edge per CTA pair
 constexpr int kRowsPerCta = 128;
-constexpr int kStages2 = 6;
 constexpr int kThreads2 = 256;                 // 8 warps
-constexpr int kStageBytes = 2 * kRowsPerCta * kBlockKBytes;   // 32 KB (A + B half)
-constexpr int kSmem2 = kStages2 * kStageBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers+ids, staging
+constexpr int kRingBytes = 192 * 1024;         // operand ring per CTA
+// stage = A + B halves (32 KB), or A_hi, B_hi, A_lo, B_lo for split precision (64 KB)
+template <bool kSplit> struct Ring2 {
+    static constexpr int kStageBytes = (kSplit ? 4 : 2) * kRowsPerCta * kBlockKBytes;
+    static constexpr int kStages = kRingBytes / kStageBytes;   // 6 or 3
+};
+constexpr int kSmem2 = kRingBytes + 1024 + 512 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers+ids, staging
 constexpr uint32_t kTmemCols = 512;            // 2 accumulators x 256 fp32 columns
 
 __device__ __forceinline__ void decode_tile(int t, const GemmShape& s, int& b, int& I, int& J) {
@@ -42,11 +46,12 @@ __device__ __forceinline__ void decode_tile(int t, const GemmShape& s, int& b, i
     J = static_cast<int>(code & 0xFFFFu);
 }
 
-template <OpType T>
+template <OpType T, bool kSplit>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
-sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmShape s, const EpiParams e) {
+sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
+    constexpr int kStages2 = Ring2<kSplit>::kStages;
+    constexpr int kStageBytes = Ring2<kSplit>::kStageBytes;
     constexpr int kBK = kBlockKBytes / Tr::kBytes;
     constexpr int kUmmaK = 32 / Tr::kBytes;
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kT2, kT2);
@@ -59,7 +64,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem;                                       // stage st: A at +0, B at +16 KB
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
     uint64_t* empty = full + kStages2;
     uint64_t* tmem_full = empty + kStages2;                     // [2]
     uint64_t* tmem_empty = tmem_full + 2;                       // [2]
@@ -67,7 +72,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint64_t* tile_empty = tile_full + kRing;                   // [kRing]
     uint32_t* tile_id = reinterpret_cast<uint32_t*>(tile_empty + kRing);   // [kRing]
     uint32_t* tmem_slot = tile_id + kRing;
-    uint8_t* epi_smem = smem + kStages2 * kStageBytes + 512;    // 4 x kEpiWarpSmemBytes
+    uint8_t* epi_smem = smem + kRingBytes + 512;                // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -76,8 +81,12 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int num_kb = s.npad / kBK;
 
     if (warp == 0 && ptx::elect_one()) {
-        ptx::tma_prefetch_desc(&tmA);
-        ptx::tma_prefetch_desc(&tmB);
+        ptx::tma_prefetch_desc(&tm.a);
+        ptx::tma_prefetch_desc(&tm.b);
+        if constexpr (kSplit) {
+            ptx::tma_prefetch_desc(&tm.a_lo);
+            ptx::tma_prefetch_desc(&tm.b_lo);
+        }
         for (int i = 0; i < kStages2; ++i) {
             ptx::mbar_init(&full[i], 2);          // leader arrive.expect_tx + peer arrive
             ptx::mbar_init(&empty[i], 1);         // one multicast MMA commit
@@ -143,8 +152,12 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     uint8_t* sa = ring + st * kStageBytes;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
-                    ptx::tma_load_2d_pair_nohint(sa, &tmA, full_leader, kb * kBK, rowA);
-                    ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tmB, full_leader, kb * kBK, rowB);
+                    ptx::tma_load_2d_pair_nohint(sa, &tm.a, full_leader, kb * kBK, rowA);
+                    ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b, full_leader, kb * kBK, rowB);
+                    if constexpr (kSplit) {
+                        ptx::tma_load_2d_pair_nohint(sa + 2 * kTileBytes1, &tm.a_lo, full_leader, kb * kBK, rowA);
+                        ptx::tma_load_2d_pair_nohint(sa + 3 * kTileBytes1, &tm.b_lo, full_leader, kb * kBK, rowB);
+                    }
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
             }
@@ -171,13 +184,22 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
                     const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
                     const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + kTileBytes1);
+                    auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
+                        if constexpr (T == OpType::TF32)
+                            ptx::mma_tf32_pair(d_tmem, a, bb, kIdesc, accumulate);
+                        else
+                            ptx::mma_f16_pair(d_tmem, a, bb, kIdesc, accumulate);
+                    };
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k) {
                         const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
-                        if constexpr (T == OpType::TF32)
-                            ptx::mma_tf32_pair(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
-                        else
-                            ptx::mma_f16_pair(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+                        mma(adesc + koff, bdesc + koff, (kb | k) != 0);
+                        if constexpr (kSplit) {
+                            const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes1);
+                            const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes1);
+                            mma(adesc + koff, blo + koff, 1u);        // A_hi B_lo
+                            mma(alo + koff, bdesc + koff, 1u);        // A_lo B_hi
+                        }
                     }
                     ptx::mma_commit_pair(&empty[st], 0x3);
                     if (kb == num_kb - 1) ptx::mma_commit_pair(&tmem_full[acc], 0x3);
@@ -233,12 +255,11 @@ sym_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     }
 }
 
-template <OpType T>
-cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s, const EpiParams& e,
-                      cudaStream_t stream) {
+template <OpType T, bool kSplit>
+cudaError_t launch2_t(const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
     static int num_sms = 0;
     if (!num_sms) {
-        cudaError_t err = cudaFuncSetAttribute(sym_gemm_2cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_2cta_kernel<T, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
         if (err != cudaSuccess) return err;
         int dev = 0;
         cudaGetDevice(&dev);
@@ -247,7 +268,7 @@ cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gemm
     const int total = s.tiles_per_matrix * s.batch;
     int clusters = num_sms / 2;
     if (clusters > total) clusters = total;
-    sym_gemm_2cta_kernel<T><<<2 * clusters, kThreads2, kSmem2, stream>>>(tmA, tmB, s, e);
+    sym_gemm_2cta_kernel<T, kSplit><<<2 * clusters, kThreads2, kSmem2, stream>>>(m, s, e);
     return cudaGetLastError();
 }
 
@@ -285,12 +306,15 @@ int64_t padded_n(int64_t n, int64_t batch) {
     return (n + m - 1) / m * m;
 }
 
-cudaError_t launch_sym_gemm_2cta(OpType t, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmShape& s,
+cudaError_t launch_sym_gemm_2cta(OpType t, bool split, const OperandMaps& m, const GemmShape& s,
                                  const EpiParams& e, cudaStream_t stream) {
     switch (t) {
-        case OpType::F16: return launch2_t<OpType::F16>(tmA, tmB, s, e, stream);
-        case OpType::BF16: return launch2_t<OpType::BF16>(tmA, tmB, s, e, stream);
-        case OpType::TF32: return launch2_t<OpType::TF32>(tmA, tmB, s, e, stream);
+        case OpType::F16: return split ? launch2_t<OpType::F16, true>(m, s, e, stream)
+                                       : launch2_t<OpType::F16, false>(m, s, e, stream);
+        case OpType::BF16: return split ? launch2_t<OpType::BF16, true>(m, s, e, stream)
+                                        : launch2_t<OpType::BF16, false>(m, s, e, stream);
+        case OpType::TF32: return split ? launch2_t<OpType::TF32, true>(m, s, e, stream)
+                                        : launch2_t<OpType::TF32, false>(m, s, e, stream);
     }
     return cudaErrorInvalidValue;
 }

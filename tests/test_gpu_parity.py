@@ -200,3 +200,38 @@ def test_c4_full_size_structured(pkg):
     for b in [0, 1, 17, 31]:
         ref = spectral.structured_project(blocks[b], *HALF, lam[b])
         assert _rel(P[b], ref) <= TOL["fp16"], (b, _rel(P[b], ref))
+
+
+# FP32-class split path (3 tcgen05 passes hi*hi + hi*lo + lo*hi): BASELINE north star bar 1e-5.
+# bf16x3 carries 2 x 8 significand bits (u ~ 2^-16): bar 1e-4.
+TOL_X3 = {"fp16x3": 1e-5, "tf32x3": 1e-5, "bf16x3": 1e-4}
+
+
+@pytest.mark.parametrize("n,batch,family,which,prec", [
+    (8, 1, "goe", "c1", "fp16x3"),            # config c1 on the FP32-class path
+    (64, 6, "goe", "c2", "fp16x3"),           # config c2 filter meets 5e-3 (and 1e-5) here
+    (256, 2, "sdp_shaped", "single", "fp16x3"),
+    (256, 2, "haar", "single", "tf32x3"),
+    (300, 1, "goe", "half", "bf16x3"),
+    (1024, 8, "goe", "single", "fp16x3"),     # CTA-pair kernel, split
+    (1024, 8, "sdp_shaped", "single", "tf32x3"),
+    (1024, 1, "goe", "c3", "fp16x3"),         # config c3, FP32-class
+])
+def test_split_precision_parity(pkg, n, batch, family, which, prec):
+    X = synth.batch(family, n, batch, synth.SEED_BASE + 5 * n)
+    P, lam, f = _gpu(pkg, _product_filter(which, pkg), X, prec)
+    assert f.status() == "PSD_OK"
+    st, kap = _oracle_filter(which)
+    for b in sorted({0, batch - 1}):
+        ref, _ = chain.project(X[b], st, kap, lam=lam[b])
+        err = _rel(P[b], ref)
+        assert err <= TOL_X3[prec], f"b={b} err={err:.3e}"
+        assert np.array_equal(P[b], P[b].T)
+
+
+def test_split_sign_parity(pkg):
+    X = synth.batch("goe", 512, 2, 77)
+    S, lam, _ = _gpu(pkg, _product_filter("single", pkg), X, "fp16x3", sign=True)
+    for b in range(2):
+        ref, _ = chain.sign(X[b], *SINGLE, lam=lam[b])
+        assert _rel(S[b], ref) <= 1e-5
