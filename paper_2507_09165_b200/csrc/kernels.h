@@ -66,6 +66,24 @@ cudaError_t launch_sym_gemm_2cta(OpType t, bool split, const OperandMaps& m, con
 bool use_pair_kernel(int64_t n, int64_t batch);
 int64_t padded_n(int64_t n, int64_t batch);
 
+// Batched small-n path (n <= 64), the whole chain in one kernel (small_batch.cu).
+struct SmallStep {
+    int slot_a, slot_b;       // byte offsets of the operand slots within a matrix's smem region
+    int slot_d;               // addend slot (-1: none; the fp32 X of a final_mode-1 step is implicit)
+    int slot_out;             // output slot (final_mode 0)
+    float alpha, beta, out_scale;
+    int final_mode;           // 0: chain product; 1: P = lambda~ alpha acc + beta X; 2: S = alpha acc + beta D
+    int reload_x0;            // restage X_0 into the Y slot before this product
+};
+struct SmallPlan {
+    int nsteps;
+    float s_x0;               // operand scale of X_0
+    SmallStep steps[40];
+};
+int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U
+cudaError_t launch_small_batch(bool split, const float* X, float* out, int n, int batch, double* lambda_out,
+                               unsigned* status, const SmallPlan& plan, cudaStream_t stream);
+
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
 int bound_blocks_per_matrix(int n);

@@ -344,6 +344,51 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     }
     double sign_only = 0.0;
     std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
+    if (n <= 64 && h->bound == PSD_BOUND_FROBENIUS && ws.op == OpType::F16 && !steps.empty() &&
+        steps.size() <= 40) {
+        // batched small-n path: the whole chain in one kernel, operands resident in smem
+        const bool sp = ws.split;
+        const double sz = sp ? h->s_z : 1.0, sy = sp ? h->s_y : 1.0, su = sp ? h->s_u : 1.0;
+        auto slot_of = [](int buf) { return buf == B_Y ? 1 : ((buf == B_UA || buf == B_UB) ? 2 : 0); };
+        const double sc_slot[3] = {sz, sy, su};
+        SmallPlan sp_plan{};
+        sp_plan.nsteps = static_cast<int>(steps.size());
+        sp_plan.s_x0 = static_cast<float>(sz);
+        for (size_t i = 0; i < steps.size(); ++i) {
+            const Step& s = steps[i];
+            SmallStep& q = sp_plan.steps[i];
+            int sa = slot_of(s.A), sb = slot_of(s.B);
+            double scale_a = sc_slot[sa], scale_b = sc_slot[sb];
+            q.reload_x0 = 0;
+            q.slot_d = -1;
+            q.beta = static_cast<float>(s.beta);
+            q.out_scale = 1.0f;
+            q.slot_out = 0;
+            if (s.outF && s.D == D_XIN) {              // reconstruction: X_0 restaged in the Y slot
+                q.reload_x0 = 1;
+                sa = 1;
+                scale_a = sz;
+                q.final_mode = 1;
+            } else if (s.outF) {
+                q.final_mode = 2;
+            } else {
+                q.final_mode = 0;
+                q.slot_out = small_slot_offset(sp, slot_of(s.out_op));
+                q.out_scale = static_cast<float>(sc_slot[slot_of(s.out_op)]);
+            }
+            if (s.D >= 0) {
+                q.slot_d = small_slot_offset(sp, slot_of(s.D));
+                q.beta = static_cast<float>(s.beta / sc_slot[slot_of(s.D)]);
+            }
+            q.slot_a = small_slot_offset(sp, sa);
+            q.slot_b = small_slot_offset(sp, sb);
+            q.alpha = static_cast<float>(s.alpha / (scale_a * scale_b));
+        }
+        e = launch_small_batch(sp, X, out, n, batch, lambda_out, ws.status, sp_plan, st);
+        if (e != cudaSuccess) return cuda_fail(e, "small_batch");
+        h->kernel_launches += 1;
+        return PSD_OK;
+    }
     const bool split = ws.split;
     double sc[B_COUNT];
     for (int i = 0; i < B_COUNT; ++i) sc[i] = 1.0;

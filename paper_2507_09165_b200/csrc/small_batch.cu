@@ -1,0 +1,335 @@
+// small_batch.cu -- batched small-n path (n <= 64): the whole of Algorithm 2 for a
+// pair of matrices per CTA iteration, on-chip, HBM touched once for X and once for P.
+//
+//   * bound + scale in-kernel: a CTA stages the two 64x64 fp32 inputs
+//     in smem, reduces ||X||_F per matrix in fp64 (deterministic fixed order) and writes X_0 in
+//     the operand format (SW128 K-major fp16, hi/lo for the split path);
+//   * every product of the chain is tcgen05.mma.cta_group::1 M=64 N=64 K=16 from smem
+//     descriptors into TMEM; the two matrices of the pair use the two half-subpartition
+//     interleaves of one 64-column accumulator (lanes 32w+[0,16) and 32w+[16,32)), so one
+//     tcgen05.ld 32x32b gives each thread one row of one matrix;
+//   * epilogue: alpha*acc + beta*D (D = the rounded operand copy in smem, reading R18), written
+//     back in place into the operand slot (the MMA has completed), fence.proxy.async, barrier;
+//   * reconstruction P = 1/2 X + 1/2 lambda~ X_0 S: X_0 is re-staged from X, and the
+//     result is symmetrised through smem (exact symmetry) and stored to HBM.
+// Two CTAs per SM (96 KB smem each) so one CTA's epilogue overlaps the other's MMAs.
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace psd {
+
+namespace {
+
+constexpr int kN = 64;                  // padded matrix edge
+constexpr int kSlotBytes = kN * 128;    // 64 rows x 128 B (fp16), one SW128 atom wide
+constexpr int kThreadsS = 128;
+
+// byte offset of element (row, col) in a SW128 K-major 64x64 fp16 slot
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+    return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <bool kSplit>
+struct SmallLayout {
+    // per matrix: Z slot, Y slot (hi [+ lo]), U slot (always 16 KB: hi + lo, or fp32 staging)
+    static constexpr int kParts = kSplit ? 2 : 1;
+    static constexpr int kZ = 0;
+    static constexpr int kY = kParts * kSlotBytes;
+    static constexpr int kU = 2 * kParts * kSlotBytes;
+    static constexpr int kPerMatrix = kU + 2 * kSlotBytes;
+    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 128;
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool kSplit>
+__device__ __forceinline__ void store_row(uint8_t* slot, int row, const float (&v)[64], float s) {
+    // hi = rn(v s) [, lo = rn(v s - hi)] into the swizzled slot row
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const float a = v[8 * c + 2 * h] * s, b = v[8 * c + 2 * h + 1] * s;
+            const __half2 hh = __floats2half2_rn(a, b);
+            hi[h] = *reinterpret_cast<const uint32_t*>(&hh);
+            if constexpr (kSplit) {
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+                lo[h] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+        }
+        *reinterpret_cast<uint4*>(slot + swz(row, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        if constexpr (kSplit)
+            *reinterpret_cast<uint4*>(slot + kSlotBytes + swz(row, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
+template <bool kSplit>
+__device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta, float (&v)[64]) {
+    // v += beta * (hi [+ lo]) of the slot row
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint4 h = *reinterpret_cast<const uint4*>(slot + swz(row, c));
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+        float2 lf[4];
+        if constexpr (kSplit) {
+            const uint4 l = *reinterpret_cast<const uint4*>(slot + kSlotBytes + swz(row, c));
+            const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) lf[q] = __half22float2(*reinterpret_cast<const __half2*>(&lw[q]));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
+            if constexpr (kSplit) {
+                f.x += lf[q].x;
+                f.y += lf[q].y;
+            }
+            v[8 * c + 2 * q] += beta * f.x;
+            v[8 * c + 2 * q + 1] += beta * f.y;
+        }
+    }
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kThreadsS, 2)
+small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
+                   double* __restrict__ lambda_out, unsigned* __restrict__ status, const SmallPlan plan) {
+    using L = SmallLayout<kSplit>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
+    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][4 warps]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = lane >> 4;                     // matrix of the pair this thread serves
+    const int row = 16 * warp + (lane & 15);     // its row
+    uint8_t* mat = smem + m * L::kPerMatrix;
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(mma_bar, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<64>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kIdesc = ptx::make_idesc(0, 64, 64);   // f16 x f16 -> f32, M=64, N=64
+    uint32_t mma_phase = 0;
+
+    const int pairs = (batch + 1) / 2;
+    for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        const int b = 2 * pr + m;
+        const bool valid = b < batch;
+        float* stage = reinterpret_cast<float*>(mat + L::kU);   // 64 x 64 fp32 staging (16 KB)
+
+        // ---- stage X (zero padded) for both matrices of the pair into the U slots: coalesced loads
+        auto stage_X = [&]() {
+            const int64_t base = static_cast<int64_t>(2 * pr) * n * n;
+            const int nvalid = min(2, batch - 2 * pr);
+            for (int e = threadIdx.x; e < 2 * kN * kN / 4; e += kThreadsS) {
+                const int mm = e / (kN * kN / 4);
+                const int rem = e - mm * (kN * kN / 4);
+                const int r = rem >> 4, q = rem & 15;
+                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (mm < nvalid && r < n) {
+                    const float* xr = X + base + static_cast<int64_t>(mm) * n * n + static_cast<int64_t>(r) * n;
+                    if (n == kN) {
+                        x = __ldg(reinterpret_cast<const float4*>(xr) + q);
+                    } else {
+                        const int c = 4 * q;
+                        if (c + 0 < n) x.x = __ldg(xr + c + 0);
+                        if (c + 1 < n) x.y = __ldg(xr + c + 1);
+                        if (c + 2 < n) x.z = __ldg(xr + c + 2);
+                        if (c + 3 < n) x.w = __ldg(xr + c + 3);
+                    }
+                }
+                // XOR-swizzle float4 columns by row to keep the transposed reads conflict-light
+                reinterpret_cast<float4*>(smem + mm * L::kPerMatrix + L::kU)[r * 16 + (q ^ (r & 15))] = x;
+            }
+            __syncthreads();
+        };
+        auto stage_at = [&](int r, int c) -> float {      // swizzled staging read
+            return stage[r * kN + (((c >> 2) ^ (r & 15)) << 2) + (c & 3)];
+        };
+        stage_X();
+        double ss = 0.0;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+            if (c >= row) {
+                const double x = stage_at(row, c);                         // upper triangle (R10)
+                ss += (c == row ? 1.0 : 2.0) * x * x;
+            }
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);   // within 16 lanes
+        if ((lane & 15) == 0) red[m * 4 + warp] = ss;
+        __syncthreads();
+        double lam = sqrt(red[m * 4 + 0] + red[m * 4 + 1] + red[m * 4 + 2] + red[m * 4 + 3]);
+        if (!isfinite(lam)) {
+            if ((lane & 15) == 0 && warp == 0 && valid) atomicOr(status, 1u);
+            lam = __longlong_as_double(0x7ff8000000000000LL);
+        }
+        if (valid && warp == 0 && (lane & 15) == 0 && lambda_out) lambda_out[b] = lam;
+        const double inv = lam > 0.0 ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);
+        auto store_x0 = [&](int slot_off) {               // X_0 = sym_upper(X) / lambda~ from staging
+            float x0[64];
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+                const float x = (c >= row) ? stage_at(row, c) : stage_at(c, row);
+                x0[c] = static_cast<float>(static_cast<double>(x) * inv);
+            }
+            store_row<kSplit>(mat + slot_off, row, x0, plan.s_x0);
+        };
+        store_x0(L::kZ);
+        fence_proxy_async_smem();
+        __syncthreads();
+
+        // ---- the chain of products
+        for (int si = 0; si < plan.nsteps; ++si) {
+            const SmallStep st = plan.steps[si];
+            if (st.reload_x0) {
+                // X_0 back into the Y slot for the reconstruction product (Z slot holds S; the
+                // U slots are free again and serve as staging)
+                stage_X();
+                store_x0(L::kY);
+                fence_proxy_async_smem();
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int mm = 0; mm < 2; ++mm) {
+                    uint8_t* mb = smem + mm * L::kPerMatrix;
+                    const uint32_t a = ptx::smem_u32(mb + st.slot_a);
+                    const uint32_t bb = ptx::smem_u32(mb + st.slot_b);
+                    const uint64_t ad = ptx::smem_desc_sw128_kmajor(a), bd = ptx::smem_desc_sw128_kmajor(bb);
+                    const uint32_t d = tmem + (static_cast<uint32_t>(16 * mm) << 16);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
+                        ptx::mma_f16(d, ad + koff, bd + koff, kIdesc, k != 0);
+                        if constexpr (kSplit) {
+                            const uint64_t al = ptx::smem_desc_sw128_kmajor(a + kSlotBytes);
+                            const uint64_t bl = ptx::smem_desc_sw128_kmajor(bb + kSlotBytes);
+                            ptx::mma_f16(d, ad + koff, bl + koff, kIdesc, 1u);
+                            ptx::mma_f16(d, al + koff, bd + koff, kIdesc, 1u);
+                        }
+                    }
+                }
+                ptx::mma_commit(mma_bar);
+            }
+            ptx::mbar_wait(mma_bar, mma_phase);
+            mma_phase ^= 1;
+            ptx::tc_fence_after();
+
+            float v[64];
+            {
+                uint32_t raw[32];
+                const uint32_t ta = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+                ptx::tmem_ld_32x32b_x32(ta, raw);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = st.alpha * __uint_as_float(raw[i]);
+                ptx::tmem_ld_32x32b_x32(ta + 32, raw);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[32 + i] = st.alpha * __uint_as_float(raw[i]);
+            }
+            ptx::tc_fence_before();
+            if (st.slot_d >= 0) add_row<kSplit>(mat + st.slot_d, row, st.beta, v);
+            if (st.final_mode == 0) {
+                // in place: the MMA that read this slot has completed (mma_bar)
+                store_row<kSplit>(mat + st.slot_out, row, v, st.out_scale);
+                fence_proxy_async_smem();
+                __syncthreads();
+            } else {
+                // final: 1/2 X + 1/2 lambda~ X0 S  (mode 1)  or  S (mode 2); symmetrise via staging
+                if (st.final_mode == 1) {
+                    // + beta X[row][c] for c >= row (the lower part is replaced by the mirror below)
+                    const float a = static_cast<float>(lam);
+                    const float* xr = X + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        const float x = (valid && row < n && c < n && c >= row) ? __ldg(xr + c) : 0.0f;
+                        v[c] = a * v[c] + st.beta * x;
+                    }
+                }
+                float4* srow = reinterpret_cast<float4*>(stage + row * kN);
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                __syncthreads();
+                if (valid && row < n) {
+                    float* orow = out + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
+                    if (n == kN) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            float4 o;
+                            o.x = (4 * q + 0 >= row) ? stage_at(row, 4 * q + 0) : stage_at(4 * q + 0, row);
+                            o.y = (4 * q + 1 >= row) ? stage_at(row, 4 * q + 1) : stage_at(4 * q + 1, row);
+                            o.z = (4 * q + 2 >= row) ? stage_at(row, 4 * q + 2) : stage_at(4 * q + 2, row);
+                            o.w = (4 * q + 3 >= row) ? stage_at(row, 4 * q + 3) : stage_at(4 * q + 3, row);
+                            __stcs(reinterpret_cast<float4*>(orow) + q, o);
+                        }
+                    } else {
+                        for (int c = 0; c < n; ++c) orow[c] = (c >= row) ? stage_at(row, c) : stage_at(c, row);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<64>(tmem);
+    }
+}
+
+template <bool kSplit>
+cudaError_t launch_small_t(const float* X, float* out, int n, int batch, double* lambda_out, unsigned* status,
+                           const SmallPlan& plan, cudaStream_t stream) {
+    using L = SmallLayout<kSplit>;
+    static int num_sms = 0;
+    if (!num_sms) {
+        cudaError_t err = cudaFuncSetAttribute(small_batch_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               L::kBytes);
+        if (err != cudaSuccess) return err;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int pairs = (batch + 1) / 2;
+    int grid = 2 * num_sms;
+    if (grid > pairs) grid = pairs;
+    small_batch_kernel<kSplit><<<grid, kThreadsS, L::kBytes, stream>>>(X, out, n, batch, lambda_out, status, plan);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int small_slot_offset(bool split, int slot) {
+    if (split) {
+        using L = SmallLayout<true>;
+        return slot == 0 ? L::kZ : (slot == 1 ? L::kY : L::kU);
+    }
+    using L = SmallLayout<false>;
+    return slot == 0 ? L::kZ : (slot == 1 ? L::kY : L::kU);
+}
+
+cudaError_t launch_small_batch(bool split, const float* X, float* out, int n, int batch, double* lambda_out,
+                               unsigned* status, const SmallPlan& plan, cudaStream_t stream) {
+    return split ? launch_small_t<true>(X, out, n, batch, lambda_out, status, plan, stream)
+                 : launch_small_t<false>(X, out, n, batch, lambda_out, status, plan, stream);
+}
+
+}  // namespace psd

@@ -238,3 +238,40 @@ def test_split_sign_parity(pkg):
     for b in range(2):
         ref, _ = chain.sign(X[b], *SINGLE, lam=lam[b])
         assert _rel(S[b], ref) <= 1e-5
+
+
+@pytest.mark.parametrize("n,batch,family,which,prec", [
+    (64, 4096, "goe", "c2", "fp16x3"),        # config c2, bench launch configuration
+    (64, 4096, "goe", "c2", "fp16"),
+    (8, 3, "goe", "c1", "fp16x3"),            # config c1 through the small path, odd batch
+    (33, 7, "sdp_shaped", "half", "fp16x3"),  # ragged n (zero padded to 64)
+    (50, 5, "haar", "single", "fp16"),
+])
+def test_small_batch_parity(pkg, n, batch, family, which, prec):
+    """Batched small-n kernel (n <= 64): whole chain on-chip; sampled matrices vs oracle,
+    every output exactly symmetric."""
+    X = synth.batch(family, n, batch, synth.SEED_BASE + 11 * n) if batch <= 64 else \
+        np.stack([synth.goe(n, synth.SEED_BASE + 7 * b) for b in range(batch)])
+    P, lam, f = _gpu(pkg, _product_filter(which, pkg), X, prec)
+    assert f.status() == "PSD_OK"
+    st, kap = _oracle_filter(which)
+    bar = (5e-5 if which == "c2" else 1e-5) if prec == "fp16x3" else tol(prec, n, which)
+    for b in sorted({0, 1, batch // 2, batch - 1}):
+        assert abs(lam[b] - chain.frobenius_bound(X[b])) <= 1e-12 * lam[b]
+        ref, _ = chain.project(X[b], st, kap, lam=lam[b])
+        err = _rel(P[b], ref)
+        assert err <= bar, f"b={b} err={err:.3e}"
+    assert all(np.array_equal(P[b], P[b].T) for b in range(0, batch, max(1, batch // 64)))
+
+
+def test_small_batch_sign_and_nonfinite(pkg):
+    X = synth.batch("goe", 40, 4, 123)
+    S, lam, f = _gpu(pkg, _product_filter("half", pkg), X, "fp16x3", sign=True)
+    for b in range(4):
+        ref, _ = chain.sign(X[b], *HALF, lam=lam[b])
+        assert _rel(S[b], ref) <= 1e-5
+        assert np.array_equal(S[b], S[b].T)
+    Xn = X.copy()
+    Xn[2, 5, 9] = np.inf
+    _, lam, f = _gpu(pkg, _product_filter("half", pkg), Xn, "fp16")
+    assert f.status() == "PSD_ENONFINITE" and np.isnan(lam[2])
