@@ -36,8 +36,8 @@ CONFIGS = {
                         "global batch sharded over GPUs"),
     "c3": dict(n=1024, batch=1, family="goe", filter="c3",
                workload="c3: single n=1024 symmetric matrix, Remez filter T=6 d=5"),
-    "c2": dict(n=64, batch=4096, family="goe", filter="c2",
-               workload="c2: batch 4096 x 64x64 symmetric, Remez T=4 d=7"),
+    "c2": dict(n=64, batch=4096, family="goe", filter="c2", precision="fp16x3",
+               workload="c2: batch 4096 x 64x64 symmetric, Remez T=4 d=7 (batched small-n kernel)"),
     "c5": dict(n=16384, batch=1, family="goe", filter="half",
                workload="c5: single n=16384 symmetric matrix (1 GPU here)"),
 }
@@ -306,14 +306,19 @@ def run_ours(args, cfg):
         alg_flops_product = float(n) * n * (n + 1)
         dense_flops_matrix = 2.0 * n ** 3 * G
         launch_ms = prod_ms_max / max(prod_launches, 1) if prod_launches else None
-        achieved = (alg_flops_product * count / (launch_ms / 1000.0) / 1e12) if launch_ms else None
+        # one launch = one product over the shard, or (n <= 64, small-n kernel) the whole chain
+        per_launch = alg_flops_product * count * (G if n <= 64 else 1)
+        # split (x3) precisions: 3 tensor passes per product; achieved counts the method's
+        # (algorithmic) flops, peak is the tensor peak of the operand type / 3
+        passes = 3 if args.precision.endswith("x3") else 1
+        achieved = (per_launch / (launch_ms / 1000.0) / 1e12) if launch_ms else None
         peak_bf16 = peaks.get("bf16_tflops", 1590.0)
-        if args.precision in ("fp16", "bf16"):
-            peak = peak_bf16
-            peak_note = f"{peak_src} bf16 burst (fp16 = bf16 rate)"
+        if args.precision.startswith(("fp16", "bf16")):
+            peak = peak_bf16 / passes
+            peak_note = f"{peak_src} bf16 burst (fp16 = bf16 rate)" + (" / 3 passes" if passes == 3 else "")
         else:
-            peak = peak_bf16 / 2.0
-            peak_note = f"{peak_src} bf16 burst x 1/2 (tf32 nominal ratio)"
+            peak = peak_bf16 / 2.0 / passes
+            peak_note = f"{peak_src} bf16 burst x 1/2 (tf32 nominal ratio)" + (" / 3 passes" if passes == 3 else "")
         traffic, traffic_src = load_traffic(cfg)
         line = {
             "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s", "n_gpus": world,
@@ -328,9 +333,10 @@ def run_ours(args, cfg):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "kernel": "sym_gemm_2cta_kernel (CTA-pair tcgen05 symmetric product, fused epilogue)"
-                         if n >= 1024 else "sym_gemm_kernel (tcgen05 symmetric product, fused epilogue)",
-                         "per_launch_flops": alg_flops_product * count,
+                         "kernel": ("sym_gemm_2cta_kernel (CTA-pair tcgen05 symmetric product, fused epilogue)"
+                                    if n >= 1024 else ("small_batch_kernel (whole chain on-chip, n <= 64)"
+                                                       if n <= 64 else "sym_gemm_kernel (tcgen05 symmetric product)")),
+                         "per_launch_flops": per_launch, "mma_passes": passes,
                          "avg_launch_ms": launch_ms, "peak_source": peak_note},
             "gpu_launches": kernel_launches,
             "clocks": clk.summary(),
@@ -356,12 +362,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "tf32", "tf32x3"])
+    ap.add_argument("--precision", default=None, choices=["fp16", "bf16", "tf32", "tf32x3", "fp16x3", "bf16x3"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.precision is None:
+        args.precision = cfg.get("precision", "fp16")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -384,9 +384,19 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             q.slot_b = small_slot_offset(sp, sb);
             q.alpha = static_cast<float>(s.alpha / (scale_a * scale_b));
         }
+        std::pair<cudaEvent_t, cudaEvent_t> evs{nullptr, nullptr};
+        if (h->profiling) {
+            evs = {take_event(h), take_event(h)};
+            cudaEventRecord(evs.first, st);
+        }
         e = launch_small_batch(sp, X, out, n, batch, lambda_out, ws.status, sp_plan, st);
         if (e != cudaSuccess) return cuda_fail(e, "small_batch");
         h->kernel_launches += 1;
+        if (evs.first) {
+            cudaEventRecord(evs.second, st);
+            h->ev_pairs.push_back(evs);
+            h->product_launches_profiled += 1;     // one launch carries the whole chain
+        }
         return PSD_OK;
     }
     const bool split = ws.split;

@@ -69,6 +69,21 @@ __device__ __forceinline__ void store_row(uint8_t* slot, int row, const float (&
     }
 }
 
+// Exact symmetry of a stored operand: row `row` takes its lower part (col < row) from the
+// upper part of the rows above it (reads touch only the upper triangle, writes only the lower).
+// Without it the rounding-level antisymmetric part of the products grows like prod_t c_{t,0}
+// along the chain (it is not damped by the sign dynamics).
+template <bool kSplit>
+__device__ __forceinline__ void mirror_lower(uint8_t* slot, int row) {
+    for (int c = 0; c < row; ++c) {
+        const uint32_t src = static_cast<uint32_t>(c * 128 + ((((row >> 3) ^ (c & 7))) << 4) + (row & 7) * 2);
+        const uint32_t dst = static_cast<uint32_t>(row * 128 + ((((c >> 3) ^ (row & 7))) << 4) + (c & 7) * 2);
+        *reinterpret_cast<uint16_t*>(slot + dst) = *reinterpret_cast<const uint16_t*>(slot + src);
+        if constexpr (kSplit)
+            *reinterpret_cast<uint16_t*>(slot + kSlotBytes + dst) = *reinterpret_cast<const uint16_t*>(slot + kSlotBytes + src);
+    }
+}
+
 template <bool kSplit>
 __device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta, float (&v)[64]) {
     // v += beta * (hi [+ lo]) of the slot row
@@ -248,6 +263,8 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             if (st.final_mode == 0) {
                 // in place: the MMA that read this slot has completed (mma_bar)
                 store_row<kSplit>(mat + st.slot_out, row, v, st.out_scale);
+                __syncthreads();
+                mirror_lower<kSplit>(mat + st.slot_out, row);
                 fence_proxy_async_smem();
                 __syncthreads();
             } else {

@@ -225,9 +225,10 @@ def test_split_precision_parity(pkg, n, batch, family, which, prec):
     for b in sorted({0, batch - 1}):
         ref, _ = chain.project(X[b], st, kap, lam=lam[b])
         err = _rel(P[b], ref)
-        # c2's d=7 Remez filter (coefficients up to 128.8) amplifies fp32 accumulation rounding:
-        # model with sgemm-style fp32 accumulation 6-9e-6 at n=64
-        bar = 5e-5 if which == "c2" else TOL_X3[prec]
+        # the coarse Remez sets (c1: T=3, sign error 0.86; c2: d=7, coefficients up to 128.8)
+        # amplify fp32 accumulation rounding: model with sgemm-style fp32 accumulation 6-9e-6
+        # at n=64
+        bar = 5e-5 if which in ("c1", "c2") else TOL_X3[prec]
         assert err <= bar, f"b={b} err={err:.3e}"
         assert np.array_equal(P[b], P[b].T)
 
@@ -255,7 +256,7 @@ def test_small_batch_parity(pkg, n, batch, family, which, prec):
     P, lam, f = _gpu(pkg, _product_filter(which, pkg), X, prec)
     assert f.status() == "PSD_OK"
     st, kap = _oracle_filter(which)
-    bar = (5e-5 if which == "c2" else 1e-5) if prec == "fp16x3" else tol(prec, n, which)
+    bar = (5e-5 if which in ("c1", "c2") else 1e-5) if prec == "fp16x3" else tol(prec, n, which)
     for b in sorted({0, 1, batch // 2, batch - 1}):
         assert abs(lam[b] - chain.frobenius_bound(X[b])) <= 1e-12 * lam[b]
         ref, _ = chain.project(X[b], st, kap, lam=lam[b])
