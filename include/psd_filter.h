@@ -162,6 +162,36 @@ psd_status_t psd_profile(psd_filter_t h, int enable);
 psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* product_launches,
                               int64_t* kernel_launches);
 
+/* ---------------------------------------------------------------- multi-GPU (row panels)
+ * One large n over P GPUs, one process per GPU.  Every
+ * product of the chain is split over the ranks by upper 256-tiles (rank r computes a balanced,
+ * disjoint share), the packed tiles are all-gathered over NCCL (NVLink / NVSwitch) and every
+ * rank rebuilds the exactly symmetric full operand; the input rows are all-gathered once.
+ * NCCL is the library torch already loaded (libnccl.so.2), resolved at run time. */
+
+/* Fills id[128] with a new NCCL unique id (call on one rank, broadcast the bytes). */
+psd_status_t psd_nccl_unique_id(char id[128]);
+/* Creates this rank's NCCL communicator (collective over the nranks processes). */
+psd_status_t psd_nccl_comm_create(const char id[128], int nranks, int rank, void** comm);
+psd_status_t psd_nccl_comm_destroy(void* comm);
+
+/* Row-panel projection: rank `rank` of `nranks` passes rows [rank*n/nranks, (rank+1)*n/nranks)
+ * of X (device fp32, row-major, n columns; the full X must be symmetric -- its upper triangle is
+ * what is used) and receives the same rows of P (or of S when want_sign).  n % nranks == 0.
+ * Precisions FP16, BF16, TF32.  Collective: every rank must call it with the same filter and n. */
+psd_status_t psd_project_rowpanel(psd_filter_t h, const float* X_rows, int64_t n, int rank, int nranks,
+                                  float* out_rows, int want_sign, void* comm, void* stream);
+
+/* The same per-rank code with `nranks` virtual ranks in this process on this GPU (the
+ * all-gather becomes shared memory): X and out are the full n x n matrices. Test path. */
+psd_status_t psd_project_rowpanel_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
+                                          int want_sign, void* stream);
+
+/* Host helper: the upper 256-tiles rank `rank` computes, as (I << 16) | J codes in its packed
+ * order, padded with 0xFFFFFFFF to the common per-rank count.  Returns the real count (codes ==
+ * NULL: returns the padded per-rank count). */
+int psd_rowpanel_tiles(int64_t n, int nranks, int rank, uint32_t* codes, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ X_T (the matrix-sign approximation), ``gemm_count`` the GEMM budget.
 """
 import ctypes
 
-from . import filters  # noqa: F401
+from . import dist, filters  # noqa: F401
 from ._lib import BOUNDS, PRECISIONS, PsdError, check, load  # noqa: F401
 
 __all__ = ["Filter", "filters", "PsdError", "version"]
@@ -131,6 +131,22 @@ class Filter:
         check(self._lib.psd_profile_read(self._h, ctypes.byref(ms), ctypes.byref(pl), ctypes.byref(kl)),
               "psd_profile_read")
         return ms.value, pl.value, kl.value
+
+    def project_rowpanel_virtual(self, X, nranks, out=None, sign=False, stream=None):
+        """Row-panel projection of one n x n matrix with `nranks` virtual ranks on this GPU (the
+        per-rank code of the multi-GPU path; see dist.RowPanelProjector for real ranks)."""
+        import torch
+        Xb = _check_matrix(X)
+        if Xb.shape[0] != 1:
+            raise ValueError("row panels project one matrix")
+        if out is None:
+            out = torch.empty_like(X)
+        n = Xb.shape[-1]
+        check(self._lib.psd_project_rowpanel_virtual(self._h, ctypes.c_void_p(Xb.data_ptr()), n, int(nranks),
+                                                     ctypes.c_void_p(_check_matrix(out).data_ptr()),
+                                                     1 if sign else 0, _stream_ptr(stream)),
+              "psd_project_rowpanel_virtual")
+        return out
 
     def sym_product(self, A, B, D=None, alpha=1.0, beta=0.0, out=None, stream=None):
         """C = alpha (A B) + beta D for commuting symmetric A, B (upper triangles read)."""

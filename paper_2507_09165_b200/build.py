@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libpsdfilter.so")
-SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "bound_scale.cu", "small_batch.cu"]
+SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "bound_scale.cu", "small_batch.cu", "rowpanel.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
@@ -46,7 +46,7 @@ def build(verbose=False, force=False):
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed for " + src)
     if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

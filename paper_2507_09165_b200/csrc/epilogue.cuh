@@ -88,7 +88,8 @@ __device__ __forceinline__ void store_op_mirrored(void* out, int64_t opBase, int
 
 template <OpType T>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
-                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem) {
+                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem,
+                                               int64_t packed_off = -1) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     const int lane = threadIdx.x & 31;
@@ -183,6 +184,34 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 v[i] += (row_ok && gj < e.nDf && gj >= gi) ? e.beta * drow[gj] : 0.0f;
             }
         }
+    }
+
+    if (packed_off >= 0) {
+        // row-panel mode: this warp's 32 x 32 block of the tile, unmirrored, row-major tile slot
+        // (row stride 256); the lower part of a diagonal tile is never read by the unpack
+        const int64_t o = packed_off + static_cast<int64_t>(lane) * 256;
+        if (e.packed_f32) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.packed) + o);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        } else if constexpr (Tr::kBytes == 2) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<op_t*>(e.packed) + o);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    w[h] = Tr::pack2(v[q * 8 + 2 * h] * e.out_scale, v[q * 8 + 2 * h + 1] * e.out_scale);
+                __stcs(dst + q, make_uint4(w[0], w[1], w[2], w[3]));
+            }
+        } else {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<op_t*>(e.packed) + o);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                __stcs(dst + q, make_float4(Tr::cvt(v[4 * q] * e.out_scale), Tr::cvt(v[4 * q + 1] * e.out_scale),
+                                            Tr::cvt(v[4 * q + 2] * e.out_scale), Tr::cvt(v[4 * q + 3] * e.out_scale)));
+        }
+        return;
     }
 
     if (e.out_op) {

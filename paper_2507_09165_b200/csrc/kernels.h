@@ -32,6 +32,11 @@ struct EpiParams {
     float* outF;              // final fp32 output, full mirrored, masked to nF (or NULL)
     int64_t ldF, strideF;
     int nF;
+    // Row-panel (multi-GPU) mode, CTA-pair kernel only: instead of the mirrored stores, tile slot
+    // t of the launch is written, unmirrored and row-major, at packed + t * 256 * 256 (elements):
+    // operand precision (out_op ignored) or fp32 when packed_f32.
+    void* packed;
+    int packed_f32;
 };
 
 struct GemmShape {
@@ -83,6 +88,11 @@ struct SmallPlan {
 int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U
 cudaError_t launch_small_batch(bool split, const float* X, float* out, int n, int batch, double* lambda_out,
                                unsigned* status, const SmallPlan& plan, cudaStream_t stream);
+
+// Row-panel multi-GPU path (rowpanel.cu).
+cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
+                                int64_t ld, cudaStream_t stream);
+int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap);
 
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.

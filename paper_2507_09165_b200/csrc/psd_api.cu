@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <dlfcn.h>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,6 +75,17 @@ struct psd_filter_s {
     Workspace ws;
     // power-of-two operand scales of the fp16 split path: Z iterates, Y = Z^2, Horner U
     double s_z = 1.0, s_y = 1.0, s_u = 1.0;
+    // row-panel (multi-GPU) workspace
+    struct RowPanel {
+        int npad = 0, nranks = 0, per = 0, n = 0;
+        OpType op = OpType::F16;
+        float* xg = nullptr;            // gathered X, n x n fp32
+        float* pfull = nullptr;         // unpacked final product, npad x npad fp32
+        void* packed_op = nullptr;      // [nranks * per][256 * 256] operand precision
+        float* packed_f32 = nullptr;    // [nranks * per][256 * 256] fp32 (final product)
+        uint32_t* codes = nullptr;      // [nranks][per] tile codes (gather order)
+        std::vector<int> counts;        // real tiles per rank
+    } rp;
     // profiling / launch accounting
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -470,6 +482,199 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     return PSD_OK;
 }
 
+// ---------------------------------------------------------------- NCCL (resolved at run time)
+struct NcclApi {
+    using GetUniqueId = int (*)(void*);
+    using CommInitRank = int (*)(void**, int, char[128], int);
+    using AllGather = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+    using CommDestroy = int (*)(void*);
+    using GetErrorString = const char* (*)(int);
+    GetUniqueId get_unique_id = nullptr;
+    CommInitRank comm_init_rank = nullptr;
+    AllGather all_gather = nullptr;
+    CommDestroy comm_destroy = nullptr;
+    GetErrorString error_string = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // the copy torch loaded
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (lib) {
+            api.get_unique_id = reinterpret_cast<NcclApi::GetUniqueId>(dlsym(lib, "ncclGetUniqueId"));
+            api.comm_init_rank = reinterpret_cast<NcclApi::CommInitRank>(dlsym(lib, "ncclCommInitRank"));
+            api.all_gather = reinterpret_cast<NcclApi::AllGather>(dlsym(lib, "ncclAllGather"));
+            api.comm_destroy = reinterpret_cast<NcclApi::CommDestroy>(dlsym(lib, "ncclCommDestroy"));
+            api.error_string = reinterpret_cast<NcclApi::GetErrorString>(dlsym(lib, "ncclGetErrorString"));
+            api.ok = api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy;
+        }
+    }
+    return api;
+}
+
+constexpr int kNcclInt8 = 0;   // byte-count all-gathers: ncclInt8
+
+psd_status_t nccl_fail(int rc, const char* where) {
+    const char* m = nccl().error_string ? nccl().error_string(rc) : "?";
+    return fail(PSD_ENCCL, std::string(where) + ": " + m);
+}
+
+void free_rowpanel_ws(psd_filter_s::RowPanel& rp) {
+    if (rp.xg) cudaFree(rp.xg);
+    if (rp.pfull) cudaFree(rp.pfull);
+    if (rp.packed_op) cudaFree(rp.packed_op);
+    if (rp.packed_f32) cudaFree(rp.packed_f32);
+    if (rp.codes) cudaFree(rp.codes);
+    rp = psd_filter_s::RowPanel();
+}
+
+void free_rowpanel(psd_filter_s* h) {
+    if (h->rp.codes) {
+        cudaDeviceSynchronize();
+        free_rowpanel_ws(h->rp);
+    }
+}
+
+psd_status_t ensure_rowpanel(psd_filter_s* h, int n, int nranks) {
+    auto& rp = h->rp;
+    const int npad = (n + 255) / 256 * 256;
+    const OpType op = op_of(h->prec);
+    if (rp.npad == npad && rp.n == n && rp.nranks == nranks && rp.op == op && rp.codes) return PSD_OK;
+    if (rp.codes) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    }
+    free_rowpanel_ws(rp);
+    const int nt = npad / 256;
+    const int per = rowpanel_tiles(nt, nranks, 0, nullptr, 0);
+    std::vector<uint32_t> codes(static_cast<size_t>(nranks) * per);
+    rp.counts.resize(nranks);
+    for (int r = 0; r < nranks; ++r) rp.counts[r] = rowpanel_tiles(nt, nranks, r, codes.data() + r * per, per);
+    const size_t tiles = static_cast<size_t>(nranks) * per;
+    if (cudaMalloc(&rp.xg, static_cast<size_t>(n) * n * 4) != cudaSuccess ||
+        cudaMalloc(&rp.pfull, static_cast<size_t>(npad) * npad * 4) != cudaSuccess ||
+        cudaMalloc(&rp.packed_op, tiles * 65536 * op_bytes(op)) != cudaSuccess ||
+        cudaMalloc(&rp.packed_f32, tiles * 65536 * 4) != cudaSuccess ||
+        cudaMalloc(&rp.codes, codes.size() * 4) != cudaSuccess) {
+        free_rowpanel_ws(rp);
+        return fail(PSD_ENOMEM, "cudaMalloc row-panel workspace failed");
+    }
+    cudaMemcpy(rp.codes, codes.data(), codes.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemset(rp.pfull, 0, static_cast<size_t>(npad) * npad * 4);
+    rp.npad = npad;
+    rp.n = n;
+    rp.nranks = nranks;
+    rp.per = per;
+    rp.op = op;
+    return PSD_OK;
+}
+
+// Row-panel Algorithm 2.  comm == nullptr: `nranks` virtual ranks in this process (X, out full).
+psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank, int nranks, float* out,
+                          bool want_sign, void* comm, cudaStream_t st) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (!X || !out) return fail(PSD_EINVAL, "null X or out");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PSD_EINVAL, "bad rank / nranks");
+    if (n64 < 256 || n64 > 65536 || n64 % nranks) return fail(PSD_EINVAL, "row panels need 256 <= n, n % nranks == 0");
+    if (split_of(h->prec)) return fail(PSD_EUNSUPPORTED, "row panels: FP16, BF16, TF32 only");
+    if (h->bound != PSD_BOUND_FROBENIUS) return fail(PSD_EUNSUPPORTED, "row panels: Frobenius bound only");
+    if (comm && !nccl().ok) return fail(PSD_ENCCL, "libnccl.so.2 not available");
+    const int n = static_cast<int>(n64);
+    const int npad = (n + 255) / 256 * 256;
+    psd_status_t rc = ensure_ws(h, npad, 1);
+    if (rc != PSD_OK) return rc;
+    rc = ensure_rowpanel(h, n, nranks);
+    if (rc != PSD_OK) return rc;
+    Workspace& ws = h->ws;
+    auto& rp = h->rp;
+    const int rows = n / nranks;
+    cudaError_t e;
+    // (1) the full X on every rank (one all-gather of the input rows)
+    const float* Xf = X;
+    if (comm) {
+        e = cudaMemcpyAsync(rp.xg + static_cast<int64_t>(rank) * rows * n, X, static_cast<size_t>(rows) * n * 4,
+                            cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "row copy");
+        int r = nccl().all_gather(rp.xg + static_cast<int64_t>(rank) * rows * n, rp.xg,
+                                  static_cast<size_t>(rows) * n * 4, kNcclInt8, comm, st);
+        if (r != 0) return nccl_fail(r, "ncclAllGather(X)");
+        Xf = rp.xg;
+    }
+    // (2) bound (identical on every rank) and (3) scale + convert into the full X_0
+    const int nblk = bound_blocks_per_matrix(n);
+    e = launch_frobenius_partials(Xf, n, 1, ws.partial, nblk, st);
+    if (e == cudaSuccess) e = launch_finalize_bound(ws.partial, nblk, 1, ws.lambda, nullptr, ws.status, st);
+    if (e == cudaSuccess)
+        e = launch_scale_convert(ws.op, Xf, n, npad, 1, ws.lambda, 1.0, ws.op_buf[B_X0], nullptr, 1.0, nullptr, 0.0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bound / scale");
+    h->kernel_launches += 3;
+    double sign_only = 0.0;
+    std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
+    if (steps.empty()) return fail(PSD_EUNSUPPORTED, "row panels: filter without products");
+    if (steps.size() * nranks > static_cast<size_t>(kMaxSteps)) return fail(PSD_EUNSUPPORTED, "too many products");
+    e = cudaMemsetAsync(ws.counters, 0, steps.size() * nranks * sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    const int ob = op_bytes(ws.op);
+    const size_t tile_elems = 65536;
+    // (4) the products: each rank its upper tiles, packed; all-gather; unpack on every rank
+    for (size_t si = 0; si < steps.size(); ++si) {
+        const Step& s = steps[si];
+        EpiParams ep{};
+        ep.alpha = static_cast<float>(s.alpha);
+        ep.alpha_dev = s.alpha_lambda ? ws.lambda : nullptr;
+        ep.beta = static_cast<float>(s.beta);
+        ep.out_scale = 1.0f;
+        if (s.D >= 0) {
+            ep.Dop = ws.op_buf[s.D];
+        } else if (s.D == D_XIN) {
+            ep.Df = Xf;
+            ep.ldDf = n;
+            ep.strideDf = static_cast<int64_t>(n) * n;
+            ep.nDf = n;
+        }
+        ep.packed_f32 = s.outF ? 1 : 0;
+        OperandMaps m;
+        m.a = ws.tmap[s.A];
+        m.b = ws.tmap[s.B];
+        m.a_lo = m.a;
+        m.b_lo = m.b;
+        const int r0 = comm ? rank : 0, r1 = comm ? rank + 1 : nranks;
+        for (int vr = r0; vr < r1; ++vr) {
+            const size_t slot0 = static_cast<size_t>(vr) * rp.per * tile_elems;
+            ep.packed = s.outF ? static_cast<void*>(rp.packed_f32 + slot0)
+                               : static_cast<void*>(static_cast<uint8_t*>(rp.packed_op) + slot0 * ob);
+            GemmShape shape{npad, 1, rp.codes + static_cast<size_t>(vr) * rp.per, rp.counts[vr],
+                            ws.counters + si * nranks + vr};
+            if (rp.counts[vr] == 0) continue;
+            e = launch_sym_gemm_2cta(ws.op, false, m, shape, ep, st);
+            if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (row panel)");
+            h->kernel_launches += 1;
+        }
+        const size_t bytes_rank = static_cast<size_t>(rp.per) * tile_elems * (s.outF ? 4 : ob);
+        void* gathered = s.outF ? static_cast<void*>(rp.packed_f32) : rp.packed_op;
+        if (comm) {
+            int r = nccl().all_gather(static_cast<uint8_t*>(gathered) + rank * bytes_rank, gathered, bytes_rank,
+                                      kNcclInt8, comm, st);
+            if (r != 0) return nccl_fail(r, "ncclAllGather(tiles)");
+        }
+        e = launch_unpack_tiles(s.outF ? 4 : ob, gathered, rp.codes, nranks * rp.per,
+                                s.outF ? static_cast<void*>(rp.pfull) : ws.op_buf[s.out_op], npad, st);
+        if (e != cudaSuccess) return cuda_fail(e, "unpack");
+        h->kernel_launches += 1;
+    }
+    // (5) this rank's rows (all rows for the virtual ranks) of the result
+    const int row0 = comm ? rank * rows : 0;
+    const int nrows = comm ? rows : n;
+    e = cudaMemcpy2DAsync(out, static_cast<size_t>(n) * 4, rp.pfull + static_cast<size_t>(row0) * npad,
+                          static_cast<size_t>(npad) * 4, static_cast<size_t>(n) * 4, nrows, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "result copy");
+    return PSD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -512,6 +717,7 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
 
 void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
+    free_rowpanel(h);
     for (auto& p : h->ev_pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto& e : h->ev_pool) cudaEventDestroy(e);
     if (h->ws.status) {
@@ -600,6 +806,46 @@ psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* produ
     h->product_launches_profiled = 0;
     h->kernel_launches = 0;
     return PSD_OK;
+}
+
+psd_status_t psd_nccl_unique_id(char id[128]) {
+    if (!id) return fail(PSD_EINVAL, "null id");
+    if (!nccl().ok) return fail(PSD_ENCCL, "libnccl.so.2 not available");
+    int r = nccl().get_unique_id(id);
+    return r ? nccl_fail(r, "ncclGetUniqueId") : PSD_OK;
+}
+
+psd_status_t psd_nccl_comm_create(const char id[128], int nranks, int rank, void** comm) {
+    if (!id || !comm) return fail(PSD_EINVAL, "null id or comm");
+    if (!nccl().ok) return fail(PSD_ENCCL, "libnccl.so.2 not available");
+    char buf[128];
+    std::memcpy(buf, id, 128);
+    int r = nccl().comm_init_rank(comm, nranks, buf, rank);
+    return r ? nccl_fail(r, "ncclCommInitRank") : PSD_OK;
+}
+
+psd_status_t psd_nccl_comm_destroy(void* comm) {
+    if (!comm) return PSD_OK;
+    if (!nccl().ok) return fail(PSD_ENCCL, "libnccl.so.2 not available");
+    int r = nccl().comm_destroy(comm);
+    return r ? nccl_fail(r, "ncclCommDestroy") : PSD_OK;
+}
+
+psd_status_t psd_project_rowpanel(psd_filter_t h, const float* X_rows, int64_t n, int rank, int nranks,
+                                  float* out_rows, int want_sign, void* comm, void* stream) {
+    if (!comm) return fail(PSD_EINVAL, "null communicator");
+    return run_rowpanel(h, X_rows, n, rank, nranks, out_rows, want_sign != 0, comm, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_project_rowpanel_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
+                                          int want_sign, void* stream) {
+    return run_rowpanel(h, X, n, 0, nranks, out, want_sign != 0, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int psd_rowpanel_tiles(int64_t n, int nranks, int rank, uint32_t* codes, int cap) {
+    if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
+    const int nt = static_cast<int>((n + 255) / 256);
+    return rowpanel_tiles(nt, nranks, rank, codes, cap);
 }
 
 psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, const float* D, double alpha,

@@ -1,0 +1,100 @@
+// rowpanel.cu -- device side of the row-panel (multi-GPU) path, SURVEY.md section 8(e) config c5.
+//
+// Every product of Algorithm 2 is split over the ranks by upper 256-tiles: rank r
+// computes a balanced, disjoint share of the upper tiles (I <= J) and writes them packed and
+// unmirrored (epilogue packed mode); an in-place all-gather of the packed buffers gives every
+// rank every upper tile (the upper triangle only: half the bytes of gathering row panels);
+// this unpack kernel rebuilds the full, exactly symmetric operand on every rank -- the same
+// deterministic rule everywhere, so all ranks hold bit-identical operands.  Exact symmetry of
+// the operands is required: a rounding-level antisymmetric part grows like prod_t c_{t,0}
+// along the chain (reading R20).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+
+namespace psd {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kBand = 32;        // rows of a tile per block
+
+// One block per (tile, 32-row band): direct copy of the band into full[I*256 + band rows][J*256 ..]
+// and the transposed band into full[J*256 ..][I*256 + band rows] through smem.
+template <typename E>
+__global__ void __launch_bounds__(256)
+unpack_tiles_kernel(const E* __restrict__ packed, const uint32_t* __restrict__ codes, int ntiles, E* __restrict__ full,
+                    int64_t ld) {
+    __shared__ E S[kBand][kT + 16 / sizeof(E)];
+    const int tile = blockIdx.x / (kT / kBand);
+    const int band = blockIdx.x % (kT / kBand);
+    if (tile >= ntiles) return;
+    const uint32_t code = codes[tile];
+    if (code == 0xFFFFFFFFu) return;          // padding slot of a rank with fewer tiles
+    const int I = static_cast<int>(code >> 16), J = static_cast<int>(code & 0xFFFFu);
+    const E* src = packed + static_cast<int64_t>(tile) * kT * kT;
+    const int r0 = band * kBand;
+    constexpr int kVec = 16 / sizeof(E);     // elements per 16-byte vector
+    constexpr int kRowVecs = kT / kVec;
+    if (I != J) {
+        for (int v = threadIdx.x; v < kBand * kRowVecs; v += 256) {
+            const int r = v / kRowVecs, q = v % kRowVecs;
+            const uint4 x = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(r0 + r) * kT)[q];
+            reinterpret_cast<uint4*>(full + static_cast<int64_t>(I * kT + r0 + r) * ld + J * kT)[q] = x;
+            const E* xe = reinterpret_cast<const E*>(&x);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) S[r][q * kVec + k] = xe[k];
+        }
+        __syncthreads();
+        // transposed: output row J*256 + c, columns I*256 + r0 .. + kBand
+        constexpr int kOutVecs = kBand / kVec;
+        for (int v = threadIdx.x; v < kT * kOutVecs; v += 256) {
+            const int c = v / kOutVecs, q = v % kOutVecs;
+            __align__(16) E tmp[kVec];
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) tmp[k] = S[q * kVec + k][c];
+            reinterpret_cast<uint4*>(full + static_cast<int64_t>(J * kT + c) * ld + I * kT + r0)[q] =
+                *reinterpret_cast<const uint4*>(tmp);
+        }
+    } else {
+        // diagonal tile: element (r, c) = packed[min][max] (the upper part is the computed one)
+        for (int e = threadIdx.x; e < kBand * kT; e += 256) {
+            const int r = r0 + e / kT, c = e % kT;
+            const E x = (c >= r) ? src[static_cast<int64_t>(r) * kT + c] : src[static_cast<int64_t>(c) * kT + r];
+            full[static_cast<int64_t>(I * kT + r) * ld + I * kT + c] = x;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
+                                int64_t ld, cudaStream_t stream) {
+    const int blocks = ntiles * (kT / kBand);
+    if (blocks == 0) return cudaSuccess;
+    if (elem_bytes == 2)
+        unpack_tiles_kernel<uint16_t><<<blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(packed), codes, ntiles,
+                                                                  static_cast<uint16_t*>(full), ld);
+    else
+        unpack_tiles_kernel<float><<<blocks, 256, 0, stream>>>(static_cast<const float*>(packed), codes, ntiles,
+                                                               static_cast<float*>(full), ld);
+    return cudaGetLastError();
+}
+
+// Balanced assignment of the upper tiles (row-major order t) of an nt x nt tile grid:
+// rank r takes t = r, r + P, r + 2P, ...; every rank's list is padded to ceil(T / P) slots.
+int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap) {
+    const int T = nt * (nt + 1) / 2;
+    const int per = (T + nranks - 1) / nranks;
+    if (!codes) return per;
+    int t = 0, k = 0;
+    for (int I = 0; I < nt; ++I)
+        for (int J = I; J < nt; ++J, ++t)
+            if (t % nranks == rank && k < cap) codes[k++] = (static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(J);
+    const int actual = k;
+    while (k < per && k < cap) codes[k++] = 0xFFFFFFFFu;
+    return actual;
+}
+
+}  // namespace psd

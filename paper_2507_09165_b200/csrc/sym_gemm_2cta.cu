@@ -240,7 +240,10 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                 uint32_t raw[32];
                 ptx::tmem_ld_32x32b_x32(tbase + c0, raw);
                 ptx::tmem_ld_wait();
-                epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+                const int64_t pk = e.packed ? static_cast<int64_t>(t) * (kT2 * kT2) +
+                                              static_cast<int64_t>(gi0 - I * kT2) * kT2 + c0
+                                            : -1;
+                epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem, pk);
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive_remote(acc ? tmem_empty_leader1 : tmem_empty_leader0);
