@@ -39,7 +39,7 @@ CONFIGS = {
     "c2": dict(n=64, batch=4096, family="goe", filter="c2", precision="fp16x3",
                workload="c2: batch 4096 x 64x64 symmetric, Remez T=4 d=7 (batched small-n kernel)"),
     "c5": dict(n=16384, batch=1, family="goe", filter="half",
-               workload="c5: single n=16384 symmetric matrix (1 GPU here)"),
+               workload="c5: single n=16384 symmetric matrix"),
 }
 
 
@@ -233,12 +233,11 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
 
     import synth
-    from paper_2507_09165_b200 import Filter
+    from paper_2507_09165_b200 import Filter, dist as pdist
     n, gb = cfg["n"], cfg["batch"]
-    if gb % world:
-        raise SystemExit(f"global batch {gb} not divisible by {world} GPUs")
-    count = gb // world
-    first = rank * count
+    if gb == 1 and world > 1:
+        return run_rowpanel(args, cfg, world, rank, dev)
+    first, count = pdist.shard_range(gb, world, rank)
 
     stages = product_filter(cfg["filter"])
     f = Filter(stages, precision=args.precision)
@@ -353,6 +352,59 @@ def run_ours(args, cfg):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_rowpanel(args, cfg, world, rank, dev):
+    """Config c5 on N GPUs: one n x n matrix, row panels, NCCL all-gathers (psd_project_rowpanel)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2507_09165_b200 import Filter, dist as pdist
+    n = cfg["n"]
+    f = Filter(product_filter(cfg["filter"]), precision=args.precision)
+    rp = pdist.RowPanelProjector(f, n)
+    r0, rows = rp.row_range()
+    g = synth.rng(synth.SEED_BASE + 5)
+    A = g.standard_normal((n, n)).astype(np.float32)          # GOE rows: every rank draws the same A
+    Xr = torch.tensor(0.5 * (A[r0:r0 + rows] + A[:, r0:r0 + rows].T), dtype=torch.float32, device=dev)
+    del A
+    out = torch.empty_like(Xr)
+    for _ in range(args.warmup):
+        rp.project(Xr, out)
+    f.profile_read()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream(dev)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rp.project(Xr, out)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    _, _, kernel_launches = f.profile_read()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    rp.close()
+    if rank == 0:
+        G = f.gemm_count(True)
+        line = {
+            "metric": "psd_projections_per_sec", "value": args.steps / (ms / 1000.0), "unit": "matrices/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"] + f" -- row panels over {world} GPUs (NCCL all-gather of "
+                                                     "packed upper tiles per product)", "n": n, "global_batch": 1,
+                       "parallelism": f"row-panel tp{world}", "products_per_matrix": G},
+            "tflops_algorithmic": float(n) * n * (n + 1) * G * args.steps / (ms / 1000.0) / 1e12,
+            "gpu_launches": kernel_launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def main():

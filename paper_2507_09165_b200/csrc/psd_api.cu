@@ -483,9 +483,13 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
 }
 
 // ---------------------------------------------------------------- NCCL (resolved at run time)
+struct NcclUniqueId {          // ncclUniqueId: passed BY VALUE to ncclCommInitRank
+    char internal[128];
+};
+
 struct NcclApi {
     using GetUniqueId = int (*)(void*);
-    using CommInitRank = int (*)(void**, int, char[128], int);
+    using CommInitRank = int (*)(void**, int, NcclUniqueId, int);
     using AllGather = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
     using CommDestroy = int (*)(void*);
     using GetErrorString = const char* (*)(int);
@@ -818,9 +822,9 @@ psd_status_t psd_nccl_unique_id(char id[128]) {
 psd_status_t psd_nccl_comm_create(const char id[128], int nranks, int rank, void** comm) {
     if (!id || !comm) return fail(PSD_EINVAL, "null id or comm");
     if (!nccl().ok) return fail(PSD_ENCCL, "libnccl.so.2 not available");
-    char buf[128];
-    std::memcpy(buf, id, 128);
-    int r = nccl().comm_init_rank(comm, nranks, buf, rank);
+    NcclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    int r = nccl().comm_init_rank(comm, nranks, uid, rank);
     return r ? nccl_fail(r, "ncclCommInitRank") : PSD_OK;
 }
 

@@ -141,3 +141,31 @@ def test_rowpanel_virtual_matches_single_gpu_path():
     a = f.project_rowpanel_virtual(Xd, 4).double().cpu().numpy()
     b = f.project(Xd[None]).double().cpu().numpy()[0]
     assert np.linalg.norm(a - b) / np.linalg.norm(b) < 2e-3
+
+
+@pytest.mark.gpu
+def test_rowpanel_nccl_world1():
+    """The real NCCL code path (library communicator, in-place all-gathers of X rows and packed
+    tiles) with a world-size-1 process group on this GPU, vs the oracle."""
+    torch = pytest.importorskip("torch")
+    import torch.distributed as tdist
+    import paper_2507_09165_b200 as pkg
+    from paper_2507_09165_b200 import dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    tdist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        n = 1024
+        X = synth.goe(n, 77)
+        f = pkg.Filter(pkg.filters.half_filter())
+        rp = dist.RowPanelProjector(f, n)
+        r0, rows = rp.row_range()
+        Xd = torch.tensor(X[r0:r0 + rows], dtype=torch.float32, device="cuda").contiguous()
+        out = rp.project(Xd).double().cpu().numpy()
+        torch.cuda.synchronize()
+        rp.close()
+        lam = chain.frobenius_bound(X)
+        ref, _ = chain.project(X, tables.F_HALF_REFINED, tables.half_kappas(7), lam=lam)
+        assert np.linalg.norm(out - ref[r0:r0 + rows]) / np.linalg.norm(ref) < 5e-3
+    finally:
+        tdist.destroy_process_group()
