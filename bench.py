@@ -272,22 +272,24 @@ def run_ours(args, cfg):
     f.profile(False)
     assert f.status() == "PSD_OK"
 
-    # e2e through the public API with pinned host buffers (H2D of the inputs and D2H of
-    # the projected matrices inside the timed region, every step)
+    # e2e through the public API with pinned host buffers: psd_project_host moves the inputs
+    # host->device, projects and moves the results device->host every step (chunked so the
+    # copies overlap the projections); all of it inside the timed region
     e2e_ms = None
     host_out = torch.empty_like(host_in, pin_memory=True)
     if not args.no_e2e:
-        e2e_steps = max(1, min(args.steps, 3))
-        f.project(X, out=out)
+        e2e_steps = max(1, min(args.steps, 5))
+        chunks = 4 if count >= 4 else 1
+        del X, out
+        torch.cuda.empty_cache()
+        f.project_host(host_in, host_out, chunks=chunks)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
-            X.copy_(host_in, non_blocking=True)
-            f.project(X, out=out)
-            host_out.copy_(out, non_blocking=True)
+            f.project_host(host_in, host_out, chunks=chunks)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -311,13 +313,15 @@ def run_ours(args, cfg):
         # (algorithmic) flops, peak is the tensor peak of the operand type / 3
         passes = 3 if args.precision.endswith("x3") else 1
         achieved = (per_launch / (launch_ms / 1000.0) / 1e12) if launch_ms else None
-        peak_bf16 = peaks.get("bf16_tflops", 1590.0)
+        # the product kernel is timed inside a long step (steps x products back to back, ~1 s of
+        # load under the 1 kW cap): the SUSTAINED measured bf16 figure is the denominator
+        peak_bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0))
         if args.precision.startswith(("fp16", "bf16")):
             peak = peak_bf16 / passes
-            peak_note = f"{peak_src} bf16 burst (fp16 = bf16 rate)" + (" / 3 passes" if passes == 3 else "")
+            peak_note = f"{peak_src} bf16 sustained (fp16 = bf16 rate)" + (" / 3 passes" if passes == 3 else "")
         else:
             peak = peak_bf16 / 2.0 / passes
-            peak_note = f"{peak_src} bf16 burst x 1/2 (tf32 nominal ratio)" + (" / 3 passes" if passes == 3 else "")
+            peak_note = f"{peak_src} bf16 sustained x 1/2 (tf32 nominal ratio)" + (" / 3 passes" if passes == 3 else "")
         traffic, traffic_src = load_traffic(cfg)
         line = {
             "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s", "n_gpus": world,

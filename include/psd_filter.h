@@ -162,6 +162,15 @@ psd_status_t psd_profile(psd_filter_t h, int enable);
 psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* product_launches,
                               int64_t* kernel_launches);
 
+/* End-to-end projection of HOST matrices: X_host and out_host are pinned host buffers
+ * (cudaMallocHost / cudaHostRegister), batch x n x n fp32.  The batch is processed in `chunks`
+ * pieces on three internal streams so the host-to-device copy of chunk c+1, the projection of
+ * chunk c and the device-to-host copy of chunk c-1 overlap (PCIe is full duplex).  Stream-ordered
+ * with respect to `stream` (it waits for prior work and later work waits for the result).
+ * out_host == X_host is allowed. */
+psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, int64_t batch, float* out_host,
+                              int chunks, void* stream);
+
 /* ---------------------------------------------------------------- multi-GPU (row panels)
  * One large n over P GPUs, one process per GPU.  Every
  * product of the chain is split over the ranks by upper 256-tiles (rank r computes a balanced,

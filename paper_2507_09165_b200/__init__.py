@@ -132,6 +132,24 @@ class Filter:
               "psd_profile_read")
         return ms.value, pl.value, kl.value
 
+    def project_host(self, X, out=None, chunks=4, stream=None):
+        """End-to-end projection of a PINNED host float32 tensor (batch, n, n): chunked so the
+        host-to-device copies, the projections and the device-to-host copies overlap
+        (psd_project_host).  Returns `out` (pinned host); valid after the stream synchronises."""
+        import torch
+        if not isinstance(X, torch.Tensor) or X.is_cuda or X.dtype != torch.float32 or not X.is_pinned():
+            raise TypeError("X must be a pinned host float32 tensor")
+        Xb = X.unsqueeze(0) if X.dim() == 2 else X
+        if out is None:
+            out = torch.empty_like(X, pin_memory=True)
+        ob = out.unsqueeze(0) if out.dim() == 2 else out
+        if not (Xb.is_contiguous() and ob.is_contiguous() and ob.shape == Xb.shape and ob.is_pinned()):
+            raise ValueError("out must be a pinned contiguous tensor shaped like X")
+        check(self._lib.psd_project_host(self._h, ctypes.c_void_p(Xb.data_ptr()), Xb.shape[-1], Xb.shape[0],
+                                         ctypes.c_void_p(ob.data_ptr()), int(chunks), _stream_ptr(stream)),
+              "psd_project_host")
+        return out
+
     def project_rowpanel_virtual(self, X, nranks, out=None, sign=False, stream=None):
         """Row-panel projection of one n x n matrix with `nranks` virtual ranks on this GPU (the
         per-rank code of the multi-GPU path; see dist.RowPanelProjector for real ranks)."""

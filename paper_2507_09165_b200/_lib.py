@@ -35,6 +35,8 @@ SIGNATURES = [
     ("psd_profile", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_profile_read", _c.c_int, [_c.c_void_p, _c.POINTER(_c.c_double), _c.POINTER(_c.c_int64),
                                     _c.POINTER(_c.c_int64)]),
+    ("psd_project_host", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_int,
+                                    _c.c_void_p]),
     ("psd_nccl_unique_id", _c.c_int, [_c.c_char_p]),
     ("psd_nccl_comm_create", _c.c_int, [_c.c_char_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_void_p)]),
     ("psd_nccl_comm_destroy", _c.c_int, [_c.c_void_p]),

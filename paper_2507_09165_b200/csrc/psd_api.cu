@@ -86,6 +86,13 @@ struct psd_filter_s {
         uint32_t* codes = nullptr;      // [nranks][per] tile codes (gather order)
         std::vector<int> counts;        // real tiles per rank
     } rp;
+    // pipelined host-buffer projection (psd_project_host)
+    struct HostPipe {
+        cudaStream_t s[3] = {nullptr, nullptr, nullptr};   // h2d, compute, d2h
+        float* dx[2] = {nullptr, nullptr};
+        float* dout[2] = {nullptr, nullptr};
+        size_t chunk_bytes = 0;
+    } hp;
     // profiling / launch accounting
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -536,6 +543,15 @@ void free_rowpanel_ws(psd_filter_s::RowPanel& rp) {
     rp = psd_filter_s::RowPanel();
 }
 
+void free_hostpipe(psd_filter_s* h) {
+    auto& hp = h->hp;
+    if (hp.s[0]) cudaDeviceSynchronize();
+    for (auto& p : hp.dx) { if (p) cudaFree(p); p = nullptr; }
+    for (auto& p : hp.dout) { if (p) cudaFree(p); p = nullptr; }
+    for (auto& q : hp.s) { if (q) cudaStreamDestroy(q); q = nullptr; }
+    hp.chunk_bytes = 0;
+}
+
 void free_rowpanel(psd_filter_s* h) {
     if (h->rp.codes) {
         cudaDeviceSynchronize();
@@ -722,6 +738,7 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
 void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
     free_rowpanel(h);
+    free_hostpipe(h);
     for (auto& p : h->ev_pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto& e : h->ev_pool) cudaEventDestroy(e);
     if (h->ws.status) {
@@ -809,6 +826,70 @@ psd_status_t psd_profile_read(psd_filter_t h, double* product_ms, int64_t* produ
     if (kernel_launches) *kernel_launches = h->kernel_launches;
     h->product_launches_profiled = 0;
     h->kernel_launches = 0;
+    return PSD_OK;
+}
+
+psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, int64_t batch, float* out_host,
+                              int chunks, void* stream) {
+    psd_status_t rc = check_args(h, X_host, n, batch, out_host);
+    if (rc != PSD_OK) return rc;
+    if (chunks < 1) chunks = 1;
+    if (chunks > batch) chunks = static_cast<int>(batch);
+    const int64_t per = (batch + chunks - 1) / chunks;
+    auto& hp = h->hp;
+    const size_t mat = static_cast<size_t>(n) * n * sizeof(float);
+    cudaError_t e;
+    if (hp.chunk_bytes < per * mat) {
+        free_hostpipe(h);
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, "cudaStreamCreate");
+        for (int i = 0; i < 2; ++i) {
+            if (cudaMalloc(&hp.dx[i], per * mat) != cudaSuccess || cudaMalloc(&hp.dout[i], per * mat) != cudaSuccess) {
+                free_hostpipe(h);
+                return fail(PSD_ENOMEM, "cudaMalloc host-pipeline buffers failed");
+            }
+        }
+        hp.chunk_bytes = per * mat;
+    }
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    auto ev = [&]() { return take_event(h); };
+    auto give = [&](cudaEvent_t x) { h->ev_pool.push_back(x); };
+    cudaEvent_t start = ev();
+    cudaEventRecord(start, user);
+    for (auto q : hp.s) cudaStreamWaitEvent(q, start, 0);
+    cudaEvent_t freed[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> used = {start};
+    for (int c = 0; c * per < batch; ++c) {
+        const int slot = c & 1;
+        const int64_t b0 = c * per;
+        const int64_t nb = std::min<int64_t>(per, batch - b0);
+        if (freed[slot]) cudaStreamWaitEvent(hp.s[0], freed[slot], 0);
+        e = cudaMemcpyAsync(hp.dx[slot], X_host + b0 * n * n, nb * mat, cudaMemcpyHostToDevice, hp.s[0]);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+        cudaEvent_t in = ev();
+        used.push_back(in);
+        cudaEventRecord(in, hp.s[0]);
+        cudaStreamWaitEvent(hp.s[1], in, 0);
+        rc = run(h, hp.dx[slot], n, nb, hp.dout[slot], nullptr, nullptr, false, hp.s[1]);
+        if (rc != PSD_OK) return rc;
+        cudaEvent_t comp = ev();
+        used.push_back(comp);
+        cudaEventRecord(comp, hp.s[1]);
+        cudaStreamWaitEvent(hp.s[2], comp, 0);
+        e = cudaMemcpyAsync(out_host + b0 * n * n, hp.dout[slot], nb * mat, cudaMemcpyDeviceToHost, hp.s[2]);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H");
+        cudaEvent_t outd = ev();
+        used.push_back(outd);
+        cudaEventRecord(outd, hp.s[2]);
+        freed[slot] = outd;      // chunk c+2 may reuse this slot's X and out buffers after the D2H
+    }
+    cudaEvent_t done = ev();
+    used.push_back(done);
+    cudaEventRecord(done, hp.s[2]);
+    cudaStreamWaitEvent(user, done, 0);
+    // cudaStreamWaitEvent binds to the record made before it, so the events can be re-recorded
+    for (auto x : used) give(x);
     return PSD_OK;
 }
 

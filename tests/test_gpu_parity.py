@@ -276,3 +276,20 @@ def test_small_batch_sign_and_nonfinite(pkg):
     Xn[2, 5, 9] = np.inf
     _, lam, f = _gpu(pkg, _product_filter("half", pkg), Xn, "fp16")
     assert f.status() == "PSD_ENONFINITE" and np.isnan(lam[2])
+
+
+def test_project_host_pipeline(pkg):
+    """psd_project_host (chunked H2D / project / D2H on three streams) equals psd_project bitwise,
+    including a ragged last chunk and in-place output."""
+    X = synth.batch("goe", 384, 7, 31)
+    f = pkg.Filter(pkg.filters.half_filter())
+    Xh = torch.tensor(X, dtype=torch.float32).pin_memory()
+    out = f.project_host(Xh, chunks=3)
+    torch.cuda.synchronize()
+    ref = f.project(Xh.cuda()).cpu()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    Xh2 = Xh.clone().pin_memory()
+    f.project_host(Xh2, Xh2, chunks=2)
+    torch.cuda.synchronize()
+    assert torch.equal(Xh2, ref)
