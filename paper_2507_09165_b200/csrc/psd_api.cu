@@ -344,23 +344,6 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     Workspace& ws = h->ws;
     cudaError_t e;
 
-    // (a1) bound
-    const double* lam = nullptr;
-    if (h->bound == PSD_BOUND_FROBENIUS) {
-        const int nblk = bound_blocks_per_matrix(n);
-        e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
-        if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
-        h->kernel_launches += 2;
-        e = launch_finalize_bound(ws.partial, nblk, batch, ws.lambda, lambda_out, ws.status, st);
-        if (e != cudaSuccess) return cuda_fail(e, "finalize_bound");
-        lam = ws.lambda;
-    } else {
-        lam = lambda_in;
-        if (lambda_out && lambda_out != lambda_in) {
-            e = cudaMemcpyAsync(lambda_out, lambda_in, batch * sizeof(double), cudaMemcpyDeviceToDevice, st);
-            if (e != cudaSuccess) return cuda_fail(e, "lambda copy");
-        }
-    }
     double sign_only = 0.0;
     std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
     if (n <= 64 && h->bound == PSD_BOUND_FROBENIUS && ws.op == OpType::F16 && !steps.empty() &&
@@ -417,6 +400,23 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             h->product_launches_profiled += 1;     // one launch carries the whole chain
         }
         return PSD_OK;
+    }
+    // (a1) bound
+    const double* lam = nullptr;
+    if (h->bound == PSD_BOUND_FROBENIUS) {
+        const int nblk = bound_blocks_per_matrix(n);
+        e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
+        if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
+        h->kernel_launches += 2;
+        e = launch_finalize_bound(ws.partial, nblk, batch, ws.lambda, lambda_out, ws.status, st);
+        if (e != cudaSuccess) return cuda_fail(e, "finalize_bound");
+        lam = ws.lambda;
+    } else {
+        lam = lambda_in;
+        if (lambda_out && lambda_out != lambda_in) {
+            e = cudaMemcpyAsync(lambda_out, lambda_in, batch * sizeof(double), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "lambda copy");
+        }
     }
     const bool split = ws.split;
     double sc[B_COUNT];

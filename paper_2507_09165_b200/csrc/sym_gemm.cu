@@ -1,16 +1,23 @@
-// sym_gemm.cu -- symmetric product C = alpha * (A B) + beta * D on sm_100a tensor cores.
+// sym_gemm.cu -- symmetric product C = alpha * (A B) + beta * D on sm_100a tensor cores, 128x128
+// upper tiles: the path for small and few-tile problems (configs c1 padded, c3: one n = 1024).
 //
-// Every product of the composite filter (Algorithm 2) multiplies two
-// commuting symmetric matrices (powers/polynomials of the same X), so
-// C is symmetric: only upper tiles (I <= J) are computed and each is stored twice
-// (direct + transposed), which halves the MMA work and makes C exactly symmetric.
-// A and B are symmetric, so both operands are read as row panels ("K-major"):
-// A tile = rows I*128.., B^T tile = rows J*128.. of B (B^T = B).
+// Every product of the composite filter (Algorithm 2) multiplies two commuting
+// symmetric matrices (powers/polynomials of the same X), so C is symmetric: only
+// upper tiles (I <= J) are computed and each is stored twice (direct + transposed).  A and B
+// are symmetric, so both operands are read as row panels ("K-major").
 //
-// Pipeline per CTA (one 128x128 upper tile):
-//   warp 0 / 1 elected lane : TMA producer  -> kStages-deep smem ring (mbarrier full/empty)
-//   warp 1 / 1 elected lane : tcgen05.mma.cta_group::1 (M=128, N=128) into TMEM
-//   warps 0-3               : epilogue  tcgen05.ld -> alpha*acc + beta*D -> mirrored stores
+// A cluster of KS CTAs (KS = 1, 2, 4; cluster split-K) owns one 128x128 upper tile:
+//   warp 0 / elected lane : TMA producer over this CTA's K slice -> kStages smem ring
+//   warp 1 / elected lane : tcgen05.mma.cta_group::1 (M = N = 128) into TMEM
+//   KS = 1 : warps 0-3 run the epilogue straight from TMEM (tcgen05.ld 32x32b)
+//   KS > 1 : every CTA parks its partial accumulator in its own (now idle) ring smem; after a
+//            cluster barrier CTA k sums rows [k*128/KS, (k+1)*128/KS) over the KS partials with
+//            ld.shared::cluster (DSMEM) and runs the epilogue for those rows -- KS x more SMs
+//            busy on few-tile problems (n = 1024: 36 tiles -> 144 CTAs) and a KS x shorter
+//            epilogue per CTA.
+// Launched with programmatic dependent launch: the prologue (barrier init, TMEM alloc,
+// descriptor prefetch) overlaps the previous kernel; griddepcontrol.wait precedes any read of
+// the previous kernel's outputs.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -41,7 +48,23 @@ __device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J)
     J = i + rem;
 }
 
-template <OpType T, bool kSplit>
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// partial-accumulator layout in smem: row-major 128 x 128 fp32, float4 column q of row r stored at
+// q ^ (r & 31) so that 32 lanes reading 32 different rows at the same q hit 32 different banks
+__device__ __forceinline__ uint32_t part_off(int r, int q) {
+    return static_cast<uint32_t>((r * 32 + (q ^ (r & 31))) * 16);
+}
+
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(cluster_addr) : "memory");
+    return v;
+}
+
+template <OpType T, bool kSplit, int KS>
 __global__ void __launch_bounds__(kThreads, 1)
 sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
@@ -61,10 +84,12 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     uint8_t* epi_smem = smem + kRingBytes1 + 256;                   // 4 x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int nt = s.npad / kTile;
     const int b = blockIdx.y;
+    const int krank = (KS > 1) ? static_cast<int>(ptx::cluster_ctarank()) : 0;
     int I, J;
-    upper_tile_coords(blockIdx.x, nt, I, J);
+    upper_tile_coords(blockIdx.x / KS, nt, I, J);
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -85,8 +110,10 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    grid_dep_wait();                                  // the operands are the previous kernel's output
 
-    const int num_kb = s.npad / kBK;
+    const int num_kb = s.npad / kBK / KS;             // this CTA's K slice
+    const int kb0 = krank * num_kb;
     const int rowA = b * s.npad + I * kTile;
     const int rowB = b * s.npad + J * kTile;
 
@@ -98,12 +125,13 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 const uint32_t ph = (kb / kStages) & 1;
                 ptx::mbar_wait(&empty[st], ph ^ 1);
                 uint8_t* sa = ring + st * kStageBytes;
+                const int kx = (kb0 + kb) * kBK;
                 ptx::mbar_arrive_expect_tx(&full[st], kStageBytes);
-                ptx::tma_load_2d(sa, &tm.a, &full[st], kb * kBK, rowA, pol);
-                ptx::tma_load_2d(sa + kTileBytes, &tm.b, &full[st], kb * kBK, rowB, pol);
+                ptx::tma_load_2d(sa, &tm.a, &full[st], kx, rowA, pol);
+                ptx::tma_load_2d(sa + kTileBytes, &tm.b, &full[st], kx, rowB, pol);
                 if constexpr (kSplit) {
-                    ptx::tma_load_2d(sa + 2 * kTileBytes, &tm.a_lo, &full[st], kb * kBK, rowA, pol);
-                    ptx::tma_load_2d(sa + 3 * kTileBytes, &tm.b_lo, &full[st], kb * kBK, rowB, pol);
+                    ptx::tma_load_2d(sa + 2 * kTileBytes, &tm.a_lo, &full[st], kx, rowA, pol);
+                    ptx::tma_load_2d(sa + 3 * kTileBytes, &tm.b_lo, &full[st], kx, rowB, pol);
                 }
             }
         }
@@ -145,21 +173,72 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     // ------------------------------------------------------------------ epilogue
     ptx::mbar_wait(accum_full, 0);
     ptx::tc_fence_after();
+    grid_dep_launch();                               // the next kernel may start its prologue
 
-    const int gi0 = I * kTile + warp * 32;          // this warp's first row (TMEM lanes 32w..)
     const bool diag = (I == J);
     float alpha = e.alpha;
     if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
     uint8_t* wsmem = epi_smem + warp * kEpiWarpSmemBytes;
 
+    if constexpr (KS == 1) {
+        const int gi0 = I * kTile + warp * 32;      // this warp's first row (TMEM lanes 32w..)
 #pragma unroll 1
-    for (int c0 = 0; c0 < kTile; c0 += 32) {
-        const int gj0 = J * kTile + c0;
-        if (diag && gj0 + 31 < gi0) continue;       // chunk below the diagonal for the whole warp
-        uint32_t raw[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
-        ptx::tmem_ld_wait();
-        epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+        for (int c0 = 0; c0 < kTile; c0 += 32) {
+            const int gj0 = J * kTile + c0;
+            if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
+            uint32_t raw[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
+            ptx::tmem_ld_wait();
+            epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+        }
+    } else {
+        // park this CTA's partial accumulator (all MMAs done -> the ring is free)
+        const int r = warp * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kTile; c0 += 32) {
+            uint32_t raw[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<uint4*>(ring + part_off(r, c0 / 4 + q)) =
+                    make_uint4(raw[4 * q], raw[4 * q + 1], raw[4 * q + 2], raw[4 * q + 3]);
+        }
+        ptx::cluster_sync();
+        // CTA k reduces row groups [k * 4/KS, (k+1) * 4/KS) x 4 column chunks; warp w takes chunks w, w+4, ..
+        constexpr int kGroups = 4 / KS;
+        const uint32_t ring_u = ptx::smem_u32(ring);
+        uint32_t peer[KS];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) peer[kk] = ptx::mapa_shared(ring_u, static_cast<uint32_t>(kk));
+#pragma unroll 1
+        for (int ch = warp; ch < kGroups * 4; ch += 4) {
+            const int rg = krank * kGroups + ch / 4;
+            const int cc = ch % 4;
+            const int gi0 = I * kTile + rg * 32;
+            const int gj0 = J * kTile + cc * 32;
+            if (diag && gj0 + 31 < gi0) continue;
+            const int row = rg * 32 + lane;
+            float acc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 v = ld_dsmem_f4(peer[kk] + part_off(row, cc * 8 + q));
+                    acc[4 * q] += v.x;
+                    acc[4 * q + 1] += v.y;
+                    acc[4 * q + 2] += v.z;
+                    acc[4 * q + 3] += v.w;
+                }
+            }
+            uint32_t raw[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(acc[i]);
+            epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+        }
+        ptx::cluster_sync();                         // peers' partials stay valid until all read
     }
 
     ptx::tc_fence_before();
@@ -170,31 +249,69 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     }
 }
 
-template <OpType T, bool kSplit>
+template <OpType T, bool kSplit, int KS>
 cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kSmemBytes);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
     const int nt = s.npad / kTile;
-    dim3 grid(nt * (nt + 1) / 2, s.batch);
-    sym_gemm_kernel<T, kSplit><<<grid, kThreads, kSmemBytes, stream>>>(m, s, e);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nt * (nt + 1) / 2 * KS, s.batch);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (KS > 1) {
+        attrs[na].id = cudaLaunchAttributeClusterDimension;
+        attrs[na].val.clusterDim.x = KS;
+        attrs[na].val.clusterDim.y = 1;
+        attrs[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, sym_gemm_kernel<T, kSplit, KS>, m, s, e);
+}
+
+template <OpType T, bool kSplit>
+cudaError_t launch_ks(int ks, const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
+    switch (ks) {
+        case 4: return launch_t<T, kSplit, 4>(m, s, e, stream);
+        case 2: return launch_t<T, kSplit, 2>(m, s, e, stream);
+        default: return launch_t<T, kSplit, 1>(m, s, e, stream);
+    }
 }
 
 }  // namespace
 
+// Split-K factor for a few-tile problem: fill the SMs (one wave), keep >= 4 k-blocks per CTA.
+int sym_gemm_split_k(int npad, int batch, OpType t) {
+    const int nt = npad / kTile;
+    const int tiles = nt * (nt + 1) / 2 * batch;
+    const int kblocks = npad / (kBlockKBytes / (t == OpType::TF32 ? 4 : 2));
+    int ks = 1;
+    while (ks < 4 && tiles * ks * 2 <= 148 && kblocks % (ks * 2) == 0 && kblocks / (ks * 2) >= 4) ks *= 2;
+    return ks;
+}
+
 cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
                             cudaStream_t stream) {
+    const int ks = sym_gemm_split_k(s.npad, s.batch, t);
     switch (t) {
-        case OpType::F16: return split ? launch_t<OpType::F16, true>(m, s, e, stream)
-                                       : launch_t<OpType::F16, false>(m, s, e, stream);
-        case OpType::BF16: return split ? launch_t<OpType::BF16, true>(m, s, e, stream)
-                                        : launch_t<OpType::BF16, false>(m, s, e, stream);
-        case OpType::TF32: return split ? launch_t<OpType::TF32, true>(m, s, e, stream)
-                                        : launch_t<OpType::TF32, false>(m, s, e, stream);
+        case OpType::F16: return split ? launch_ks<OpType::F16, true>(ks, m, s, e, stream)
+                                       : launch_ks<OpType::F16, false>(ks, m, s, e, stream);
+        case OpType::BF16: return split ? launch_ks<OpType::BF16, true>(ks, m, s, e, stream)
+                                        : launch_ks<OpType::BF16, false>(ks, m, s, e, stream);
+        case OpType::TF32: return split ? launch_ks<OpType::TF32, true>(ks, m, s, e, stream)
+                                        : launch_ks<OpType::TF32, false>(ks, m, s, e, stream);
     }
     return cudaErrorInvalidValue;
 }
