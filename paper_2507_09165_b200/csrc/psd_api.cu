@@ -86,6 +86,23 @@ struct psd_filter_s {
         uint32_t* codes = nullptr;      // [nranks][per] tile codes (gather order)
         std::vector<int> counts;        // real tiles per rank
     } rp;
+    // CUDA-graph cache of whole psd_project sequences (host launch overhead dominates small n)
+    struct GraphEntry {
+        const void* X;
+        const void* out;
+        const void* lin;
+        const void* lout;
+        int64_t n, batch;
+        int want_sign, prec, bound;
+        cudaGraphExec_t exec;
+        int64_t kernels, products;
+        uint64_t last_use;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
+    bool use_graphs = true;
+    cudaStream_t capture_stream = nullptr;
+    bool capturing = false;
     // pipelined host-buffer projection (psd_project_host)
     struct HostPipe {
         cudaStream_t s[3] = {nullptr, nullptr, nullptr};   // h2d, compute, d2h
@@ -179,6 +196,8 @@ int64_t ws_bytes(OpType op, bool split, int64_t npad, int64_t batch) {
     return (split ? 2 : 1) * B_COUNT * mat * op_bytes(op) + batch * 256 * 8 + batch * 8 + 64;
 }
 
+void free_graphs(psd_filter_s* h);
+
 psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     Workspace& ws = h->ws;
     const OpType op = op_of(h->prec);
@@ -188,6 +207,7 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
     }
+    free_graphs(h);          // captured sequences point into the old workspace
     free_ws(ws);
     const size_t mat = static_cast<size_t>(npad) * npad * batch;
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
@@ -332,8 +352,8 @@ cudaEvent_t take_event(psd_filter_s* h) {
     return e;
 }
 
-psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
-                 const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
+psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
+                      const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
     psd_status_t rc = check_args(h, X, n64, batch64, out);
     if (rc != PSD_OK) return rc;
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
@@ -387,7 +407,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             q.alpha = static_cast<float>(s.alpha / (scale_a * scale_b));
         }
         std::pair<cudaEvent_t, cudaEvent_t> evs{nullptr, nullptr};
-        if (h->profiling) {
+        if (h->profiling && !h->capturing) {
             evs = {take_event(h), take_event(h)};
             cudaEventRecord(evs.first, st);
         }
@@ -446,7 +466,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
-    if (h->profiling && !steps.empty()) {
+    if (h->profiling && !h->capturing && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
     }
@@ -485,6 +505,90 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         cudaEventRecord(evp.second, st);
         h->ev_pairs.push_back(evp);
         h->product_launches_profiled += static_cast<int64_t>(steps.size());
+    }
+    return PSD_OK;
+}
+
+void free_graphs(psd_filter_s* h) {
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
+}
+
+// psd_project through the graph cache: the first call with a given (pointers, shape, mode) key is
+// captured (thread-local capture mode, internal stream) and instantiated; every call then costs
+// one cudaGraphLaunch on the caller's stream.  Workspace growth happens before capture.
+psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
+                 const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
+    if (!h || !h->use_graphs || h->capturing) return run_body(h, X, n64, batch64, out, lambda_in, lambda_out, want_sign, st);
+    psd_status_t rc = check_args(h, X, n64, batch64, out);
+    if (rc != PSD_OK) return rc;
+    const int64_t key_prec = h->prec, key_bound = h->bound;
+    psd_filter_s::GraphEntry* hit = nullptr;
+    for (auto& g : h->graphs)
+        if (g.X == X && g.out == out && g.lin == lambda_in && g.lout == lambda_out && g.n == n64 && g.batch == batch64 &&
+            g.want_sign == static_cast<int>(want_sign) && g.prec == key_prec && g.bound == key_bound) {
+            hit = &g;
+            break;
+        }
+    if (!hit) {
+        // make sure every allocation exists, then capture
+        rc = ensure_ws(h, static_cast<int>(padded_n(n64, batch64)), static_cast<int>(batch64));
+        if (rc != PSD_OK) return rc;
+        if (!h->capture_stream) {
+            cudaError_t e = cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+        const int64_t k0 = h->kernel_launches, p0 = h->product_launches_profiled;
+        cudaError_t e = cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
+        h->capturing = true;
+        rc = run_body(h, X, n64, batch64, out, lambda_in, lambda_out, want_sign, h->capture_stream);
+        h->capturing = false;
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(h->capture_stream, &graph);
+        if (rc != PSD_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+        if (h->graphs.size() >= 8) {       // evict the least recently used
+            size_t lru = 0;
+            for (size_t i = 1; i < h->graphs.size(); ++i)
+                if (h->graphs[i].last_use < h->graphs[lru].last_use) lru = i;
+            cudaGraphExecDestroy(h->graphs[lru].exec);
+            h->graphs.erase(h->graphs.begin() + lru);
+        }
+        psd_filter_s::GraphEntry g{X, out, lambda_in, lambda_out, n64, batch64, static_cast<int>(want_sign), static_cast<int>(key_prec),
+                     static_cast<int>(key_bound), exec, h->kernel_launches - k0, 0, 0};
+        // the product count of the sequence (for profiling) = its number of product kernels
+        std::vector<Step> steps_probe;
+        {
+            double so = 0.0;
+            steps_probe = build_plan(h, want_sign, &so);
+        }
+        g.products = (n64 <= 64) ? 1 : static_cast<int64_t>(steps_probe.size());
+        h->kernel_launches = k0;
+        h->product_launches_profiled = p0;
+        h->graphs.push_back(g);
+        hit = &h->graphs.back();
+    }
+    hit->last_use = ++h->graph_clock;
+    std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
+    if (h->profiling) {
+        evp = {take_event(h), take_event(h)};
+        cudaEventRecord(evp.first, st);
+    }
+    cudaError_t e = cudaGraphLaunch(hit->exec, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    h->kernel_launches += hit->kernels;
+    if (evp.first) {
+        cudaEventRecord(evp.second, st);
+        h->ev_pairs.push_back(evp);
+        h->product_launches_profiled += hit->products;
     }
     return PSD_OK;
 }
@@ -739,6 +843,8 @@ void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
     free_rowpanel(h);
     free_hostpipe(h);
+    free_graphs(h);
+    if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
     for (auto& p : h->ev_pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto& e : h->ev_pool) cudaEventDestroy(e);
     if (h->ws.status) {
