@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "epilogue.cuh"
 #include "kernels.h"
 #include "optraits.cuh"
@@ -266,9 +268,12 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
     int na = 0;
-    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
+    static const bool pdl = !std::getenv("PSD_NO_PDL");
+    if (pdl) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     if (KS > 1) {
         attrs[na].id = cudaLaunchAttributeClusterDimension;
         attrs[na].val.clusterDim.x = KS;
@@ -294,6 +299,8 @@ cudaError_t launch_ks(int ks, const OperandMaps& m, const GemmShape& s, const Ep
 
 // Split-K factor for a few-tile problem: fill the SMs (one wave), keep >= 4 k-blocks per CTA.
 int sym_gemm_split_k(int npad, int batch, OpType t) {
+    static const int forced = std::getenv("PSD_SPLITK") ? std::atoi(std::getenv("PSD_SPLITK")) : 0;
+    if (forced == 1 || forced == 2 || forced == 4) return forced;
     const int nt = npad / kTile;
     const int tiles = nt * (nt + 1) / 2 * batch;
     const int kblocks = npad / (kBlockKBytes / (t == OpType::TF32 ? 4 : 2));
