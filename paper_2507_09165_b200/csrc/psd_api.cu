@@ -100,7 +100,7 @@ struct psd_filter_s {
     };
     std::vector<GraphEntry> graphs;
     uint64_t graph_clock = 0;
-    bool use_graphs = true;
+    bool use_graphs = std::getenv("PSD_NO_GRAPH") == nullptr;
     cudaStream_t capture_stream = nullptr;
     bool capturing = false;
     // pipelined host-buffer projection (psd_project_host)
