@@ -37,6 +37,8 @@ struct EpiParams {
     // operand precision (out_op ignored) or fp32 when packed_f32.
     void* packed;
     int packed_f32;
+    // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
+    unsigned long long* dbg;
 };
 
 struct GemmShape {

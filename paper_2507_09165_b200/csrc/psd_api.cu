@@ -1071,6 +1071,7 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.ldF = n;
     ep.strideF = static_cast<int64_t>(n) * n;
     ep.nF = n;
+    if (std::getenv("PSD_DEBUG_STAMPS")) ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial);  // debug only
     e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     const GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
@@ -1084,6 +1085,14 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
             : launch_sym_gemm(ws.op, split, m, shape, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
+    if (ep.dbg) {            // debug: print the kernel phase stamps (ns since the first)
+        unsigned long long t[6] = {};
+        cudaStreamSynchronize(st);
+        cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "psd stamps n=%d: prologue %.2f us, dep-wait %.2f us, mainloop %.2f us, epilogue %.2f us, teardown %.2f us\n",
+                     n, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                     (t[5] - t[4]) * 1e-3);
+    }
     return PSD_OK;
 }
 

@@ -50,6 +50,13 @@ __device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J)
     J = i + rem;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DBG_STAMP(i) do { if (e.dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) e.dbg[i] = gtimer(); } while (0)
+
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
@@ -92,6 +99,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     const int krank = (KS > 1) ? static_cast<int>(ptx::cluster_ctarank()) : 0;
     int I, J;
     upper_tile_coords(blockIdx.x / KS, nt, I, J);
+    DBG_STAMP(0);
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -112,7 +120,9 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    DBG_STAMP(1);
     grid_dep_wait();                                  // the operands are the previous kernel's output
+    DBG_STAMP(2);
 
     const int num_kb = s.npad / kBK / KS;             // this CTA's K slice
     const int kb0 = krank * num_kb;
@@ -175,6 +185,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     // ------------------------------------------------------------------ epilogue
     ptx::mbar_wait(accum_full, 0);
     ptx::tc_fence_after();
+    DBG_STAMP(3);
     grid_dep_launch();                               // the next kernel may start its prologue
 
     const bool diag = (I == J);
@@ -243,12 +254,14 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         ptx::cluster_sync();                         // peers' partials stay valid until all read
     }
 
+    DBG_STAMP(4);
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<kTile>(tmem_base);
     }
+    DBG_STAMP(5);
 }
 
 template <OpType T, bool kSplit, int KS>
