@@ -2,17 +2,19 @@
 //
 // One warp owns 32 consecutive output rows gi0..gi0+31 of an upper tile (I <= J); lane l
 // holds row gi = gi0 + l and processes 32 accumulator columns gj0..gj0+31 at a time (one
-// tcgen05.ld 32x32b.x32):
+// tcgen05.ld 32x32b.x32, or a DSMEM-reduced split-K partial):
 //     v = alpha * acc + beta * D[gi][gj]         D: the operand-precision copy of the addend
-//                                                (Z or Y, upper triangle) or, for the
-//                                                reconstruction, the fp32 input X
+//                                                (Z or Y; hi + lo on the split path) or, for
+//                                                the reconstruction, the fp32 input X
 //     operand copy: out_op[gi][gj] = out_op[gj][gi] = v   (mirrored -> exactly symmetric)
 //     final output: outF[gi][gj]  = outF[gj][gi]  = v     (fp32, masked to n)
-// The mirrored half goes through a per-warp 32x32 smem transpose so that both halves are
-// written as 16-byte row segments.  On a diagonal tile only gj >= gi is valid (scalar path).
-// This is where the polynomial's axpy terms (c_j Y, c_0 Z) and the reconstruction
-// 1/2 X + 1/2 lambda~ X_0 S of Algorithm 2 are fused: no separate
-// elementwise pass touches HBM.
+// Chunks are 32-aligned, so a chunk is either strictly above the diagonal (gj0 > gi0: direct
+// rows + the mirrored block through a per-warp 32x32 smem transpose) or a diagonal 32x32
+// block (gj0 == gi0: the block is symmetrised from its upper triangle through smem and
+// written as full rows).  Callers skip blocks below the diagonal.  Every store is a 16-byte
+// row segment.  This is where the polynomial's axpy terms (c_j Y, c_0 Z) and the reconstruction
+// 1/2 X + 1/2 lambda~ X_0 S of Algorithm 2 are fused: no separate elementwise
+// pass touches HBM.
 #pragma once
 #include "kernels.h"
 #include "optraits.cuh"
@@ -23,154 +25,132 @@ namespace psd {
 // 8-lane phases conflict-free); reused as 32 x 40 fp16 (row stride 80 B)
 constexpr int kEpiWarpSmemBytes = 32 * 36 * 4;
 
+// Symmetrise a diagonal 32x32 block in registers: lane r keeps row r of upper(v) + mirror.
+__device__ __forceinline__ void symmetrize_block(float (&v)[32], uint8_t* wsmem) {
+    const int lane = threadIdx.x & 31;
+    float* S = reinterpret_cast<float*>(wsmem);
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) S[lane * 36 + c] = v[c];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        if (c < lane) v[c] = S[c * 36 + lane];          // element (lane, c) := computed (c, lane)
+    __syncwarp();
+}
+
+// Store a 32x32 block (rows gi0.., columns gj0..) in operand precision; mirror it to
+// (gj0.., gi0..) unless it is a (symmetrised) diagonal block.
 template <OpType T>
-__device__ __forceinline__ void store_op_mirrored(void* out, int64_t opBase, int npad, int gi0, int gj0, bool diag,
-                                                  const float (&v)[32], uint8_t* wsmem) {
+__device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int npad, int gi0, int gj0, bool diag32,
+                                               const float (&v)[32], uint8_t* wsmem) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     const int lane = threadIdx.x & 31;
-    const int gi = gi0 + lane;
-    {
-        op_t* out_op = reinterpret_cast<op_t*>(out);
-        op_t* orow = out_op + opBase + static_cast<int64_t>(gi) * npad;
-        if (!diag) {
-            // direct half: 32 contiguous elements of row gi
-            if constexpr (Tr::kBytes == 2) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
+    op_t* out_op = reinterpret_cast<op_t*>(out);
+    op_t* orow = out_op + opBase + static_cast<int64_t>(gi0 + lane) * npad;
+    if constexpr (Tr::kBytes == 2) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + gj0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t w[4];
+        for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) w[h] = Tr::pack2(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
-                    __stcs(dst + q, make_uint4(w[0], w[1], w[2], w[3]));
-                }
-                // mirrored half: transpose the warp's 32x32 block through smem (row stride 80 B)
-                uint16_t* S = reinterpret_cast<uint16_t*>(wsmem);
-                __syncwarp();
+            for (int h = 0; h < 4; ++h) w[h] = Tr::pack2(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
+            __stcs(dst + q, make_uint4(w[0], w[1], w[2], w[3]));
+        }
+        if (diag32) return;
+        // mirrored block: transpose through smem (row stride 80 B)
+        uint16_t* S = reinterpret_cast<uint16_t*>(wsmem);
+        __syncwarp();
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const op_t cv = Tr::cvt(v[c]);
-                    S[c * 40 + lane] = *reinterpret_cast<const uint16_t*>(&cv);
-                }
-                __syncwarp();
-                const uint4* src = reinterpret_cast<const uint4*>(S + lane * 40);
-                uint4* tdst = reinterpret_cast<uint4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
+        for (int c = 0; c < 32; ++c) {
+            const op_t cv = Tr::cvt(v[c]);
+            S[c * 40 + lane] = *reinterpret_cast<const uint16_t*>(&cv);
+        }
+        __syncwarp();
+        const uint4* src = reinterpret_cast<const uint4*>(S + lane * 40);
+        uint4* tdst = reinterpret_cast<uint4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) __stcs(tdst + q, src[q]);
-            } else {
-                float4* dst = reinterpret_cast<float4*>(orow + gj0);
+        for (int q = 0; q < 4; ++q) __stcs(tdst + q, src[q]);
+    } else {
+        float4* dst = reinterpret_cast<float4*>(orow + gj0);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    __stcs(dst + q, make_float4(Tr::cvt(v[4 * q]), Tr::cvt(v[4 * q + 1]), Tr::cvt(v[4 * q + 2]),
-                                                Tr::cvt(v[4 * q + 3])));
-                float* S = reinterpret_cast<float*>(wsmem);
-                __syncwarp();
+        for (int q = 0; q < 8; ++q)
+            __stcs(dst + q, make_float4(Tr::cvt(v[4 * q]), Tr::cvt(v[4 * q + 1]), Tr::cvt(v[4 * q + 2]),
+                                        Tr::cvt(v[4 * q + 3])));
+        if (diag32) return;
+        float* S = reinterpret_cast<float*>(wsmem);
+        __syncwarp();
 #pragma unroll
-                for (int c = 0; c < 32; ++c) S[c * 36 + lane] = Tr::cvt(v[c]);
-                __syncwarp();
-                const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
-                float4* tdst = reinterpret_cast<float4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
+        for (int c = 0; c < 32; ++c) S[c * 36 + lane] = Tr::cvt(v[c]);
+        __syncwarp();
+        const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+        float4* tdst = reinterpret_cast<float4*>(out_op + opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+        for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+    }
+}
+
+template <OpType T>
+__device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int npad, int gi, int gj0, float beta,
+                                           float (&v)[32]) {
+    using Tr = OpTraits<T>;
+    using op_t = typename Tr::type;
+    const op_t* drow = reinterpret_cast<const op_t*>(D) + opBase + static_cast<int64_t>(gi) * npad + gj0;
+    if constexpr (Tr::kBytes == 2) {
+        const uint4* d4 = reinterpret_cast<const uint4*>(drow);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 d = d4[q];
+            const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                float lo, hi;
+                Tr::unpack2(w[h], lo, hi);
+                v[q * 8 + 2 * h] += beta * lo;
+                v[q * 8 + 2 * h + 1] += beta * hi;
             }
-        } else {
+        }
+    } else {
+        const float4* d4 = reinterpret_cast<const float4*>(drow);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                if (gj < gi) continue;
-                const op_t cv = Tr::cvt(v[i]);
-                orow[gj] = cv;
-                if (gj != gi) out_op[opBase + static_cast<int64_t>(gj) * npad + gi] = cv;
-            }
+        for (int q = 0; q < 8; ++q) {
+            const float4 d = d4[q];
+            v[4 * q] += beta * d.x;
+            v[4 * q + 1] += beta * d.y;
+            v[4 * q + 2] += beta * d.z;
+            v[4 * q + 3] += beta * d.w;
         }
     }
 }
 
 template <OpType T>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
-                                               bool diag, const uint32_t (&raw)[32], uint8_t* wsmem,
+                                               bool /*tile_diag*/, const uint32_t (&raw)[32], uint8_t* wsmem,
                                                int64_t packed_off = -1) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     const int lane = threadIdx.x & 31;
     const int gi = gi0 + lane;
+    const bool diag32 = (gi0 == gj0);                   // diagonal 32x32 block
     const int64_t opBase = static_cast<int64_t>(b) * npad * npad;
     float v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
 
-    if (e.Dop) {                                     // addend in operand precision, ld npad
-        const op_t* drow = reinterpret_cast<const op_t*>(e.Dop) + opBase + static_cast<int64_t>(gi) * npad;
-        if (!diag) {
-            if constexpr (Tr::kBytes == 2) {
-                const uint4* d4 = reinterpret_cast<const uint4*>(drow + gj0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint4 d = d4[q];
-                    const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        float lo, hi;
-                        Tr::unpack2(w[h], lo, hi);
-                        v[q * 8 + 2 * h] += e.beta * lo;
-                        v[q * 8 + 2 * h + 1] += e.beta * hi;
-                    }
-                }
-                if (e.Dop_lo) {
-                    const uint4* l4 = reinterpret_cast<const uint4*>(
-                        reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad + gj0);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 d = l4[q];
-                        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            float lo, hi;
-                            Tr::unpack2(w[h], lo, hi);
-                            v[q * 8 + 2 * h] += e.beta * lo;
-                            v[q * 8 + 2 * h + 1] += e.beta * hi;
-                        }
-                    }
-                }
-            } else {
-                const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 d = d4[q];
-                    v[4 * q] += e.beta * d.x;
-                    v[4 * q + 1] += e.beta * d.y;
-                    v[4 * q + 2] += e.beta * d.z;
-                    v[4 * q + 3] += e.beta * d.w;
-                }
-                if (e.Dop_lo) {
-                    const float4* l4 = reinterpret_cast<const float4*>(
-                        reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad + gj0);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 d = l4[q];
-                        v[4 * q] += e.beta * d.x;
-                        v[4 * q + 1] += e.beta * d.y;
-                        v[4 * q + 2] += e.beta * d.z;
-                        v[4 * q + 3] += e.beta * d.w;
-                    }
-                }
-            }
-        } else {
-            const op_t* lrow = e.Dop_lo ? reinterpret_cast<const op_t*>(e.Dop_lo) + opBase + static_cast<int64_t>(gi) * npad
-                                        : nullptr;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (gj0 + i >= gi)
-                    v[i] += e.beta * (Tr::to_float(drow[gj0 + i]) + (lrow ? Tr::to_float(lrow[gj0 + i]) : 0.0f));
-        }
+    // addends: full 32-element row segments (the values left of the diagonal are discarded
+    // by the symmetrisation of a diagonal block)
+    if (e.Dop) {
+        add_op_row<T>(e.Dop, opBase, npad, gi, gj0, e.beta, v);
+        if (e.Dop_lo) add_op_row<T>(e.Dop_lo, opBase, npad, gi, gj0, e.beta, v);
     }
     if (e.Df) {                                      // fp32 addend (the input X), masked to nDf
         const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
-        if (!diag && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
+        if (gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
             const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const float4 d = d4[q];
+                const float4 d = __ldcs(d4 + q);
                 v[4 * q] += e.beta * d.x;
                 v[4 * q + 1] += e.beta * d.y;
                 v[4 * q + 2] += e.beta * d.z;
@@ -179,16 +159,14 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         } else {
             const bool row_ok = gi < e.nDf;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                v[i] += (row_ok && gj < e.nDf && gj >= gi) ? e.beta * drow[gj] : 0.0f;
-            }
+            for (int i = 0; i < 32; ++i) v[i] += (row_ok && gj0 + i < e.nDf) ? e.beta * drow[gj0 + i] : 0.0f;
         }
     }
+    if (diag32) symmetrize_block(v, wsmem);
 
     if (packed_off >= 0) {
         // row-panel mode: this warp's 32 x 32 block of the tile, unmirrored, row-major tile slot
-        // (row stride 256); the lower part of a diagonal tile is never read by the unpack
+        // (row stride 256)
         const int64_t o = packed_off + static_cast<int64_t>(lane) * 256;
         if (e.packed_f32) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.packed) + o);
@@ -227,34 +205,36 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 lo[i] = w[i] - h;
                 w[i] = h;
             }
-            store_op_mirrored<T>(e.out_lo, opBase, npad, gi0, gj0, diag, lo, wsmem);
+            store_op_block<T>(e.out_lo, opBase, npad, gi0, gj0, diag32, lo, wsmem);
         }
-        store_op_mirrored<T>(e.out_op, opBase, npad, gi0, gj0, diag, w, wsmem);
+        store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem);
     }
 
     if (e.outF) {
         float* F = e.outF + static_cast<int64_t>(b) * e.strideF;
-        const bool fast = !diag && (e.ldF & 3) == 0 && gi0 + 32 <= e.nF && gj0 + 32 <= e.nF;
+        const bool fast = (e.ldF & 3) == 0 && gi0 + 32 <= e.nF && gj0 + 32 <= e.nF;
         if (fast) {
             float4* dst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gi) * e.ldF + gj0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-            float* S = reinterpret_cast<float*>(wsmem);
-            __syncwarp();
+            if (!diag32) {
+                float* S = reinterpret_cast<float*>(wsmem);
+                __syncwarp();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
-            __syncwarp();
-            const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
-            float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * e.ldF + gi0);
+                for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
+                __syncwarp();
+                const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+                float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * e.ldF + gi0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+                for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+            }
         } else if (gi < e.nF) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int gj = gj0 + i;
-                if (gj >= e.nF || gj < gi) continue;     // upper part of this tile only
+                if (gj >= e.nF) continue;
                 F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
-                if (gj != gi) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
+                if (!diag32) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
             }
         }
     }
