@@ -54,7 +54,9 @@ struct GemmShape {
 void make_tile_order(int nt, const char* order, uint32_t* out);
 
 // Host-side TMA descriptor for an operand buffer [batch*npad rows][npad cols].
-bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch);
+bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch, int box_rows = kTile);
+// 1-CTA product kernel tile width for (npad, batch): 128, or 64 for few-tile problems.
+int sym_gemm_bn(int npad, int batch);
 
 // Operand tensor maps of one product: A, B (high parts) and, for split precision, their
 // low parts (A*B ~= Ahi Bhi + Ahi Blo + Alo Bhi, three tcgen05.mma passes, one accumulator).

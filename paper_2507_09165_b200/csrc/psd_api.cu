@@ -53,6 +53,7 @@ struct Workspace {
     double* lambda = nullptr;
     unsigned* status = nullptr;
     CUtensorMap tmap[2 * B_COUNT];
+    CUtensorMap tmap64[2 * B_COUNT];        // 64-row boxes: B operand of the 128 x 64 tiles
     int nblk = 0;
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
@@ -227,7 +228,8 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     // Zero everything once: padded rows/cols of every operand buffer must read as 0.
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
-        if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch)) {
+        if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch) ||
+            !make_operand_tmap(&ws.tmap64[i], ws.op_buf[i], op, npad, batch, 64)) {
             free_ws(ws);
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
         }
@@ -446,12 +448,14 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         sc[B_Y] = h->s_y;
         sc[B_UA] = sc[B_UB] = h->s_u;
     }
+    const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
+    const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     auto maps = [&](int A, int B) {
         OperandMaps m;
         m.a = ws.tmap[A];
-        m.b = ws.tmap[B];
+        m.b = bmaps[B];
         m.a_lo = ws.tmap[split ? A + B_COUNT : A];
-        m.b_lo = ws.tmap[split ? B + B_COUNT : B];
+        m.b_lo = bmaps[split ? B + B_COUNT : B];
         return m;
     };
     // (a2) scale + convert; the products-free sign chain finishes here
@@ -1075,11 +1079,13 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     const GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
+    const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
+    const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     OperandMaps m;
     m.a = ws.tmap[B_XA];
-    m.b = ws.tmap[B_XB];
+    m.b = bmaps[B_XB];
     m.a_lo = ws.tmap[split ? B_XA + B_COUNT : B_XA];
-    m.b_lo = ws.tmap[split ? B_XB + B_COUNT : B_XB];
+    m.b_lo = bmaps[split ? B_XB + B_COUNT : B_XB];
     e = (npad % 256 == 0 && use_pair_kernel(n, batch))
             ? launch_sym_gemm_2cta(ws.op, split, m, shape, ep, st)
             : launch_sym_gemm(ws.op, split, m, shape, ep, st);

@@ -35,19 +35,24 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTile * kBlockKBytes;                 // 16 KB per operand tile
 constexpr int kRingBytes1 = 128 * 1024;
-template <bool kSplit> struct Ring1 {
-    static constexpr int kStageBytes = (kSplit ? 4 : 2) * kTileBytes;   // A, B (+ A_lo, B_lo)
-    static constexpr int kStages = kRingBytes1 / kStageBytes;           // 4 or 2
+template <bool kSplit, int BN> struct Ring1 {
+    static constexpr int kBBytes = BN * kBlockKBytes;                   // B tile: BN rows
+    static constexpr int kStageBytes = (kSplit ? 2 : 1) * (kTileBytes + kBBytes);   // A, B (+ A_lo, B_lo)
+    static constexpr int kStages = kRingBytes1 / kStageBytes;
 };
 constexpr int kSmemBytes = kRingBytes1 + 1024 + 256 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers, staging
 
-__device__ __forceinline__ void upper_tile_coords(int t, int nt, int& I, int& J) {
-    // row-major enumeration of {(I, J): 0 <= I <= J < nt}
+// Row-major enumeration of the 128 x BN tiles (row block I, column block J) that hold any
+// upper-triangle element: J >= I * (128 / BN).
+template <int BN>
+__device__ __forceinline__ void upper_tile_coords(int t, int npad, int& I, int& J) {
+    constexpr int r = kTile / BN;
+    const int ncb = npad / BN;
     int i = 0;
     int rem = t;
-    while (rem >= nt - i) { rem -= nt - i; ++i; }
+    while (rem >= ncb - i * r) { rem -= ncb - i * r; ++i; }
     I = i;
-    J = i + rem;
+    J = i * r + rem;
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -73,15 +78,17 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
     return v;
 }
 
-template <OpType T, bool kSplit, int KS>
+template <OpType T, bool kSplit, int KS, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
-    constexpr int kStages = Ring1<kSplit>::kStages;
-    constexpr int kStageBytes = Ring1<kSplit>::kStageBytes;
+    static_assert(KS == 1 || BN == kTile, "cluster split-K uses 128-wide tiles");
+    constexpr int kStages = Ring1<kSplit, BN>::kStages;
+    constexpr int kStageBytes = Ring1<kSplit, BN>::kStageBytes;
+    constexpr int kBBytes = Ring1<kSplit, BN>::kBBytes;
     constexpr int kBK = kBlockKBytes / Tr::kBytes;     // K elements per block (64 f16 / 32 tf32)
     constexpr int kUmmaK = 32 / Tr::kBytes;            // K per tcgen05.mma (16 f16 / 8 tf32)
-    constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, kTile);
+    constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, BN);
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -94,11 +101,10 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int nt = s.npad / kTile;
     const int b = blockIdx.y;
     const int krank = (KS > 1) ? static_cast<int>(ptx::cluster_ctarank()) : 0;
     int I, J;
-    upper_tile_coords(blockIdx.x / KS, nt, I, J);
+    upper_tile_coords<BN>(blockIdx.x / KS, s.npad, I, J);
     DBG_STAMP(0);
 
     if (warp == 0) {
@@ -114,7 +120,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         }
         __syncwarp();
     } else if (warp == 1) {
-        ptx::tmem_alloc<kTile>(tmem_slot);
+        ptx::tmem_alloc<BN>(tmem_slot);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -127,7 +133,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     const int num_kb = s.npad / kBK / KS;             // this CTA's K slice
     const int kb0 = krank * num_kb;
     const int rowA = b * s.npad + I * kTile;
-    const int rowB = b * s.npad + J * kTile;
+    const int rowB = b * s.npad + J * BN;
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -142,8 +148,8 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 ptx::tma_load_2d(sa, &tm.a, &full[st], kx, rowA, pol);
                 ptx::tma_load_2d(sa + kTileBytes, &tm.b, &full[st], kx, rowB, pol);
                 if constexpr (kSplit) {
-                    ptx::tma_load_2d(sa + 2 * kTileBytes, &tm.a_lo, &full[st], kx, rowA, pol);
-                    ptx::tma_load_2d(sa + 3 * kTileBytes, &tm.b_lo, &full[st], kx, rowB, pol);
+                    ptx::tma_load_2d(sa + kTileBytes + kBBytes, &tm.a_lo, &full[st], kx, rowA, pol);
+                    ptx::tma_load_2d(sa + 2 * kTileBytes + kBBytes, &tm.b_lo, &full[st], kx, rowB, pol);
                 }
             }
         }
@@ -169,8 +175,8 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                     const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);   // 32 B per K step
                     mma(adesc + koff, bdesc + koff, (kb | k) != 0);
                     if constexpr (kSplit) {
-                        const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes);
-                        const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes);
+                        const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + kTileBytes + kBBytes);
+                        const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes + kBBytes);
                         mma(adesc + koff, blo + koff, 1u);            // A_hi B_lo
                         mma(alo + koff, bdesc + koff, 1u);            // A_lo B_hi
                     }
@@ -188,7 +194,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     DBG_STAMP(3);
     grid_dep_launch();                               // the next kernel may start its prologue
 
-    const bool diag = (I == J);
+    const bool diag = (I * kTile < J * BN + BN) && (J * BN < I * kTile + kTile);   // tile meets the diagonal
     float alpha = e.alpha;
     if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
     uint8_t* wsmem = epi_smem + warp * kEpiWarpSmemBytes;
@@ -196,8 +202,8 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     if constexpr (KS == 1) {
         const int gi0 = I * kTile + warp * 32;      // this warp's first row (TMEM lanes 32w..)
 #pragma unroll 1
-        for (int c0 = 0; c0 < kTile; c0 += 32) {
-            const int gj0 = J * kTile + c0;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            const int gj0 = J * BN + c0;
             if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
             uint32_t raw[32];
             ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
@@ -259,23 +265,24 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<kTile>(tmem_base);
+        ptx::tmem_dealloc<BN>(tmem_base);
     }
     DBG_STAMP(5);
 }
 
-template <OpType T, bool kSplit, int KS>
+template <OpType T, bool kSplit, int KS, int BN>
 cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               kSmemBytes);
+        cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit, KS, BN>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
-    const int nt = s.npad / kTile;
+    const int nrb = s.npad / kTile, ncb = s.npad / BN;
+    const int tiles = nrb * ncb - (kTile / BN) * nrb * (nrb - 1) / 2;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(nt * (nt + 1) / 2 * KS, s.batch);
+    cfg.gridDim = dim3(tiles * KS, s.batch);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = stream;
@@ -296,15 +303,17 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, sym_gemm_kernel<T, kSplit, KS>, m, s, e);
+    return cudaLaunchKernelEx(&cfg, sym_gemm_kernel<T, kSplit, KS, BN>, m, s, e);
 }
 
 template <OpType T, bool kSplit>
-cudaError_t launch_ks(int ks, const OperandMaps& m, const GemmShape& s, const EpiParams& e, cudaStream_t stream) {
+cudaError_t launch_ks(int ks, int bn, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
+                      cudaStream_t stream) {
+    if (bn == 64) return launch_t<T, kSplit, 1, 64>(m, s, e, stream);
     switch (ks) {
-        case 4: return launch_t<T, kSplit, 4>(m, s, e, stream);
-        case 2: return launch_t<T, kSplit, 2>(m, s, e, stream);
-        default: return launch_t<T, kSplit, 1>(m, s, e, stream);
+        case 4: return launch_t<T, kSplit, 4, kTile>(m, s, e, stream);
+        case 2: return launch_t<T, kSplit, 2, kTile>(m, s, e, stream);
+        default: return launch_t<T, kSplit, 1, kTile>(m, s, e, stream);
     }
 }
 
@@ -312,7 +321,10 @@ cudaError_t launch_ks(int ks, const OperandMaps& m, const GemmShape& s, const Ep
 
 // Split-K factor for a few-tile problem: fill the SMs (one wave), keep >= 4 k-blocks per CTA.
 int sym_gemm_split_k(int npad, int batch, OpType t) {
-    static const int forced = std::getenv("PSD_SPLITK") ? std::atoi(std::getenv("PSD_SPLITK")) : 0;
+    // measured (tools/latency_probe.py, n = 1024, 19 products): KS = 1 211 us, 2 229 us, 4 386 us --
+    // the cluster barriers / DSMEM reduction cost more than the extra SMs gain once the epilogue
+    // is vectorised, so split-K is off unless forced (PSD_SPLITK = 2 | 4)
+    static const int forced = std::getenv("PSD_SPLITK") ? std::atoi(std::getenv("PSD_SPLITK")) : 1;
     if (forced == 1 || forced == 2 || forced == 4) return forced;
     const int nt = npad / kTile;
     const int tiles = nt * (nt + 1) / 2 * batch;
@@ -322,16 +334,25 @@ int sym_gemm_split_k(int npad, int batch, OpType t) {
     return ks;
 }
 
+// 128 x 64 tiles for few-tile problems: twice the CTAs, half the MMA and epilogue per CTA.
+int sym_gemm_bn(int npad, int batch) {
+    static const int forced = std::getenv("PSD_BN") ? std::atoi(std::getenv("PSD_BN")) : 0;
+    if (forced == 64 || forced == 128) return forced;
+    const int nt = npad / kTile;
+    return (nt * (nt + 1) / 2 * batch < 100) ? 64 : 128;
+}
+
 cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
                             cudaStream_t stream) {
     const int ks = sym_gemm_split_k(s.npad, s.batch, t);
+    const int bn = sym_gemm_bn(s.npad, s.batch);
     switch (t) {
-        case OpType::F16: return split ? launch_ks<OpType::F16, true>(ks, m, s, e, stream)
-                                       : launch_ks<OpType::F16, false>(ks, m, s, e, stream);
-        case OpType::BF16: return split ? launch_ks<OpType::BF16, true>(ks, m, s, e, stream)
-                                        : launch_ks<OpType::BF16, false>(ks, m, s, e, stream);
-        case OpType::TF32: return split ? launch_ks<OpType::TF32, true>(ks, m, s, e, stream)
-                                        : launch_ks<OpType::TF32, false>(ks, m, s, e, stream);
+        case OpType::F16: return split ? launch_ks<OpType::F16, true>(ks, bn, m, s, e, stream)
+                                       : launch_ks<OpType::F16, false>(ks, bn, m, s, e, stream);
+        case OpType::BF16: return split ? launch_ks<OpType::BF16, true>(ks, bn, m, s, e, stream)
+                                        : launch_ks<OpType::BF16, false>(ks, bn, m, s, e, stream);
+        case OpType::TF32: return split ? launch_ks<OpType::TF32, true>(ks, bn, m, s, e, stream)
+                                        : launch_ks<OpType::TF32, false>(ks, bn, m, s, e, stream);
     }
     return cudaErrorInvalidValue;
 }
@@ -354,7 +375,7 @@ EncodeFn get_encode() {
 }
 }  // namespace
 
-bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch) {
+bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch, int box_rows) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     const int bytes = (t == OpType::TF32) ? 4 : 2;
@@ -363,7 +384,7 @@ bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, i
                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(npad), static_cast<cuuint64_t>(npad) * batch};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(npad) * bytes};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockKBytes / bytes), static_cast<cuuint32_t>(kTile)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockKBytes / bytes), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
