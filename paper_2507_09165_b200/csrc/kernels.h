@@ -83,6 +83,7 @@ struct SmallStep {
     float alpha, beta, out_scale;
     int final_mode;           // 0: chain product; 1: P = lambda~ alpha acc + beta X; 2: S = alpha acc + beta D
     int reload_x0;            // restage X_0 into the Y slot before this product
+    int mirror;               // make the output exactly symmetric (stage outputs Z; reading R20)
 };
 struct SmallPlan {
     int nsteps;

@@ -384,6 +384,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             int sa = slot_of(s.A), sb = slot_of(s.B);
             double scale_a = sc_slot[sa], scale_b = sc_slot[sb];
             q.reload_x0 = 0;
+            q.mirror = 0;
             q.slot_d = -1;
             q.beta = static_cast<float>(s.beta);
             q.out_scale = 1.0f;
@@ -399,6 +400,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
                 q.final_mode = 0;
                 q.slot_out = small_slot_offset(sp, slot_of(s.out_op));
                 q.out_scale = static_cast<float>(sc_slot[slot_of(s.out_op)]);
+                q.mirror = slot_of(s.out_op) == 0 ? 1 : 0;
             }
             if (s.D >= 0) {
                 q.slot_d = small_slot_offset(sp, slot_of(s.D));

@@ -263,8 +263,13 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             if (st.final_mode == 0) {
                 // in place: the MMA that read this slot has completed (mma_bar)
                 store_row<kSplit>(mat + st.slot_out, row, v, st.out_scale);
-                __syncthreads();
-                mirror_lower<kSplit>(mat + st.slot_out, row);
+                if (st.mirror) {
+                    // the stage output Z must be exactly symmetric: its antisymmetric part would
+                    // grow like prod c_{t,0} over the stages (R20); Y and U need not be (their
+                    // rounding-level asymmetry is not amplified -- rounding model)
+                    __syncthreads();
+                    mirror_lower<kSplit>(mat + st.slot_out, row);
+                }
                 fence_proxy_async_smem();
                 __syncthreads();
             } else {
