@@ -84,6 +84,42 @@ __device__ __forceinline__ void mirror_lower(uint8_t* slot, int row) {
     }
 }
 
+// Block version: the 64x64 fp16 part(s) of a slot as 8x8 blocks of 8x8 elements; block (bi, bj),
+// bi > bj, becomes the transpose of block (bj, bi); a diagonal block takes its lower triangle from
+// its upper triangle.  36 block tasks per matrix part, one per thread (16-byte smem accesses).
+__device__ __forceinline__ void mirror_block_task(uint8_t* part, int task) {
+    // task -> (bi >= bj): row-major over the lower triangle of the 8 x 8 block grid
+    int bi = 0, rem = task;
+    while (rem > bi) { rem -= bi + 1; ++bi; }
+    const int bj = rem;
+    uint16_t blk[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int row = 8 * bj + r;                    // source: block (bj, bi) (upper)
+        const uint4 q = *reinterpret_cast<const uint4*>(part + swz(row, bi));
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(&q);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) blk[r][c] = h[c];
+    }
+    if (bi != bj) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            __align__(16) uint16_t o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) o[c] = blk[c][r];   // transpose
+            *reinterpret_cast<uint4*>(part + swz(8 * bi + r, bj)) = *reinterpret_cast<const uint4*>(o);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            __align__(16) uint16_t o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) o[c] = (c >= r) ? blk[r][c] : blk[c][r];
+            *reinterpret_cast<uint4*>(part + swz(8 * bi + r, bj)) = *reinterpret_cast<const uint4*>(o);
+        }
+    }
+}
+
 template <bool kSplit>
 __device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta, float (&v)[64]) {
     // v += beta * (hi [+ lo]) of the slot row
@@ -268,7 +304,12 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     // grow like prod c_{t,0} over the stages (R20); Y and U need not be (their
                     // rounding-level asymmetry is not amplified -- rounding model)
                     __syncthreads();
-                    mirror_lower<kSplit>(mat + st.slot_out, row);
+                    constexpr int kParts = kSplit ? 2 : 1;
+                    for (int task = threadIdx.x; task < 2 * kParts * 36; task += kThreadsS) {
+                        const int mm = task / (kParts * 36);
+                        const int part = (task / 36) % kParts;
+                        mirror_block_task(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes, task % 36);
+                    }
                 }
                 fence_proxy_async_smem();
                 __syncthreads();
