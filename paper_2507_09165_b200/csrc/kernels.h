@@ -88,6 +88,7 @@ struct SmallStep {
 struct SmallPlan {
     int nsteps;
     float s_x0;               // operand scale of X_0
+    unsigned long long* dbg;  // debug: per-phase clock totals of CTA 0 (NULL in production)
     SmallStep steps[40];
 };
 int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U

@@ -415,8 +415,20 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             evs = {take_event(h), take_event(h)};
             cudaEventRecord(evs.first, st);
         }
+        const bool dbg = std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        if (dbg) {
+            sp_plan.dbg = reinterpret_cast<unsigned long long*>(ws.partial);
+            cudaMemsetAsync(ws.partial, 0, 64, st);
+        }
         e = launch_small_batch(sp, X, out, n, batch, lambda_out, ws.status, sp_plan, st);
         if (e != cudaSuccess) return cuda_fail(e, "small_batch");
+        if (dbg) {
+            unsigned long long t[4] = {};
+            cudaStreamSynchronize(st);
+            cudaMemcpy(t, sp_plan.dbg, sizeof(t), cudaMemcpyDeviceToHost);
+            if (t[3]) std::fprintf(stderr, "psd small stamps (cycles/step, CTA 0, %llu steps): mma %.0f, tmem-ld %.0f, epilogue+sync %.0f\n",
+                                   t[3], double(t[0]) / t[3], double(t[1]) / t[3], double(t[2]) / t[3]);
+        }
         h->kernel_launches += 1;
         if (evs.first) {
             cudaEventRecord(evs.second, st);

@@ -254,6 +254,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 fence_proxy_async_smem();
                 __syncthreads();
             }
+            long long t_a = clock64();
             if (threadIdx.x == 0) {
                 ptx::tc_fence_after();
 #pragma unroll 1
@@ -280,6 +281,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             ptx::mbar_wait(mma_bar, mma_phase);
             mma_phase ^= 1;
             ptx::tc_fence_after();
+            long long t_b = clock64();
 
             float v[64];
             {
@@ -295,6 +297,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 for (int i = 0; i < 32; ++i) v[32 + i] = st.alpha * __uint_as_float(raw[i]);
             }
             ptx::tc_fence_before();
+            long long t_c = clock64();
             if (st.slot_d >= 0) add_row<kSplit>(mat + st.slot_d, row, st.beta, v);
             if (st.final_mode == 0) {
                 // in place: the MMA that read this slot has completed (mma_bar)
