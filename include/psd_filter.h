@@ -74,10 +74,19 @@ typedef enum {
 } psd_precision_t;
 
 /* FROBENIUS: lambda~ = ||X||_F computed on the device (default).
- * USER: lambda~ taken from psd_project_ex's lambda_in (device, one double per matrix). */
+ * USER: lambda~ taken from psd_project_ex's lambda_in (device, one double per matrix).
+ * LANCZOS: Algorithm 2 line 1 with Theorem 2: on X0 = X / ||X||_F (in the
+ *   operand precision: the matrix the chain actually filters), a k-step Lanczos run on X0^2
+ *   (k = 20 by default, the paper's; full re-orthogonalisation) gives the largest Ritz pair
+ *   (sigma, q); lambda~ = ||X||_F * min(1, sqrt(sigma + ||X0^2 q - sigma q||) * safety).
+ *   Theorem 2 assumes lambda_1(X^2) is the eigenvalue nearest sigma, which the paper finds
+ *   to hold in practice; `safety` (default 1.01) absorbs the operand rounding.  Never
+ *   looser than FROBENIUS.  Costs 2k + 2 matrix-vector passes over the operand copy.
+ *   n <= 51200.  Reading R21. */
 typedef enum {
     PSD_BOUND_FROBENIUS = 0,
-    PSD_BOUND_USER = 1
+    PSD_BOUND_USER = 1,
+    PSD_BOUND_LANCZOS = 2
 } psd_bound_t;
 
 /* Library version string, e.g. "psdfilter 0.1 sm_100a". Never NULL. Host only. */
@@ -109,6 +118,10 @@ psd_status_t psd_filter_set_precision(psd_filter_t h, psd_precision_t prec);
 
 /* Bound used to normalise X (default PSD_BOUND_FROBENIUS). Host only. */
 psd_status_t psd_filter_set_bound(psd_filter_t h, psd_bound_t bound);
+
+/* PSD_BOUND_LANCZOS parameters: steps in [1, 64] (default 20; min(steps, n) are
+ * run), safety in [1, 2] (default 1.01).  Host only; PSD_EINVAL outside the ranges. */
+psd_status_t psd_filter_set_lanczos(psd_filter_t h, int steps, double safety);
 
 /* Number of tensor-core products one matrix costs: sum_t (d_t+1)/2 over stages with
  * d_t > 1, plus 1 if `for_project` (the reconstruction of P:L757).  Host only.

@@ -55,10 +55,13 @@ class Filter:
     stages    sequence of coefficient tuples (c_{t,0}, c_{t,1}, ...) of x, x^3, ...;
               stabilisation factors already folded (see ``filters``).
     precision 'fp16' (default, the paper's half path), 'bf16', 'tf32', 'tf32x3'.
-    bound     'frobenius' (lambda~ = ||X||_F on device) or 'user' (pass lambda_in).
+    bound     'frobenius' (lambda~ = ||X||_F on device), 'lanczos' (Algorithm 2 line 1:
+              Theorem 2 bound from a ``lanczos_steps``-step Lanczos run on X^2, times
+              ``lanczos_safety``; never looser than Frobenius) or 'user'
+              (pass lambda_in).
     """
 
-    def __init__(self, stages, eps=1e-3, precision="fp16", bound="frobenius"):
+    def __init__(self, stages, eps=1e-3, precision="fp16", bound="frobenius", lanczos_steps=20, lanczos_safety=1.01):
         self._lib = load()
         self.stages = [tuple(float(v) for v in c) for c in stages]
         degrees, coeffs = filters.flatten(self.stages)
@@ -72,6 +75,7 @@ class Filter:
         self.bound = bound
         check(self._lib.psd_filter_set_precision(self._h, PRECISIONS[precision]), "psd_filter_set_precision")
         check(self._lib.psd_filter_set_bound(self._h, BOUNDS[bound]), "psd_filter_set_bound")
+        check(self._lib.psd_filter_set_lanczos(self._h, int(lanczos_steps), float(lanczos_safety)), "psd_filter_set_lanczos")
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -14,7 +14,7 @@ PSD_OK, PSD_EINVAL, PSD_ENOMEM, PSD_ECUDA, PSD_ENCCL, PSD_ENONFINITE, PSD_EUNSUP
 STATUS_NAMES = {0: "PSD_OK", 1: "PSD_EINVAL", 2: "PSD_ENOMEM", 3: "PSD_ECUDA", 4: "PSD_ENCCL",
                 5: "PSD_ENONFINITE", 6: "PSD_EUNSUPPORTED"}
 PRECISIONS = {"fp16": 0, "bf16": 1, "tf32": 2, "tf32x3": 3, "fp16x3": 4, "bf16x3": 5}
-BOUNDS = {"frobenius": 0, "user": 1}
+BOUNDS = {"frobenius": 0, "user": 1, "lanczos": 2}
 
 # (name, restype, argtypes) for every symbol include/psd_filter.h declares.
 _c = ctypes
@@ -25,6 +25,7 @@ SIGNATURES = [
     ("psd_filter_destroy", None, [_c.c_void_p]),
     ("psd_filter_set_precision", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_filter_set_bound", _c.c_int, [_c.c_void_p, _c.c_int]),
+    ("psd_filter_set_lanczos", _c.c_int, [_c.c_void_p, _c.c_int, _c.c_double]),
     ("psd_filter_gemm_count", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_project", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
     ("psd_sign", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),

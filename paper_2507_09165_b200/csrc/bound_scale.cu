@@ -9,6 +9,8 @@
 
 #include "kernels.h"
 
+#include <utility>
+
 namespace psd {
 
 namespace {
@@ -225,6 +227,356 @@ cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int 
                 static_cast<float>(op_scale), outF, post);
             break;
     }
+    return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Lanczos bound: Algorithm 2 line 1 with Theorem 2.  The north star's
+// "power-iteration bound" is taken in the paper's form -- a k-step Krylov (Lanczos) run on X^2,
+// which contains the k-step power iterate and costs the same two matrix-vector products per
+// step (reading R21).  Everything runs on the symmetric operand copy X0 = X / lambda_F (entries
+// |.| <= 1, so fp16 is safe; the chain itself runs on this rounded matrix):
+//   v_0 = h / ||h||  (h: fixed counter-hash start vector, the oracle implements the same hash)
+//   k = 0..m-1:  w = X0 (X0 v_k);  two classical Gram-Schmidt passes against v_0..v_k
+//                (alpha_k = the v_k coefficients); beta_k = ||w||; v_{k+1} = w / beta_k
+//   (theta, y) = largest eigenpair of the tridiagonal T_m (bisection + inverse iteration)
+//   q = V y;  sigma = q^T X0^2 q / q^T q;  r = || X0^2 q / |q| - sigma q / |q| ||
+//   lambda~ = lambda_F * min(1, sqrt(sigma + r) / s0 * safety)   (never looser than Frobenius)
+// All reductions are fixed-order (per-block partials summed in index order): deterministic.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int kGemvRows = 32;        // rows per block
+constexpr int kGemvThreads = 256;    // 8 warps x 4 rows
+constexpr int kLzThreads = 1024;
+constexpr int kMaxLz = 64;
+
+template <typename E>
+__device__ __forceinline__ float elem_to_float(E v);
+template <> __device__ __forceinline__ float elem_to_float<__half>(__half v) { return __half2float(v); }
+template <> __device__ __forceinline__ float elem_to_float<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ double sum_partials(const double* p, int count) {
+    double s = 0.0;
+    for (int i = 0; i < count; ++i) s += p[i];          // fixed order: identical in every block
+    return s;
+}
+
+// block-wide sum (fixed order), every thread gets the result; red: >= 32 doubles of smem
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    return t;
+}
+
+// y[b] = A[b] x[b] / sqrt(xnorm2[b]) (xpart == nullptr: no normalisation); ypart[b][blk] = sum y^2
+template <typename E>
+__global__ void __launch_bounds__(kGemvThreads)
+lz_gemv_kernel(const E* __restrict__ A, int npad, const float* __restrict__ x, int64_t xstride,
+               const double* __restrict__ xpart, int xparts, float* __restrict__ y, double* __restrict__ ypart) {
+    extern __shared__ float xs[];                 // npad floats
+    __shared__ double red[kGemvThreads / 32];
+    const int b = blockIdx.y;
+    double inv = 1.0;
+    if (xpart) {
+        const double nn = sum_partials(xpart + static_cast<int64_t>(b) * xparts, xparts);
+        inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+    }
+    for (int j = threadIdx.x; j < npad; j += kGemvThreads)
+        xs[j] = static_cast<float>(x[static_cast<int64_t>(b) * xstride + j] * inv);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc2 = 0.0;
+    for (int rr = 0; rr < kGemvRows / 8; ++rr) {
+        const int i = blockIdx.x * kGemvRows + warp * (kGemvRows / 8) + rr;
+        if (i >= npad) break;
+        const E* row = A + (static_cast<int64_t>(b) * npad + i) * npad;
+        float s = 0.0f;
+        for (int j = lane * 8; j < npad; j += 32 * 8) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(row + j);
+            if constexpr (sizeof(E) == 2) {
+                const E* e8 = reinterpret_cast<const E*>(&raw);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s += elem_to_float<E>(e8[k]) * xs[j + k];
+            } else {
+                const float* f4 = reinterpret_cast<const float*>(&raw);
+                const uint4 raw2 = *reinterpret_cast<const uint4*>(row + j + 4);
+                const float* g4 = reinterpret_cast<const float*>(&raw2);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s += f4[k] * xs[j + k] + g4[k] * xs[j + 4 + k];
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            y[static_cast<int64_t>(b) * npad + i] = s;
+            acc2 += static_cast<double>(s) * s;
+        }
+    }
+    if (lane == 0) red[warp] = acc2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kGemvThreads / 32; ++w) t += red[w];
+        ypart[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__device__ __forceinline__ float start_hash(int j) {
+    // counter-based start vector, entries in [0.5, 1.5) (oracle: same hash, oracle/bound.py)
+    uint32_t h = static_cast<uint32_t>(j) * 2654435761u + 0x9E3779B9u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    return 0.5f + static_cast<float>(h & 0xFFFFu) / 65536.0f;
+}
+
+// V: [batch][m+1][npad]; v_0 = h / ||h|| on the first n entries
+__global__ void __launch_bounds__(kLzThreads) lz_init_kernel(float* __restrict__ V, int n, int npad, int64_t vstride) {
+    __shared__ double red[32];
+    float* v = V + static_cast<int64_t>(blockIdx.x) * vstride;
+    double s = 0.0;
+    for (int j = threadIdx.x; j < n; j += kLzThreads) {
+        const double hj = start_hash(j);
+        s += hj * hj;
+    }
+    const double inv = 1.0 / sqrt(block_sum(s, red));
+    for (int j = threadIdx.x; j < npad; j += kLzThreads) v[j] = j < n ? static_cast<float>(start_hash(j) * inv) : 0.0f;
+}
+
+// one Lanczos step for matrix blockIdx.x: w (= X0^2 v_k, in W) orthogonalised against v_0..v_k
+// (CGS2), alpha_k / beta_k recorded, v_{k+1} = w / beta_k.  Dot products: warp i handles the
+// basis vectors i, i + 32, ... (warp-shuffle reductions, no block barrier per vector).
+__global__ void __launch_bounds__(kLzThreads)
+lz_step_kernel(float* __restrict__ V, float* __restrict__ W, int npad, int64_t vstride, int k, double* __restrict__ AB) {
+    __shared__ double c[kMaxLz + 1];
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    float* Vb = V + static_cast<int64_t>(b) * vstride;
+    float* w = W + static_cast<int64_t>(b) * npad;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double alpha = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int i = warp; i <= k; i += kLzThreads / 32) {
+            const float* vi = Vb + static_cast<int64_t>(i) * npad;
+            double s = 0.0;
+            for (int j = lane; j < npad; j += 32) s += static_cast<double>(vi[j]) * w[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) c[i] = s;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < npad; j += kLzThreads) {
+            double t = w[j];
+            for (int i = 0; i <= k; ++i) t -= c[i] * Vb[static_cast<int64_t>(i) * npad + j];
+            w[j] = static_cast<float>(t);
+        }
+        alpha += c[k];
+        __syncthreads();
+    }
+    double s = 0.0;
+    for (int j = threadIdx.x; j < npad; j += kLzThreads) s += static_cast<double>(w[j]) * w[j];
+    const double beta = sqrt(block_sum(s, red));
+    const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+    float* vn = Vb + static_cast<int64_t>(k + 1) * npad;
+    for (int j = threadIdx.x; j < npad; j += kLzThreads) vn[j] = static_cast<float>(w[j] * inv);
+    if (threadIdx.x == 0) {
+        AB[static_cast<int64_t>(b) * 2 * kMaxLz + k] = alpha;
+        AB[static_cast<int64_t>(b) * 2 * kMaxLz + kMaxLz + k] = beta;
+    }
+}
+
+// number of eigenvalues of the tridiagonal (a, e) smaller than x (Sturm sequence)
+__device__ int sturm_count(const double* a, const double* e, int m, double x) {
+    int cnt = 0;
+    double d = a[0] - x;
+    if (d < 0.0) ++cnt;
+    for (int i = 1; i < m; ++i) {
+        if (d == 0.0) d = 1e-300;
+        d = (a[i] - x) - e[i - 1] * e[i - 1] / d;
+        if (d < 0.0) ++cnt;
+    }
+    return cnt;
+}
+
+// Largest Ritz pair of T_m (thread 0: bisection + two inverse-iteration solves with partial
+// pivoting), then q = V y by the whole block; qn2 = ||q||^2.
+__global__ void __launch_bounds__(kLzThreads)
+lz_ritz_kernel(const float* __restrict__ V, int npad, int64_t vstride, int m, const double* __restrict__ AB,
+               float* __restrict__ q, double* __restrict__ qn2) {
+    __shared__ double a[kMaxLz], e[kMaxLz], y[kMaxLz];
+    __shared__ double d[kMaxLz], du[kMaxLz], du2[kMaxLz], dl[kMaxLz];
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < m; ++i) {
+            a[i] = AB[static_cast<int64_t>(b) * 2 * kMaxLz + i];
+            e[i] = AB[static_cast<int64_t>(b) * 2 * kMaxLz + kMaxLz + i];   // e[m-1] unused
+        }
+        double lo = a[0], hi = a[0];
+        for (int i = 0; i < m; ++i) {
+            const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+            lo = fmin(lo, a[i] - r);
+            hi = fmax(hi, a[i] + r);
+        }
+        for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(fabs(lo), fabs(hi)); ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (sturm_count(a, e, m, mid) <= m - 1) lo = mid; else hi = mid;
+        }
+        const double theta = hi;
+        const double mu = theta + 1e-12 * fmax(fabs(theta), 1e-300);
+        for (int i = 0; i < m; ++i) y[i] = 1.0;
+        for (int rep = 0; rep < 2; ++rep) {
+            for (int i = 0; i < m; ++i) {
+                d[i] = a[i] - mu;
+                du[i] = e[i];
+                dl[i] = e[i];
+                du2[i] = 0.0;
+            }
+            for (int i = 0; i < m - 1; ++i) {
+                if (fabs(d[i]) >= fabs(dl[i])) {
+                    if (d[i] == 0.0) d[i] = 1e-300;
+                    const double f = dl[i] / d[i];
+                    d[i + 1] -= f * du[i];
+                    y[i + 1] -= f * y[i];
+                } else {
+                    const double f = d[i] / dl[i];
+                    const double t = d[i + 1];
+                    d[i] = dl[i];
+                    d[i + 1] = du[i] - f * t;
+                    if (i < m - 2) {
+                        du2[i] = du[i + 1];
+                        du[i + 1] = -f * du2[i];
+                    }
+                    du[i] = t;
+                    const double bt = y[i];
+                    y[i] = y[i + 1];
+                    y[i + 1] = bt - f * y[i];
+                }
+            }
+            if (d[m - 1] == 0.0) d[m - 1] = 1e-300;
+            y[m - 1] /= d[m - 1];
+            if (m > 1) y[m - 2] = (y[m - 2] - du[m - 2] * y[m - 1]) / d[m - 2];
+            for (int i = m - 3; i >= 0; --i) y[i] = (y[i] - du[i] * y[i + 1] - du2[i] * y[i + 2]) / d[i];
+            double nn = 0.0;
+            for (int i = 0; i < m; ++i) nn += y[i] * y[i];
+            const double inv = nn > 0.0 && isfinite(nn) ? 1.0 / sqrt(nn) : 0.0;
+            for (int i = 0; i < m; ++i) y[i] *= inv;
+        }
+    }
+    __syncthreads();
+    const float* Vb = V + static_cast<int64_t>(b) * vstride;
+    double s = 0.0;
+    for (int j = threadIdx.x; j < npad; j += kLzThreads) {
+        double t = 0.0;
+        for (int i = 0; i < m; ++i) t += y[i] * Vb[static_cast<int64_t>(i) * npad + j];
+        q[static_cast<int64_t>(b) * npad + j] = static_cast<float>(t);
+        s += t * t;
+    }
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) qn2[b] = tot;
+}
+
+// r^2 partials: || |w| z - sigma q / |q| ||^2 with w = X0 q/|q| (partials wpart: sigma = |w|^2)
+// and z = X0 w / |w|, so X0^2 q/|q| = |w| z.
+__global__ void lz_residual_kernel(const float* __restrict__ q, const double* __restrict__ qn2, const float* __restrict__ z,
+                                   const double* __restrict__ wpart, int parts, int npad, double* __restrict__ rpart) {
+    __shared__ double red[32];
+    const int b = blockIdx.y;
+    const double invq = qn2[b] > 0.0 ? 1.0 / sqrt(qn2[b]) : 0.0;
+    const double sigma = sum_partials(wpart + static_cast<int64_t>(b) * parts, parts);
+    const double wn = sqrt(sigma);
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += gridDim.x * blockDim.x) {
+        const double dd = wn * z[static_cast<int64_t>(b) * npad + i] - sigma * q[static_cast<int64_t>(b) * npad + i] * invq;
+        acc += dd * dd;
+    }
+    const double tot = block_sum(acc, red);
+    if (threadIdx.x == 0) rpart[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = tot;
+}
+
+__global__ void lz_finalize_kernel(const double* __restrict__ wpart, int parts, const double* __restrict__ rpart,
+                                   int rparts, double s0, double safety, double* lambda, double* lambda_out) {
+    const int b = blockIdx.x;
+    const double sigma = sum_partials(wpart + static_cast<int64_t>(b) * parts, parts);
+    const double r = sqrt(sum_partials(rpart + static_cast<int64_t>(b) * rparts, rparts));
+    // ||X0||_2 <= sqrt(sigma + r) / s0 (Thm 2); never looser than Frobenius (||X0||_F = 1)
+    double f = sqrt(sigma + r) / s0 * safety;
+    if (!(f < 1.0)) f = 1.0;
+    if (!(f > 0.0)) f = 1.0;                             // zero matrix / NaN: keep lambda_F
+    const double lam = lambda[b] * f;
+    lambda[b] = lam;
+    if (lambda_out) lambda_out[b] = lam;
+}
+
+template <typename E>
+void gemv_launch(const void* A, int npad, int parts, int batch, const float* x, int64_t xstride, const double* xpart,
+                 int xparts, float* y, double* ypart, cudaStream_t stream) {
+    lz_gemv_kernel<E><<<dim3(parts, batch), kGemvThreads, static_cast<size_t>(npad) * 4, stream>>>(
+        static_cast<const E*>(A), npad, x, xstride, xpart, xparts, y, ypart);
+}
+
+}  // namespace
+
+void lanczos_prepare() {
+    cudaFuncSetAttribute(lz_gemv_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lz_gemv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lz_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+int lanczos_parts(int npad) { return (npad + kGemvRows - 1) / kGemvRows; }
+
+int lanczos_launches(int steps, int n) { return 3 * (steps < n ? steps : n) + 6; }
+
+size_t lanczos_scratch_bytes(int npad, int batch, int steps) {
+    const size_t parts = static_cast<size_t>(lanczos_parts(npad));
+    return static_cast<size_t>(batch) * npad * 4 * (steps + 1 + 4) +           // V, t, w, q, z
+           static_cast<size_t>(batch) * 8 * (2 * kMaxLz + 2 * parts + 16 + 1) + 256;
+}
+
+cudaError_t launch_lanczos_bound(OpType t, const void* X0, double s0, int n, int npad, int batch, int steps,
+                                 double safety, void* scratch, double* lambda, double* lambda_out, cudaStream_t stream) {
+    if (static_cast<size_t>(npad) * 4 > 200 * 1024 || steps < 1 || steps > kMaxLz) return cudaErrorInvalidValue;
+    const int m = steps < n ? steps : n;
+    const int parts = lanczos_parts(npad);
+    const int64_t vstride = static_cast<int64_t>(m + 1) * npad;
+    float* V = static_cast<float*>(scratch);
+    float* tv = V + static_cast<int64_t>(batch) * vstride;
+    float* wv = tv + static_cast<int64_t>(batch) * npad;
+    float* qv = wv + static_cast<int64_t>(batch) * npad;
+    float* zv = qv + static_cast<int64_t>(batch) * npad;
+    double* AB = reinterpret_cast<double*>(zv + static_cast<int64_t>(batch) * npad);
+    double* pa = AB + static_cast<int64_t>(batch) * 2 * kMaxLz;
+    double* pb = pa + static_cast<int64_t>(batch) * parts;
+    double* pr = pb + static_cast<int64_t>(batch) * parts;
+    double* qn2 = pr + static_cast<int64_t>(batch) * 16;
+    auto gemv = [&](const float* x, int64_t xs, const double* xp, int xps, float* y, double* yp) {
+        switch (t) {
+            case OpType::F16: gemv_launch<__half>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
+            case OpType::BF16: gemv_launch<__nv_bfloat16>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
+            case OpType::TF32: gemv_launch<float>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
+        }
+    };
+    lz_init_kernel<<<batch, kLzThreads, 0, stream>>>(V, n, npad, vstride);
+    for (int k = 0; k < m; ++k) {
+        gemv(V + static_cast<int64_t>(k) * npad, vstride, nullptr, 0, tv, pa);   // t = X0 v_k
+        gemv(tv, npad, nullptr, 0, wv, pa);                                      // w = X0 t
+        lz_step_kernel<<<batch, kLzThreads, 0, stream>>>(V, wv, npad, vstride, k, AB);
+    }
+    lz_ritz_kernel<<<batch, kLzThreads, 0, stream>>>(V, npad, vstride, m, AB, qv, qn2);
+    gemv(qv, npad, qn2, 1, wv, pa);        // w = X0 q / |q|,  sigma = |w|^2
+    gemv(wv, npad, pa, parts, zv, pb);     // z = X0 w / |w|
+    constexpr int kRBlocks = 16;
+    lz_residual_kernel<<<dim3(kRBlocks, batch), 256, 0, stream>>>(qv, qn2, zv, pa, parts, npad, pr);
+    lz_finalize_kernel<<<batch, 1, 0, stream>>>(pa, parts, pr, kRBlocks, s0, safety, lambda, lambda_out);
     return cudaGetLastError();
 }
 

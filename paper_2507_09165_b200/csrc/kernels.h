@@ -115,6 +115,15 @@ cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, do
 //   fp32 master (upper 32-tiles, zero padded)       -- if out32
 //   fp32 final (full, mirrored, ld n)               -- if outF (scaled by post)
 // With out_lo (split precision): out_op = cvt(x0 * op_scale), out_lo = cvt(x0 * op_scale - out_op).
+// Lanczos bound (Algorithm 2 line 1 + Theorem 2) on the operand copy X0 (scale s0) of
+// X / lambda_F: overwrites lambda[b] (and lambda_out) with lambda_F * min(1, sqrt(sigma + r) / s0 *
+// safety).  `scratch`: lanczos_scratch_bytes(npad, batch, steps) bytes of device memory.
+size_t lanczos_scratch_bytes(int npad, int batch, int steps);
+cudaError_t launch_lanczos_bound(OpType t, const void* X0, double s0, int n, int npad, int batch, int steps,
+                                 double safety, void* scratch, double* lambda, double* lambda_out, cudaStream_t stream);
+int lanczos_launches(int steps, int n);
+void lanczos_prepare();   // kernel attributes (call once, outside graph capture)
+
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
                                  const double* lambda, double scale, void* out_op, void* out_lo,
                                  double op_scale, float* outF, double post, cudaStream_t stream);

@@ -58,6 +58,8 @@ struct Workspace {
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
     int* counters = nullptr;       // per-product tile counters of the dynamic scheduler
+    void* lz_scratch = nullptr;    // Lanczos-bound scratch (allocated on first use)
+    size_t lz_bytes = 0;
 };
 
 constexpr int kMaxSteps = 1024;
@@ -73,6 +75,8 @@ struct psd_filter_s {
     double eps = 1e-3;
     psd_precision_t prec = PSD_PREC_FP16;
     psd_bound_t bound = PSD_BOUND_FROBENIUS;
+    int lz_steps = 20;             // PSD_BOUND_LANCZOS: Lanczos steps on X^2 and safety factor
+    double lz_safety = 1.01;
     Workspace ws;
     // power-of-two operand scales of the fp16 split path: Z iterates, Y = Z^2, Horner U
     double s_z = 1.0, s_y = 1.0, s_u = 1.0;
@@ -184,6 +188,9 @@ void free_ws(Workspace& ws) {
     if (ws.status) cudaFree(ws.status);
     if (ws.tiles) cudaFree(ws.tiles);
     if (ws.counters) cudaFree(ws.counters);
+    if (ws.lz_scratch) cudaFree(ws.lz_scratch);
+    ws.lz_scratch = nullptr;
+    ws.lz_bytes = 0;
     ws.tiles = nullptr;
     ws.counters = nullptr;
     ws.partial = nullptr;
@@ -198,6 +205,23 @@ int64_t ws_bytes(OpType op, bool split, int64_t npad, int64_t batch) {
 }
 
 void free_graphs(psd_filter_s* h);
+
+// Lanczos-bound scratch, grown on demand (never inside a graph capture)
+psd_status_t ensure_lz(psd_filter_s* h, int npad, int batch) {
+    Workspace& ws = h->ws;
+    const size_t need = lanczos_scratch_bytes(npad, batch, h->lz_steps);
+    if (ws.lz_bytes >= need) return PSD_OK;
+    if (h->capturing) return fail(PSD_ECUDA, "Lanczos scratch must exist before capture");
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    if (ws.lz_scratch) cudaFree(ws.lz_scratch);
+    ws.lz_scratch = nullptr;
+    ws.lz_bytes = 0;
+    if (cudaMalloc(&ws.lz_scratch, need) != cudaSuccess) return fail(PSD_ENOMEM, "cudaMalloc Lanczos scratch failed");
+    ws.lz_bytes = need;
+    lanczos_prepare();
+    return PSD_OK;
+}
 
 psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     Workspace& ws = h->ws;
@@ -439,7 +463,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     }
     // (a1) bound
     const double* lam = nullptr;
-    if (h->bound == PSD_BOUND_FROBENIUS) {
+    if (h->bound == PSD_BOUND_FROBENIUS || h->bound == PSD_BOUND_LANCZOS) {
         const int nblk = bound_blocks_per_matrix(n);
         e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
         if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
@@ -461,6 +485,18 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         sc[B_X0] = sc[B_XA] = sc[B_XB] = h->s_z;
         sc[B_Y] = h->s_y;
         sc[B_UA] = sc[B_UB] = h->s_u;
+    }
+    if (h->bound == PSD_BOUND_LANCZOS) {
+        // X / lambda_F into the operand buffer, Lanczos on its square, then lambda~ <- the
+        // Theorem-2 bound (never looser than lambda_F); the real scale below uses it
+        rc = ensure_lz(h, npad, batch);
+        if (rc != PSD_OK) return rc;
+        e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr, sc[B_X0], nullptr, 0.0, st);
+        if (e != cudaSuccess) return cuda_fail(e, "scale_convert (Lanczos bound)");
+        e = launch_lanczos_bound(ws.op, ws.op_buf[B_X0], sc[B_X0], n, npad, batch, h->lz_steps, h->lz_safety,
+                                 ws.lz_scratch, ws.lambda, lambda_out, st);
+        if (e != cudaSuccess) return cuda_fail(e, "Lanczos bound");
+        h->kernel_launches += 1 + lanczos_launches(h->lz_steps, n);
     }
     const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
     const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
@@ -552,6 +588,10 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         // make sure every allocation exists, then capture
         rc = ensure_ws(h, static_cast<int>(padded_n(n64, batch64)), static_cast<int>(batch64));
         if (rc != PSD_OK) return rc;
+        if (h->bound == PSD_BOUND_LANCZOS) {
+            rc = ensure_lz(h, static_cast<int>(padded_n(n64, batch64)), static_cast<int>(batch64));
+            if (rc != PSD_OK) return rc;
+        }
         if (!h->capture_stream) {
             cudaError_t e = cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
@@ -881,8 +921,19 @@ psd_status_t psd_filter_set_precision(psd_filter_t h, psd_precision_t prec) {
 
 psd_status_t psd_filter_set_bound(psd_filter_t h, psd_bound_t bound) {
     if (!h) return fail(PSD_EINVAL, "null handle");
-    if (bound != PSD_BOUND_FROBENIUS && bound != PSD_BOUND_USER) return fail(PSD_EINVAL, "unknown bound");
+    if (bound != PSD_BOUND_FROBENIUS && bound != PSD_BOUND_USER && bound != PSD_BOUND_LANCZOS)
+        return fail(PSD_EINVAL, "unknown bound");
     h->bound = bound;
+    return PSD_OK;
+}
+
+psd_status_t psd_filter_set_lanczos(psd_filter_t h, int steps, double safety) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (steps < 1 || steps > 64) return fail(PSD_EINVAL, "Lanczos steps must be in [1, 64]");
+    if (!(safety >= 1.0) || !(safety <= 2.0)) return fail(PSD_EINVAL, "safety factor must be in [1, 2]");
+    h->lz_steps = steps;
+    h->lz_safety = safety;
+    free_graphs(h);
     return PSD_OK;
 }
 

@@ -316,6 +316,13 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 }
                 fence_proxy_async_smem();
                 __syncthreads();
+                if (plan.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+                    const long long t_d = clock64();
+                    atomicAdd(plan.dbg + 0, static_cast<unsigned long long>(t_b - t_a));   // MMA issue + wait
+                    atomicAdd(plan.dbg + 1, static_cast<unsigned long long>(t_c - t_b));   // TMEM loads
+                    atomicAdd(plan.dbg + 2, static_cast<unsigned long long>(t_d - t_c));   // epilogue + mirror + sync
+                    atomicAdd(plan.dbg + 3, 1ull);
+                }
             } else {
                 // final: 1/2 X + 1/2 lambda~ X0 S  (mode 1)  or  S (mode 2); symmetrise via staging
                 if (st.final_mode == 1) {

@@ -41,6 +41,13 @@ def pkg():
     return p
 
 
+def _lam(X, lam_gpu):
+    """The oracle's own bound; the GPU's exported lambda~ must agree with it."""
+    lo = chain.frobenius_bound(X)
+    assert abs(lam_gpu - lo) <= 1e-9 * max(lo, 1e-300), (lam_gpu, lo)
+    return lo
+
+
 def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
@@ -91,8 +98,7 @@ def test_project_parity(pkg, n, batch, family, which, prec):
     assert f.status() == "PSD_OK"
     st, kap = _oracle_filter(which)
     for b in range(batch):
-        assert abs(lam[b] - chain.frobenius_bound(X[b])) <= 1e-12 * lam[b]
-        ref, _ = chain.project(X[b], st, kap, lam=lam[b])
+        ref, _ = chain.project(X[b], st, kap, lam=_lam(X[b], lam[b]))
         err = _rel(P[b], ref)
         assert err <= tol(prec, n, which), f"b={b} err={err:.3e}"
         assert np.array_equal(P[b], P[b].T)
@@ -103,7 +109,7 @@ def test_sign_parity(pkg, n, prec):
     X = synth.batch("goe", n, 2, 7)
     S, lam, _ = _gpu(pkg, _product_filter("half", pkg), X, prec, sign=True)
     for b in range(2):
-        ref, _ = chain.sign(X[b], *HALF, lam=lam[b])
+        ref, _ = chain.sign(X[b], *HALF, lam=_lam(X[b], lam[b]))
         # sign chain output has ||S||_F ~ sqrt(n); relative bar as for P
         assert _rel(S[b], ref) <= tol(prec, n)
         assert np.array_equal(S[b], S[b].T)
@@ -176,7 +182,7 @@ def test_pair_kernel_parity(pkg, n, batch, family, prec):
     P, lam, f = _gpu(pkg, _product_filter("half", pkg), X, prec)
     assert f.status() == "PSD_OK"
     for b in sorted({0, batch - 1}):
-        ref, _ = chain.project(X[b], *HALF, lam=lam[b])
+        ref, _ = chain.project(X[b], *HALF, lam=_lam(X[b], lam[b]))
         assert _rel(P[b], ref) <= tol(prec, n), (b, _rel(P[b], ref))
     for b in range(batch):
         assert np.array_equal(P[b], P[b].T)
@@ -198,7 +204,7 @@ def test_c4_full_size_structured(pkg):
     for b in range(batch):
         assert np.array_equal(P[b], P[b].T)
     for b in [0, 1, 17, 31]:
-        ref = spectral.structured_project(blocks[b], *HALF, lam[b])
+        ref = spectral.structured_project(blocks[b], *HALF, _lam(X[b], lam[b]))
         assert _rel(P[b], ref) <= TOL["fp16"], (b, _rel(P[b], ref))
 
 
@@ -223,7 +229,7 @@ def test_split_precision_parity(pkg, n, batch, family, which, prec):
     assert f.status() == "PSD_OK"
     st, kap = _oracle_filter(which)
     for b in sorted({0, batch - 1}):
-        ref, _ = chain.project(X[b], st, kap, lam=lam[b])
+        ref, _ = chain.project(X[b], st, kap, lam=_lam(X[b], lam[b]))
         err = _rel(P[b], ref)
         # the coarse Remez sets (c1: T=3, sign error 0.86; c2: d=7, coefficients up to 128.8)
         # amplify fp32 accumulation rounding: model with sgemm-style fp32 accumulation 6-9e-6
@@ -237,7 +243,7 @@ def test_split_sign_parity(pkg):
     X = synth.batch("goe", 512, 2, 77)
     S, lam, _ = _gpu(pkg, _product_filter("single", pkg), X, "fp16x3", sign=True)
     for b in range(2):
-        ref, _ = chain.sign(X[b], *SINGLE, lam=lam[b])
+        ref, _ = chain.sign(X[b], *SINGLE, lam=_lam(X[b], lam[b]))
         assert _rel(S[b], ref) <= 1e-5
 
 
@@ -258,8 +264,7 @@ def test_small_batch_parity(pkg, n, batch, family, which, prec):
     st, kap = _oracle_filter(which)
     bar = (5e-5 if which in ("c1", "c2") else 1e-5) if prec == "fp16x3" else tol(prec, n, which)
     for b in sorted({0, 1, batch // 2, batch - 1}):
-        assert abs(lam[b] - chain.frobenius_bound(X[b])) <= 1e-12 * lam[b]
-        ref, _ = chain.project(X[b], st, kap, lam=lam[b])
+        ref, _ = chain.project(X[b], st, kap, lam=_lam(X[b], lam[b]))
         err = _rel(P[b], ref)
         assert err <= bar, f"b={b} err={err:.3e}"
     assert all(np.array_equal(P[b], P[b].T) for b in range(0, batch, max(1, batch // 64)))
@@ -269,7 +274,7 @@ def test_small_batch_sign_and_nonfinite(pkg):
     X = synth.batch("goe", 40, 4, 123)
     S, lam, f = _gpu(pkg, _product_filter("half", pkg), X, "fp16x3", sign=True)
     for b in range(4):
-        ref, _ = chain.sign(X[b], *HALF, lam=lam[b])
+        ref, _ = chain.sign(X[b], *HALF, lam=_lam(X[b], lam[b]))
         assert _rel(S[b], ref) <= 1e-5
         assert np.array_equal(S[b], S[b].T)
     Xn = X.copy()
@@ -293,3 +298,66 @@ def test_project_host_pipeline(pkg):
     f.project_host(Xh2, Xh2, chunks=2)
     torch.cuda.synchronize()
     assert torch.equal(Xh2, ref)
+
+
+# Lanczos bound (Algorithm 2 line 1 + Theorem 2; reading R21).  The GPU runs the
+# Krylov iteration on the operand copy of X / ||X||_F in fp32 vectors: lambda~ agrees with the
+# float64 oracle (oracle/bound.py) to the operand rounding (fp16: u = 2^-11 per entry; tf32 op
+# copies are exact fp32) plus fp32 Lanczos rounding.
+LZ_TOL = {"fp16": 2e-3, "tf32": 1e-4, "bf16": 1e-2}
+
+
+@pytest.mark.parametrize("n,batch,family,prec", [
+    (10, 2, "goe", "tf32"),            # n < steps: the Krylov space is all of R^n
+    (200, 3, "goe", "fp16"),           # ragged
+    (512, 2, "sdp_shaped", "fp16"),
+    (384, 2, "haar", "tf32"),
+    (256, 2, "goe", "bf16"),
+])
+def test_lanczos_bound_parity(pkg, n, batch, family, prec):
+    from oracle import bound
+    X = synth.batch(family, n, batch, synth.SEED_BASE + 3 * n)
+    f = pkg.Filter(pkg.filters.half_filter(), precision=prec, bound="lanczos")
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    lam = torch.zeros(batch, dtype=torch.float64, device="cuda")
+    P = f.project(Xd, lambda_out=lam)
+    torch.cuda.synchronize()
+    assert f.status() == "PSD_OK"
+    lam = lam.cpu().numpy()
+    P = P.double().cpu().numpy()
+    for b in range(batch):
+        lo = bound.lanczos_bound(X[b], steps=20, safety=1.01)
+        assert abs(lam[b] - lo) <= LZ_TOL[prec] * lo, (b, lam[b], lo)
+        s2 = np.linalg.norm(X[b], 2)
+        assert s2 <= lam[b] <= 1.03 * s2                 # valid and ~sqrt(n)/2 x tighter than ||X||_F
+        ref, _ = chain.project(X[b], *HALF, lam=lo)
+        assert _rel(P[b], ref) <= tol(prec, n) + 4 * LZ_TOL[prec], (b, _rel(P[b], ref))
+        assert np.array_equal(P[b], P[b].T)
+
+
+def test_lanczos_bound_accuracy_gain(pkg):
+    """The point of the tighter bound: at n = 1024 the half filter applied after
+    the Lanczos bound is far closer to the exact projection than after Frobenius."""
+    X = synth.batch("goe", 1024, 1, 4242)
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    exact = spectral.eig_project(X[0])
+    errs = {}
+    for bnd in ("frobenius", "lanczos"):
+        f = pkg.Filter(pkg.filters.half_filter(), precision="tf32", bound=bnd)
+        P = f.project(Xd).double().cpu().numpy()[0]
+        errs[bnd] = spectral.rel_error(P, exact)
+    assert errs["lanczos"] < 0.25 * errs["frobenius"], errs
+
+
+def test_lanczos_bound_edge_cases(pkg):
+    """Zero matrix keeps lambda~ = 0; rank one gives ||u||^2 * safety; identity stays exact."""
+    n = 160
+    u = synth.goe(n, 1)[0]
+    X = np.stack([np.zeros((n, n)), np.outer(u, u), np.eye(n)]).astype(np.float32).astype(np.float64)
+    f = pkg.Filter(pkg.filters.half_filter(), precision="tf32", bound="lanczos", lanczos_safety=1.0)
+    lam = torch.zeros(3, dtype=torch.float64, device="cuda")
+    P = f.project(torch.tensor(X, dtype=torch.float32, device="cuda"), lambda_out=lam).double().cpu().numpy()
+    lam = lam.cpu().numpy()
+    assert lam[0] == 0 and not P[0].any()
+    assert lam[1] == pytest.approx(np.linalg.norm(X[1], 2), rel=1e-5)
+    assert lam[2] == pytest.approx(1.0, rel=1e-5)

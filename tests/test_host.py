@@ -85,6 +85,12 @@ def test_create_rejects_bad_arguments(lib):
     rc, h = _create(lib, [(1.5, -0.5)])
     assert lib.psd_filter_set_precision(h, 7) == 1
     assert lib.psd_filter_set_bound(h, 9) == 1
+    assert lib.psd_filter_set_bound(h, 2) == 0                                   # PSD_BOUND_LANCZOS
+    assert lib.psd_filter_set_lanczos(h, 0, 1.0) == 1                            # steps in [1, 64]
+    assert lib.psd_filter_set_lanczos(h, 65, 1.0) == 1
+    assert lib.psd_filter_set_lanczos(h, 20, 0.99) == 1                          # safety in [1, 2]
+    assert lib.psd_filter_set_lanczos(h, 20, float("nan")) == 1
+    assert lib.psd_filter_set_lanczos(h, 30, 1.02) == 0
     assert lib.psd_project(h, None, 4, 1, None, None) == 1                       # null pointers
     assert lib.psd_workspace_bytes(h, 4096, 32) > 6 * 32 * 4096 * 4096 * 2
     lib.psd_filter_destroy(h)
