@@ -256,6 +256,7 @@ template <typename E>
 __device__ __forceinline__ float elem_to_float(E v);
 template <> __device__ __forceinline__ float elem_to_float<__half>(__half v) { return __half2float(v); }
 template <> __device__ __forceinline__ float elem_to_float<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <> __device__ __forceinline__ float elem_to_float<float>(float v) { return v; }
 
 __device__ __forceinline__ double sum_partials(const double* p, int count) {
     double s = 0.0;
@@ -300,18 +301,27 @@ lz_gemv_kernel(const E* __restrict__ A, int npad, const float* __restrict__ x, i
         if (i >= npad) break;
         const E* row = A + (static_cast<int64_t>(b) * npad + i) * npad;
         float s = 0.0f;
-        for (int j = lane * 8; j < npad; j += 32 * 8) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(row + j);
-            if constexpr (sizeof(E) == 2) {
-                const E* e8 = reinterpret_cast<const E*>(&raw);
+        constexpr int kEl = 16 / sizeof(E);             // elements per 16-byte load
+        constexpr int kU = 4;                           // independent loads in flight per lane
+        for (int j0 = lane * kEl; j0 < npad; j0 += 32 * kEl * kU) {
+            uint4 raw[kU];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) s += elem_to_float<E>(e8[k]) * xs[j + k];
-            } else {
-                const float* f4 = reinterpret_cast<const float*>(&raw);
-                const uint4 raw2 = *reinterpret_cast<const uint4*>(row + j + 4);
-                const float* g4 = reinterpret_cast<const float*>(&raw2);
+            for (int u = 0; u < kU; ++u) {
+                const int j = j0 + u * 32 * kEl;
+                raw[u] = j < npad ? __ldcs(reinterpret_cast<const uint4*>(row + j)) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s += f4[k] * xs[j + k] + g4[k] * xs[j + 4 + k];
+            for (int u = 0; u < kU; ++u) {
+                const int j = j0 + u * 32 * kEl;
+                if (j < npad) {
+                    const E* e = reinterpret_cast<const E*>(&raw[u]);
+#pragma unroll
+                    for (int k = 0; k < kEl; k += 4) {
+                        const float4 xv = *reinterpret_cast<const float4*>(xs + j + k);   // 16 B smem reads
+                        s += elem_to_float<E>(e[k]) * xv.x + elem_to_float<E>(e[k + 1]) * xv.y +
+                             elem_to_float<E>(e[k + 2]) * xv.z + elem_to_float<E>(e[k + 3]) * xv.w;
+                    }
+                }
             }
         }
 #pragma unroll
