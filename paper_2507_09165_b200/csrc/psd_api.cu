@@ -549,11 +549,29 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.strideF = static_cast<int64_t>(n) * n;
             ep.nF = n;
         }
-        e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-                ? launch_sym_gemm_2cta(ws.op, split, maps(s.A, s.B), shape, ep, st)
-                : launch_sym_gemm(ws.op, split, maps(s.A, s.B), shape, ep, st);
+        const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+        const bool dbg = pair && !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        if (dbg) {
+            ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial + batch * 128);
+            cudaMemsetAsync(ep.dbg, 0, 128, st);
+            cudaMemsetAsync(ep.dbg + 8, 0xFF, 8, st);
+            cudaMemsetAsync(ep.dbg + 11, 0xFF, 8, st);
+        }
+        e = pair ? launch_sym_gemm_2cta(ws.op, split, maps(s.A, s.B), shape, ep, st)
+                 : launch_sym_gemm(ws.op, split, maps(s.A, s.B), shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
+        if (dbg) {           // debug only: per-product phase counters of the pair kernel
+            unsigned long long t[13] = {};
+            cudaStreamSynchronize(st);
+            cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);
+            const double tiles = t[4] ? double(t[4]) : 1.0;
+            std::fprintf(stderr, "psd step %zu (D %d, out %s): loop %.0f = tile %.0f + acc %.0f + operand %.0f + issue; "
+                         "epilogue acc-wait %.0f work %.0f cycles/tile; %llu clusters (tiles %llu..%llu), starts "
+                         "spread %.1f us, last end %.1f us after first start\n", si, s.D, s.outF ? "fp32" : "op",
+                         t[3] / tiles, t[0] / tiles, t[1] / tiles, t[2] / tiles, t[5] / (2 * tiles), t[6] / (2 * tiles),
+                         t[7], t[11], t[12], (t[9] - t[8]) * 1e-3, (t[10] - t[8]) * 1e-3);
+        }
     }
     if (evp.first) {
         cudaEventRecord(evp.second, st);
@@ -1151,12 +1169,20 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     m.b = bmaps[B_XB];
     m.a_lo = ws.tmap[split ? B_XA + B_COUNT : B_XA];
     m.b_lo = bmaps[split ? B_XB + B_COUNT : B_XB];
-    e = (npad % 256 == 0 && use_pair_kernel(n, batch))
-            ? launch_sym_gemm_2cta(ws.op, split, m, shape, ep, st)
-            : launch_sym_gemm(ws.op, split, m, shape, ep, st);
+    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+    if (ep.dbg && pair) cudaMemsetAsync(ep.dbg, 0, 64, st);
+    e = pair ? launch_sym_gemm_2cta(ws.op, split, m, shape, ep, st) : launch_sym_gemm(ws.op, split, m, shape, ep, st);
     if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
     h->kernel_launches += 3;
-    if (ep.dbg) {            // debug: print the kernel phase stamps (ns since the first)
+    if (ep.dbg && pair) {    // debug: summed over the leader MMA threads / epilogue warp 4 of every CTA
+        unsigned long long t[7] = {};
+        cudaStreamSynchronize(st);
+        cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);
+        const double tiles = t[4] ? double(t[4]) : 1.0;
+        std::fprintf(stderr, "psd pair stamps n=%d (cycles per tile, %llu tiles): mma-loop %.0f = tile-id wait %.0f + "
+                     "accumulator wait %.0f + operand wait %.0f + issue; epilogue: acc wait %.0f, work %.0f\n",
+                     n, t[4], t[3] / tiles, t[0] / tiles, t[1] / tiles, t[2] / tiles, t[5] / (2 * tiles), t[6] / (2 * tiles));
+    } else if (ep.dbg) {            // debug: print the kernel phase stamps (ns since the first)
         unsigned long long t[6] = {};
         cudaStreamSynchronize(st);
         cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);

@@ -169,17 +169,32 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             int st = 0;
             uint32_t ph = 0;
             int it = 0;
+            // debug phase counters (e.dbg): cycles waiting for a tile id, a free accumulator,
+            // operand stages; total cycles in the loop
+            unsigned long long w_tile = 0, w_tmem = 0, w_full = 0;
+            const unsigned long long t_start = clock64();
+            unsigned long long g_start = 0;
+            if (e.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
             for (;; ++it) {
+                unsigned long long c0 = e.dbg ? clock64() : 0;
                 const int t = next_tile(it);
                 release_tile(it);
+                if (e.dbg) { const unsigned long long c1 = clock64(); w_tile += c1 - c0; c0 = c1; }
                 if (t >= total_tiles) break;
                 const int acc = it & 1;
                 const uint32_t acc_ph = (it >> 1) & 1;
                 ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
+                if (e.dbg) { const unsigned long long c1 = clock64(); w_tmem += c1 - c0; }
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kT2;
                 for (int kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait(&full[st], ph);
+                    if (e.dbg) {
+                        const unsigned long long c2 = clock64();
+                        ptx::mbar_wait(&full[st], ph);
+                        w_full += clock64() - c2;
+                    } else {
+                        ptx::mbar_wait(&full[st], ph);
+                    }
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
                     const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
@@ -206,6 +221,21 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
             }
+            if (e.dbg) {
+                atomicAdd(e.dbg + 0, w_tile);
+                atomicAdd(e.dbg + 1, w_tmem);
+                atomicAdd(e.dbg + 2, w_full);
+                atomicAdd(e.dbg + 3, clock64() - t_start);
+                atomicAdd(e.dbg + 4, static_cast<unsigned long long>(it));
+                unsigned long long g_end;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+                atomicAdd(e.dbg + 7, 1ull);                                   // clusters
+                atomicMin(e.dbg + 8, g_start);                                // first start
+                atomicMax(e.dbg + 9, g_start);                                // last start
+                atomicMax(e.dbg + 10, g_end);                                 // last end
+                atomicMin(e.dbg + 11, static_cast<unsigned long long>(it));   // fewest tiles
+                atomicMax(e.dbg + 12, static_cast<unsigned long long>(it));   // most tiles
+            }
             // drain: the last accumulators must be read out before the pair tears down
             for (int last = it - 2; last < it; ++last)
                 if (last >= 0) ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
@@ -226,7 +256,9 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             int b, I, J;
             decode_tile(t, s, b, I, J);
             const int acc = it & 1;
+            const unsigned long long e0 = (e.dbg && q == 0 && ptx::elect_one()) ? clock64() : 0;
             ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
+            const unsigned long long e1 = e0 ? clock64() : 0;
             ptx::tc_fence_after();
             const int gi0 = I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32;
             const bool diag = (I == J);
@@ -247,6 +279,10 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive_remote(acc ? tmem_empty_leader1 : tmem_empty_leader0);
+            if (e0) {
+                atomicAdd(e.dbg + 5, e1 - e0);                 // epilogue warp 4 waiting for an accumulator
+                atomicAdd(e.dbg + 6, clock64() - e1);          // its epilogue work per tile
+            }
         }
     }
 
