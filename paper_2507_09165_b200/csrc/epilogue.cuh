@@ -91,7 +91,9 @@ __device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int np
     }
 }
 
-template <OpType T>
+// kCg: load through L2 only (ld.global.cg) -- the persistent chain kernel rewrites the addend
+// buffers between its products, so a line this SM cached in L1 earlier may be stale.
+template <OpType T, bool kCg = false>
 __device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int npad, int gi, int gj0, float beta,
                                            float (&v)[32]) {
     using Tr = OpTraits<T>;
@@ -101,7 +103,7 @@ __device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int np
         const uint4* d4 = reinterpret_cast<const uint4*>(drow);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint4 d = d4[q];
+            const uint4 d = kCg ? __ldcg(d4 + q) : d4[q];
             const uint32_t w[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -115,7 +117,7 @@ __device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int np
         const float4* d4 = reinterpret_cast<const float4*>(drow);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const float4 d = d4[q];
+            const float4 d = kCg ? __ldcg(d4 + q) : d4[q];
             v[4 * q] += beta * d.x;
             v[4 * q + 1] += beta * d.y;
             v[4 * q + 2] += beta * d.z;
@@ -124,10 +126,34 @@ __device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int np
     }
 }
 
+// Addend words of one chunk fetched ahead of time (the chain kernel loads them while the MMAs
+// run): the 16-byte row segments of the primary addend, Dop (4 words for 16-bit operands, 8 for
+// tf32) or the fp32 X (8 words).  Returns false (nothing loaded) where the masked path is needed.
 template <OpType T>
+__device__ __forceinline__ bool prefetch_addend(const EpiParams& e, int b, int npad, int gi, int gj0, uint4 (&pre)[8]) {
+    using Tr = OpTraits<T>;
+    if (e.Dop) {
+        const uint4* d4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(e.Dop) +
+                                                         (static_cast<int64_t>(b) * npad * npad +
+                                                          static_cast<int64_t>(gi) * npad + gj0) * Tr::kBytes);
+#pragma unroll
+        for (int q = 0; q < 2 * Tr::kBytes; ++q) pre[q] = __ldcg(d4 + q);
+        return true;
+    }
+    if (e.Df && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
+        const uint4* d4 = reinterpret_cast<const uint4*>(e.Df + static_cast<int64_t>(b) * e.strideDf +
+                                                         static_cast<int64_t>(gi) * e.ldDf + gj0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pre[q] = __ldcs(d4 + q);
+        return true;
+    }
+    return false;
+}
+
+template <OpType T, bool kCg = false>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
                                                bool /*tile_diag*/, const uint32_t (&raw)[32], uint8_t* wsmem,
-                                               int64_t packed_off = -1) {
+                                               int64_t packed_off = -1, const uint4* pre = nullptr) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     const int lane = threadIdx.x & 31;
@@ -140,11 +166,41 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
 
     // addends: full 32-element row segments (the values left of the diagonal are discarded
     // by the symmetrisation of a diagonal block)
-    if (e.Dop) {
-        add_op_row<T>(e.Dop, opBase, npad, gi, gj0, e.beta, v);
-        if (e.Dop_lo) add_op_row<T>(e.Dop_lo, opBase, npad, gi, gj0, e.beta, v);
-    }
-    if (e.Df) {                                      // fp32 addend (the input X), masked to nDf
+    if (pre && e.Dop) {                              // prefetched primary addend
+        if constexpr (Tr::kBytes == 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t w[4] = {pre[q].x, pre[q].y, pre[q].z, pre[q].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    float lo, hi;
+                    Tr::unpack2(w[h], lo, hi);
+                    v[q * 8 + 2 * h] += e.beta * lo;
+                    v[q * 8 + 2 * h + 1] += e.beta * hi;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[4 * q] += e.beta * __uint_as_float(pre[q].x);
+                v[4 * q + 1] += e.beta * __uint_as_float(pre[q].y);
+                v[4 * q + 2] += e.beta * __uint_as_float(pre[q].z);
+                v[4 * q + 3] += e.beta * __uint_as_float(pre[q].w);
+            }
+        }
+        if (e.Dop_lo) add_op_row<T, kCg>(e.Dop_lo, opBase, npad, gi, gj0, e.beta, v);
+    } else if (pre && e.Df) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[4 * q] += e.beta * __uint_as_float(pre[q].x);
+            v[4 * q + 1] += e.beta * __uint_as_float(pre[q].y);
+            v[4 * q + 2] += e.beta * __uint_as_float(pre[q].z);
+            v[4 * q + 3] += e.beta * __uint_as_float(pre[q].w);
+        }
+    } else if (e.Dop) {
+        add_op_row<T, kCg>(e.Dop, opBase, npad, gi, gj0, e.beta, v);
+        if (e.Dop_lo) add_op_row<T, kCg>(e.Dop_lo, opBase, npad, gi, gj0, e.beta, v);
+    } else if (e.Df) {                               // fp32 addend (the input X), masked to nDf
         const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
         if (gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
             const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);

@@ -75,6 +75,29 @@ cudaError_t launch_sym_gemm_2cta(OpType t, bool split, const OperandMaps& m, con
 bool use_pair_kernel(int64_t n, int64_t batch);
 int64_t padded_n(int64_t n, int64_t batch);
 
+// Persistent chain kernel (chain.cu): every product of one projection in ONE launch for the
+// few-tile regime (n < 1024 or few 256-tiles).  A cluster of CS CTAs owns a 128 x 128 upper tile,
+// CTA r computing its columns [r*BN, (r+1)*BN), BN = 128 / CS, with the A row panel split in CS
+// slices multicast to the whole cluster (each CTA reads 1/CS of A from L2); a grid barrier
+// separates consecutive products.
+constexpr int kChainMaxSteps = 48;
+constexpr int kChainMaps = 12;            // [0, 6): high parts of the operand buffers, [6, 12): low parts
+struct ChainStep {
+    int a, b;                 // operand buffer ids (map index; + 6 for the low part)
+    EpiParams ep;
+};
+struct ChainParams {
+    CUtensorMap map[kChainMaps];    // box rows 128 / CS = BN: the multicast A slices and the B rows
+    int npad, batch, nsteps;
+    unsigned* barrier;              // zeroed grid-barrier counter
+    unsigned long long* dbg;        // debug: %globaltimer phase stamps of CTA 0 [step][8] (NULL in production)
+    int flags;                      // debug bits (PSD_CHAIN_FLAGS): 1 = no addend prefetch, 2 = no tensormap prefetch
+    ChainStep steps[kChainMaxSteps];
+};
+// Cluster size for (npad, batch): 4 or 2, or 0 when the chain kernel cannot run it.
+int chain_cluster_size(OpType t, bool split, int npad, int batch);
+cudaError_t launch_chain(OpType t, bool split, int cs, const ChainParams& p, cudaStream_t stream);
+
 // Batched small-n path (n <= 64), the whole chain in one kernel (small_batch.cu).
 struct SmallStep {
     int slot_a, slot_b;       // byte offsets of the operand slots within a matrix's smem region

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <dlfcn.h>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -53,7 +54,8 @@ struct Workspace {
     double* lambda = nullptr;
     unsigned* status = nullptr;
     CUtensorMap tmap[2 * B_COUNT];
-    CUtensorMap tmap64[2 * B_COUNT];        // 64-row boxes: B operand of the 128 x 64 tiles
+    CUtensorMap tmap64[2 * B_COUNT];        // 64-row boxes: B operand of the 128 x 64 tiles, chain kernel CS = 2
+    CUtensorMap tmap32[2 * B_COUNT];        // 32-row boxes: chain kernel CS = 4
     int nblk = 0;
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
@@ -106,6 +108,9 @@ struct psd_filter_s {
     std::vector<GraphEntry> graphs;
     uint64_t graph_clock = 0;
     bool use_graphs = std::getenv("PSD_NO_GRAPH") == nullptr;
+    // persistent chain kernel (few-tile regime): opt-in (PSD_CHAIN=1) -- measured no faster than
+    // one launch per product at c3 (grid barrier + pipeline refill per product)
+    bool use_chain = std::getenv("PSD_CHAIN") != nullptr && std::getenv("PSD_NO_CHAIN") == nullptr;
     cudaStream_t capture_stream = nullptr;
     bool capturing = false;
     // pipelined host-buffer projection (psd_project_host)
@@ -121,6 +126,7 @@ struct psd_filter_s {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
     int64_t product_launches_profiled = 0;
     int64_t kernel_launches = 0;
+    int64_t last_products = 0;     // product-carrying launches of the last run_body (graph accounting)
 };
 
 namespace {
@@ -253,7 +259,8 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
         if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch) ||
-            !make_operand_tmap(&ws.tmap64[i], ws.op_buf[i], op, npad, batch, 64)) {
+            !make_operand_tmap(&ws.tmap64[i], ws.op_buf[i], op, npad, batch, 64) ||
+            !make_operand_tmap(&ws.tmap32[i], ws.op_buf[i], op, npad, batch, 32)) {
             free_ws(ws);
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
         }
@@ -439,11 +446,12 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             evs = {take_event(h), take_event(h)};
             cudaEventRecord(evs.first, st);
         }
-        const bool dbg = std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        const bool dbg = !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
             sp_plan.dbg = reinterpret_cast<unsigned long long*>(ws.partial);
             cudaMemsetAsync(ws.partial, 0, 64, st);
         }
+        h->last_products = 1;
         e = launch_small_batch(sp, X, out, n, batch, lambda_out, ws.status, sp_plan, st);
         if (e != cudaSuccess) return cuda_fail(e, "small_batch");
         if (dbg) {
@@ -524,9 +532,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
     }
-    for (size_t si = 0; si < steps.size(); ++si) {
-        const Step& s = steps[si];
-        shape.counter = ws.counters + si;
+    auto make_ep = [&](const Step& s) {
         EpiParams ep{};
         ep.alpha = static_cast<float>(s.alpha / (sc[s.A] * sc[s.B]));
         ep.alpha_dev = s.alpha_lambda ? lam : nullptr;
@@ -549,7 +555,68 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.strideF = static_cast<int64_t>(n) * n;
             ep.nF = n;
         }
-        const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+        return ep;
+    };
+    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+    const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
+                             ? chain_cluster_size(ws.op, split, npad, batch)
+                             : 0;
+    if (chain_cs) {
+        // (a3-a6) every product in one persistent launch (chain.cu)
+        std::unique_ptr<ChainParams> cp(new ChainParams());
+        const CUtensorMap* src = chain_cs == 4 ? ws.tmap32 : ws.tmap64;
+        for (int i = 0; i < B_COUNT; ++i) {
+            cp->map[i] = src[i];
+            cp->map[i + kChainMaps / 2] = src[split ? i + B_COUNT : i];
+        }
+        cp->npad = npad;
+        cp->batch = batch;
+        cp->nsteps = static_cast<int>(steps.size());
+        cp->flags = std::getenv("PSD_CHAIN_FLAGS") ? std::atoi(std::getenv("PSD_CHAIN_FLAGS")) : 0;
+        cp->barrier = reinterpret_cast<unsigned*>(ws.counters + (kMaxSteps - 1));
+        for (size_t si = 0; si < steps.size(); ++si) {
+            cp->steps[si].a = steps[si].A;
+            cp->steps[si].b = steps[si].B;
+            cp->steps[si].ep = make_ep(steps[si]);
+        }
+        e = cudaMemsetAsync(cp->barrier, 0, sizeof(unsigned), st);
+        if (e != cudaSuccess) return cuda_fail(e, "chain barrier reset");
+        const bool dbg = !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        unsigned long long* dbg_buf = nullptr;
+        if (dbg && cudaMalloc(&dbg_buf, kChainMaxSteps * 8 * 8) == cudaSuccess) {
+            cudaMemsetAsync(dbg_buf, 0, kChainMaxSteps * 8 * 8, st);
+            cp->dbg = dbg_buf;
+        }
+        h->last_products = 1;
+        e = launch_chain(ws.op, split, chain_cs, *cp, st);
+        if (e != cudaSuccess) return cuda_fail(e, "chain kernel");
+        if (dbg_buf) {       // debug only: per-step phase stamps of CTA 0 (us since the step start)
+            std::vector<unsigned long long> t(kChainMaxSteps * 8);
+            cudaStreamSynchronize(st);
+            cudaMemcpy(t.data(), dbg_buf, t.size() * 8, cudaMemcpyDeviceToHost);
+            cudaFree(dbg_buf);
+            for (size_t si = 0; si < steps.size(); ++si) {
+                const unsigned long long* q = &t[si * 8];
+                auto d = [&](int k) { return q[k] ? (double(q[k]) - double(q[0])) * 1e-3 : -1.0; };
+                const double nxt = si + 1 < steps.size() ? (double(t[(si + 1) * 8]) - double(q[0])) * 1e-3 : -1.0;
+                std::fprintf(stderr, "chain step %2zu (cs %d): first TMA %.2f, first full %.2f, last MMA %.2f, acc ready %.2f, "
+                             "epilogue done %.2f, barrier arrive %.2f, next step %.2f us\n", si, chain_cs, d(1), d(2), d(3), d(4),
+                             d(5), d(6), nxt);
+            }
+        }
+        h->kernel_launches += 1;
+        if (evp.first) {
+            cudaEventRecord(evp.second, st);
+            h->ev_pairs.push_back(evp);
+            h->product_launches_profiled += 1;      // one launch carries every product
+        }
+        return PSD_OK;
+    }
+    h->last_products = static_cast<int64_t>(steps.size());
+    for (size_t si = 0; si < steps.size(); ++si) {
+        const Step& s = steps[si];
+        shape.counter = ws.counters + si;
+        EpiParams ep = make_ep(s);
         const bool dbg = pair && !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
             ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial + batch * 128);
@@ -610,6 +677,11 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             rc = ensure_lz(h, static_cast<int>(padded_n(n64, batch64)), static_cast<int>(batch64));
             if (rc != PSD_OK) return rc;
         }
+        {   // kernel attributes / occupancy queries of the chain kernel happen outside the capture
+            const int npad = static_cast<int>(padded_n(n64, batch64));
+            if (n64 > 64 && !(npad % 256 == 0 && use_pair_kernel(n64, batch64)))
+                chain_cluster_size(op_of(h->prec), split_of(h->prec), npad, static_cast<int>(batch64));
+        }
         if (!h->capture_stream) {
             cudaError_t e = cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
@@ -641,12 +713,7 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         psd_filter_s::GraphEntry g{X, out, lambda_in, lambda_out, n64, batch64, static_cast<int>(want_sign), static_cast<int>(key_prec),
                      static_cast<int>(key_bound), exec, h->kernel_launches - k0, 0, 0};
         // the product count of the sequence (for profiling) = its number of product kernels
-        std::vector<Step> steps_probe;
-        {
-            double so = 0.0;
-            steps_probe = build_plan(h, want_sign, &so);
-        }
-        g.products = (n64 <= 64) ? 1 : static_cast<int64_t>(steps_probe.size());
+        g.products = h->last_products;
         h->kernel_launches = k0;
         h->product_launches_profiled = p0;
         h->graphs.push_back(g);

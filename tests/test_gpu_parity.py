@@ -367,3 +367,47 @@ def test_lanczos_bound_edge_cases(pkg):
     assert lam[0] == 0 and not P[0].any()
     assert lam[1] == pytest.approx(np.linalg.norm(X[1], 2), rel=1e-5)
     assert abs(lam[2] - 1.0) <= 2.0 ** -11
+
+
+def _with_env(var, value, fn):
+    import os
+    old = os.environ.get(var)
+    if value is None:
+        os.environ.pop(var, None)
+    else:
+        os.environ[var] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            os.environ.pop(var, None)
+        else:
+            os.environ[var] = old
+
+
+@pytest.mark.parametrize("n,batch,which,prec,cs", [
+    (1024, 1, "c3", "fp16", None),            # config c3: the chain kernel's one-wave case
+    (1024, 1, "c3", "fp16", "2"),             # same with 2-CTA clusters (64-column CTAs)
+    (384, 24, "half", "fp16", None),          # 144 tiles: several tiles per cluster (double-buffered TMEM)
+    (640, 3, "single", "tf32", None),         # tf32 operands, ragged tile count
+])
+def test_chain_kernel_parity(pkg, n, batch, which, prec, cs):
+    """Persistent chain kernel (every product in one launch, grid barrier between products,
+    multicast A slices; opt-in, PSD_CHAIN=1) vs the oracle, and vs the per-product launches of the
+    same plan."""
+    X = synth.batch("goe", n, batch, synth.SEED_BASE + 13 * n)
+    run = lambda: _with_env("PSD_CHAIN", "1", lambda: _gpu(pkg, _product_filter(which, pkg), X, prec))
+    P, lam, f = _with_env("PSD_CHAIN_CS", cs, run)
+    assert f.status() == "PSD_OK"
+    st, kap = _oracle_filter(which)
+    bar = TOL_X3.get(prec) or tol(prec, n, which)
+    for b in sorted({0, batch // 2, batch - 1}):
+        ref, _ = chain.project(X[b], st, kap, lam=_lam(X[b], lam[b]))
+        assert _rel(P[b], ref) <= bar, (b, _rel(P[b], ref))
+    for b in range(batch):
+        assert np.array_equal(P[b], P[b].T)
+    # the same plan as one launch per product (the default): same operands, same K order per element
+    P2, lam2, _ = _gpu(pkg, _product_filter(which, pkg), X, prec)
+    assert np.array_equal(lam, lam2)
+    for b in range(batch):
+        assert _rel(P[b], P2[b]) <= 1e-6, (b, _rel(P[b], P2[b]))
