@@ -146,6 +146,25 @@ psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t b
                             float* out, const double* lambda_in, double* lambda_out,
                             int want_sign, void* stream);
 
+/* One fused S- and X-update of the three-step ADMM for the SDP pair of Eq. (exp:sdp)
+ * (Eq. exp:admm-three-step), for diagonal constraint operators (max-cut:
+ * A_i = e_i e_i^T, so A* y = Diag(y)):
+ *     M      = C - Diag(y) - X_k / sigma          formed on the fly by the bound and scale kernels
+ *     S_out  = P(M)                               the composite-filter projection (psd_project of M)
+ *     X_out  = X_k + sigma (S_out + Diag(y) - C)  = sigma (S_out - M), fused into the
+ *                                                 reconstruction epilogue (one extra fp32 store)
+ * M is formed in fp32 with one rounding per operation, (C - X_k * fl(1/sigma)) - y_i on the
+ * diagonal (reading R22); S_out is what psd_project returns for that M.
+ *   C, Xk : device, batch x n x n fp32 (upper triangles read), 16-byte aligned.
+ *   y     : device, batch x n fp32 (the diagonal of A* y per matrix), or NULL (y = 0).
+ *   sigma : ADMM penalty, finite and > 0.
+ *   S_out, X_out : device, batch x n x n fp32, fully written, exactly symmetric.  S_out == C and
+ *           X_out == Xk (in place) are allowed; S_out == X_out is not (PSD_EINVAL).
+ * Not with bound USER (PSD_EUNSUPPORTED).  Stream-ordered; not graph-cached (sigma and the extra
+ * pointers are kernel arguments).  Errors as psd_project. */
+psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, const float* y, double sigma,
+                             int64_t n, int64_t batch, float* S_out, float* X_out, void* stream);
+
 /* Synchronises `stream`, then returns and clears the handle's device status word:
  * PSD_OK or PSD_ENONFINITE (some input had a non-finite entry). */
 psd_status_t psd_status(psd_filter_t h, void* stream);

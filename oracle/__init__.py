@@ -19,6 +19,8 @@ chain     -- Algorithm 2: bound, rescale, T stages, reconstruction.
 certify   -- e_float certificate over every float32 in [-1,1],
              C kernel ``certify.c`` (plain loops, OpenMP).
 remez     -- Algorithm 1 sequential Remez + App. A.
+admm      -- the SDP consumer: three-step ADMM with the filter as Pi; the
+             fused S/X update of psd_admm_update and the full iteration for the pins.
 spectral  -- Higham closed form via numpy eigh, spectral operator
              (P:L381-399), Hadamard-conjugated structured oracle for large n.
 

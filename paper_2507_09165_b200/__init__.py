@@ -115,6 +115,31 @@ class Filter:
         """S = X_T = f_T o ... o f_1 (X / lambda~)."""
         return self._run(X, out, lambda_in, lambda_out, True, stream)
 
+    def admm_update(self, C, Xk, y, sigma, S_out=None, X_out=None, stream=None):
+        """One fused ADMM S/X update (Eq. exp:admm-three-step) for diagonal
+        constraints (A* y = Diag(y)): S = P(C - Diag(y) - Xk / sigma) by this filter and
+        X_next = Xk + sigma (S + Diag(y) - C).  ``y``: (batch, n) or (n,) float32 CUDA tensor or
+        None.  Returns (S_out, X_out); X_out may be Xk (in place)."""
+        import torch
+        Cb, Kb = _check_matrix(C), _check_matrix(Xk)
+        if Kb.shape != Cb.shape:
+            raise ValueError("Xk shape mismatch")
+        B, n = Cb.shape[0], Cb.shape[-1]
+        if y is not None:
+            if not (isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float32 and y.is_contiguous()
+                    and y.numel() == B * n):
+                raise ValueError("y must be a contiguous float32 CUDA tensor of batch * n elements")
+        S_out = torch.empty_like(C) if S_out is None else S_out
+        X_out = torch.empty_like(Xk) if X_out is None else X_out
+        Sb, Ob = _check_matrix(S_out), _check_matrix(X_out)
+        if Sb.shape != Cb.shape or Ob.shape != Cb.shape:
+            raise ValueError("output shape mismatch")
+        check(self._lib.psd_admm_update(self._h, ctypes.c_void_p(Cb.data_ptr()), ctypes.c_void_p(Kb.data_ptr()),
+                                        ctypes.c_void_p(y.data_ptr()) if y is not None else None, float(sigma), n, B,
+                                        ctypes.c_void_p(Sb.data_ptr()), ctypes.c_void_p(Ob.data_ptr()),
+                                        _stream_ptr(stream)), "psd_admm_update")
+        return S_out, X_out
+
     def status(self, stream=None):
         """Synchronise and return 'PSD_OK' or 'PSD_ENONFINITE' (device numeric status)."""
         from ._lib import STATUS_NAMES

@@ -23,17 +23,31 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// ADMM input formation (psd_admm_update): m = (x - xk * inv_sigma) - [i == j] y_i, fp32 with one
+// rounding per operation (no contraction), the same wherever the input is read (R22).
+__device__ __forceinline__ float form_m(float x, float xk, float inv_sigma) {
+    return __fsub_rn(x, __fmul_rn(xk, inv_sigma));
+}
+
 __global__ void __launch_bounds__(kBoundThreads)
-frobenius_partials_kernel(const float* __restrict__ X, int n, int nblk, double* __restrict__ partial) {
+frobenius_partials_kernel(const float* __restrict__ X, int n, int nblk, double* __restrict__ partial,
+                          const InputForm form) {
     const int b = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float* Xb = X + static_cast<int64_t>(b) * n * n;
+    const float* Kb = form.Xk ? form.Xk + static_cast<int64_t>(b) * n * n : nullptr;
     double acc = 0.0;
     // rows i == blockIdx.x (mod nblk), one warp per row, upper part j >= i
     for (int i = blockIdx.x + nblk * warp; i < n; i += nblk * (kBoundThreads / 32)) {
         const float* row = Xb + static_cast<int64_t>(i) * n;
+        const float yi = (Kb && form.y) ? form.y[static_cast<int64_t>(b) * n + i] : 0.0f;
         for (int j = i + lane; j < n; j += 32) {
-            const double x = row[j];
+            float m = row[j];
+            if (Kb) {
+                m = form_m(m, Kb[static_cast<int64_t>(i) * n + j], form.inv_sigma);
+                if (j == i) m = __fsub_rn(m, yi);
+            }
+            const double x = m;
             acc += (j == i ? 1.0 : 2.0) * x * x;
         }
     }
@@ -106,7 +120,7 @@ template <OpType T>
 __global__ void __launch_bounds__(256)
 scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double* __restrict__ lambda,
                      double scale, typename Cvt<T>::type* __restrict__ out_op, typename Cvt<T>::type* __restrict__ out_lo,
-                     float op_scale, float* __restrict__ outF, double post) {
+                     float op_scale, float* __restrict__ outF, double post, const InputForm form) {
     using op_t = typename Cvt<T>::type;
     __shared__ float S[kST][kST + 1];
     const int b = blockIdx.y;
@@ -122,13 +136,30 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
         inv = (lam > 0.0) ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);   // NaN stays NaN; 0 -> zeros
     }
     const int r0 = I * kST, c0 = J * kST;
+    const float* Kb = form.Xk ? form.Xk + static_cast<int64_t>(b) * n * n : nullptr;
+    const float* yb = (form.Xk && form.y) ? form.y + static_cast<int64_t>(b) * n : nullptr;
     if ((n & 3) == 0 && r0 + kST <= n && c0 + kST <= n) {
         // 64 rows x 16 float4; 4 per thread, coalesced
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int idx = tid + 256 * k;
             const int r = idx >> 4, q = idx & 15;
-            const float4 x = __ldcs(reinterpret_cast<const float4*>(Xb + static_cast<int64_t>(r0 + r) * n + c0) + q);
+            float4 x = __ldcs(reinterpret_cast<const float4*>(Xb + static_cast<int64_t>(r0 + r) * n + c0) + q);
+            if (Kb) {        // ADMM: M = C - Xk / sigma - Diag(y)
+                const float4 k4 = __ldcs(reinterpret_cast<const float4*>(Kb + static_cast<int64_t>(r0 + r) * n + c0) + q);
+                x.x = form_m(x.x, k4.x, form.inv_sigma);
+                x.y = form_m(x.y, k4.y, form.inv_sigma);
+                x.z = form_m(x.z, k4.z, form.inv_sigma);
+                x.w = form_m(x.w, k4.w, form.inv_sigma);
+                if (yb && r0 == c0) {
+                    const int d = r - 4 * q;           // which component sits on the diagonal
+                    const float yv = yb[r0 + r];
+                    if (d == 0) x.x = __fsub_rn(x.x, yv);
+                    if (d == 1) x.y = __fsub_rn(x.y, yv);
+                    if (d == 2) x.z = __fsub_rn(x.z, yv);
+                    if (d == 3) x.w = __fsub_rn(x.w, yv);
+                }
+            }
             S[r][4 * q] = static_cast<float>(static_cast<double>(x.x) * inv);
             S[r][4 * q + 1] = static_cast<float>(static_cast<double>(x.y) * inv);
             S[r][4 * q + 2] = static_cast<float>(static_cast<double>(x.z) * inv);
@@ -138,7 +169,11 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
         for (int idx = tid; idx < kST * kST; idx += 256) {
             const int r = idx >> 6, c = idx & 63;
             const int gi = r0 + r, gj = c0 + c;
-            const float x = (gi < n && gj < n) ? Xb[static_cast<int64_t>(gi) * n + gj] : 0.0f;
+            float x = (gi < n && gj < n) ? Xb[static_cast<int64_t>(gi) * n + gj] : 0.0f;
+            if (Kb && gi < n && gj < n) {
+                x = form_m(x, Kb[static_cast<int64_t>(gi) * n + gj], form.inv_sigma);
+                if (yb && gi == gj) x = __fsub_rn(x, yb[gi]);
+            }
             S[r][c] = static_cast<float>(static_cast<double>(x) * inv);
         }
     }
@@ -193,9 +228,9 @@ int bound_blocks_per_matrix(int n) {
 }
 
 cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
-                                      cudaStream_t stream) {
+                                      cudaStream_t stream, const InputForm& form) {
     dim3 grid(nblk, batch);
-    frobenius_partials_kernel<<<grid, kBoundThreads, 0, stream>>>(X, n, nblk, partial);
+    frobenius_partials_kernel<<<grid, kBoundThreads, 0, stream>>>(X, n, nblk, partial, form);
     return cudaGetLastError();
 }
 
@@ -207,24 +242,25 @@ cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, do
 
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
                                  const double* lambda, double scale, void* out_op, void* out_lo,
-                                 double op_scale, float* outF, double post, cudaStream_t stream) {
+                                 double op_scale, float* outF, double post, cudaStream_t stream,
+                                 const InputForm& form) {
     const int nt = npad / kST;
     dim3 grid(nt * (nt + 1) / 2, batch);
     switch (t) {
         case OpType::F16:
             scale_convert_kernel<OpType::F16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__half*>(out_op), static_cast<__half*>(out_lo),
-                static_cast<float>(op_scale), outF, post);
+                static_cast<float>(op_scale), outF, post, form);
             break;
         case OpType::BF16:
             scale_convert_kernel<OpType::BF16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__nv_bfloat16*>(out_op),
-                static_cast<__nv_bfloat16*>(out_lo), static_cast<float>(op_scale), outF, post);
+                static_cast<__nv_bfloat16*>(out_lo), static_cast<float>(op_scale), outF, post, form);
             break;
         case OpType::TF32:
             scale_convert_kernel<OpType::TF32><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<float*>(out_op), static_cast<float*>(out_lo),
-                static_cast<float>(op_scale), outF, post);
+                static_cast<float>(op_scale), outF, post, form);
             break;
     }
     return cudaGetLastError();

@@ -140,7 +140,7 @@ __device__ __forceinline__ bool prefetch_addend(const EpiParams& e, int b, int n
         for (int q = 0; q < 2 * Tr::kBytes; ++q) pre[q] = __ldcg(d4 + q);
         return true;
     }
-    if (e.Df && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
+    if (e.Df && !e.Df2 && gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
         const uint4* d4 = reinterpret_cast<const uint4*>(e.Df + static_cast<int64_t>(b) * e.strideDf +
                                                          static_cast<int64_t>(gi) * e.ldDf + gj0);
 #pragma unroll
@@ -148,6 +148,60 @@ __device__ __forceinline__ bool prefetch_addend(const EpiParams& e, int b, int n
         return true;
     }
     return false;
+}
+
+// Store a 32x32 fp32 block (rows gi0.., columns gj0..) of the final output F (ld, masked to nF),
+// mirrored to (gj0.., gi0..) unless it is a (symmetrised) diagonal block.
+__device__ __forceinline__ void store_f32_block(float* F, int64_t ld, int nF, int gi0, int gj0, bool diag32,
+                                                const float (&v)[32], uint8_t* wsmem) {
+    const int lane = threadIdx.x & 31;
+    const int gi = gi0 + lane;
+    const bool fast = (ld & 3) == 0 && gi0 + 32 <= nF && gj0 + 32 <= nF;
+    if (fast) {
+        float4* dst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gi) * ld + gj0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        if (!diag32) {
+            float* S = reinterpret_cast<float*>(wsmem);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
+            __syncwarp();
+            const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+            float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * ld + gi0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+            __syncwarp();
+        }
+    } else if (gi < nF) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int gj = gj0 + i;
+            if (gj >= nF) continue;
+            F[static_cast<int64_t>(gi) * ld + gj] = v[i];
+            if (!diag32) F[static_cast<int64_t>(gj) * ld + gi] = v[i];
+        }
+    }
+}
+
+// fp32 row segment [gj0, gj0 + 32) of row gi of F (ld, masked to nF: zero outside)
+__device__ __forceinline__ void load_f32_row(const float* F, int64_t ld, int nF, int gi, int gj0, float (&d)[32]) {
+    const float* row = F + static_cast<int64_t>(gi) * ld;
+    if (gi < nF && gj0 + 32 <= nF && (ld & 3) == 0) {
+        const float4* d4 = reinterpret_cast<const float4*>(row + gj0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 x = __ldcs(d4 + q);
+            d[4 * q] = x.x;
+            d[4 * q + 1] = x.y;
+            d[4 * q + 2] = x.z;
+            d[4 * q + 3] = x.w;
+        }
+    } else {
+        const bool row_ok = gi < nF;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) d[i] = (row_ok && gj0 + i < nF) ? row[gj0 + i] : 0.0f;
+    }
 }
 
 template <OpType T, bool kCg = false>
@@ -201,21 +255,30 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         add_op_row<T, kCg>(e.Dop, opBase, npad, gi, gj0, e.beta, v);
         if (e.Dop_lo) add_op_row<T, kCg>(e.Dop_lo, opBase, npad, gi, gj0, e.beta, v);
     } else if (e.Df) {                               // fp32 addend (the input X), masked to nDf
-        const float* drow = e.Df + static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf;
-        if (gi < e.nDf && gj0 + 32 <= e.nDf && (e.ldDf & 3) == 0) {
-            const float4* d4 = reinterpret_cast<const float4*>(drow + gj0);
+        float m[32];
+        load_f32_row(e.Df + static_cast<int64_t>(b) * e.strideDf, e.ldDf, e.nDf, gi, gj0, m);
+        if (e.Df2) {
+            // ADMM: m = C - X_k / sigma - Diag(y), one rounding per operation (as the bound and
+            // scale kernels form it, R22)
+            float k[32];
+            load_f32_row(e.Df2 + static_cast<int64_t>(b) * e.strideDf, e.ldDf, e.nDf, gi, gj0, k);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float4 d = __ldcs(d4 + q);
-                v[4 * q] += e.beta * d.x;
-                v[4 * q + 1] += e.beta * d.y;
-                v[4 * q + 2] += e.beta * d.z;
-                v[4 * q + 3] += e.beta * d.w;
+            for (int i = 0; i < 32; ++i) m[i] = __fsub_rn(m[i], __fmul_rn(k[i], e.df2_scale));
+            if (e.ddiag && diag32 && gi < e.nDf) {
+                const float yv = e.ddiag[static_cast<int64_t>(b) * e.nDf + gi];
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i == lane) m[i] = __fsub_rn(m[i], yv);
             }
-        } else {
-            const bool row_ok = gi < e.nDf;
+        }
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += (row_ok && gj0 + i < e.nDf) ? e.beta * drow[gj0 + i] : 0.0f;
+        for (int i = 0; i < 32; ++i) v[i] += e.beta * m[i];
+        if (e.outF2) {
+            // X_next = sigma (S - M) (P:L934-936 with M = C - A*y - X_k / sigma), stored like outF
+#pragma unroll
+            for (int i = 0; i < 32; ++i) m[i] = e.outF2_scale * (v[i] - m[i]);
+            if (diag32) symmetrize_block(m, wsmem);
+            store_f32_block(e.outF2 + static_cast<int64_t>(b) * e.strideF, e.ldF, e.nF, gi0, gj0, diag32, m, wsmem);
         }
     }
     if (diag32) symmetrize_block(v, wsmem);
@@ -266,34 +329,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem);
     }
 
-    if (e.outF) {
-        float* F = e.outF + static_cast<int64_t>(b) * e.strideF;
-        const bool fast = (e.ldF & 3) == 0 && gi0 + 32 <= e.nF && gj0 + 32 <= e.nF;
-        if (fast) {
-            float4* dst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gi) * e.ldF + gj0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-            if (!diag32) {
-                float* S = reinterpret_cast<float*>(wsmem);
-                __syncwarp();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
-                __syncwarp();
-                const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
-                float4* tdst = reinterpret_cast<float4*>(F + static_cast<int64_t>(gj0 + lane) * e.ldF + gi0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
-            }
-        } else if (gi < e.nF) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int gj = gj0 + i;
-                if (gj >= e.nF) continue;
-                F[static_cast<int64_t>(gi) * e.ldF + gj] = v[i];
-                if (!diag32) F[static_cast<int64_t>(gj) * e.ldF + gi] = v[i];
-            }
-        }
-    }
+    if (e.outF) store_f32_block(e.outF + static_cast<int64_t>(b) * e.strideF, e.ldF, e.nF, gi0, gj0, diag32, v, wsmem);
 }
 
 }  // namespace psd

@@ -39,6 +39,22 @@ struct EpiParams {
     int packed_f32;
     // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
     unsigned long long* dbg;
+    // Fused ADMM update (psd_admm_update): the fp32 addend is formed on the fly as
+    // m = Df + df2_scale * Df2 - Diag(ddiag) (C - X_k / sigma - Diag(y); Df2 shares Df's layout,
+    // ddiag is batch x nDf), and outF2 = outF2_scale * (v - m) = sigma (S - M) is stored like outF.
+    const float* Df2;
+    float df2_scale;
+    const float* ddiag;
+    float* outF2;
+    float outF2_scale;
+};
+
+// The input of the bound / scale kernels: X itself, or the ADMM argument formed on the fly,
+// M = X - inv_sigma * Xk - Diag(y)  (X = C; Xk, y as in psd_admm_update; Xk == NULL: plain X).
+struct InputForm {
+    const float* Xk = nullptr;
+    const float* y = nullptr;          // batch x n (NULL: no diagonal term)
+    float inv_sigma = 0.0f;
 };
 
 struct GemmShape {
@@ -111,6 +127,9 @@ struct SmallStep {
 struct SmallPlan {
     int nsteps;
     float s_x0;               // operand scale of X_0
+    InputForm form;           // ADMM: the input is M = X - inv_sigma Xk - Diag(y) (form.Xk != NULL)
+    float* out2;              // ADMM: X_next = sigma2 (P - M), stored like out
+    float sigma2;
     unsigned long long* dbg;  // debug: per-phase clock totals of CTA 0 (NULL in production)
     SmallStep steps[40];
 };
@@ -127,7 +146,7 @@ int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap);
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
 int bound_blocks_per_matrix(int n);
 cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
-                                      cudaStream_t stream);
+                                      cudaStream_t stream, const InputForm& form = InputForm());
 
 // lambda[b] = sqrt(sum_k partial[b*nblk+k]) (fixed order); status |= 1 if non-finite.
 cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, double* lambda,
@@ -149,6 +168,7 @@ void lanczos_prepare();   // kernel attributes (call once, outside graph capture
 
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
                                  const double* lambda, double scale, void* out_op, void* out_lo,
-                                 double op_scale, float* outF, double post, cudaStream_t stream);
+                                 double op_scale, float* outF, double post, cudaStream_t stream,
+                                 const InputForm& form = InputForm());
 
 }  // namespace psd

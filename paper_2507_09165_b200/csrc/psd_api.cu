@@ -385,8 +385,18 @@ cudaEvent_t take_event(psd_filter_s* h) {
     return e;
 }
 
+// psd_admm_update: the input is M = X - X_k / sigma - Diag(y) (X = C), formed on the fly, and the
+// reconstruction also writes X_next = sigma (S - M)
+struct AdmmArgs {
+    InputForm form;
+    float sigma;
+    float* x_out;
+};
+
 psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, float* out,
-                      const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st) {
+                      const double* lambda_in, double* lambda_out, bool want_sign, cudaStream_t st,
+                      const AdmmArgs* admm = nullptr) {
+    const InputForm form = admm ? admm->form : InputForm();
     psd_status_t rc = check_args(h, X, n64, batch64, out);
     if (rc != PSD_OK) return rc;
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
@@ -408,6 +418,11 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         const double sc_slot[3] = {sz, sy, su};
         SmallPlan sp_plan{};
         sp_plan.nsteps = static_cast<int>(steps.size());
+        if (admm) {
+            sp_plan.form = admm->form;
+            sp_plan.out2 = admm->x_out;
+            sp_plan.sigma2 = admm->sigma;
+        }
         sp_plan.s_x0 = static_cast<float>(sz);
         for (size_t i = 0; i < steps.size(); ++i) {
             const Step& s = steps[i];
@@ -473,7 +488,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     const double* lam = nullptr;
     if (h->bound == PSD_BOUND_FROBENIUS || h->bound == PSD_BOUND_LANCZOS) {
         const int nblk = bound_blocks_per_matrix(n);
-        e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st);
+        e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st, form);
         if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
         h->kernel_launches += 2;
         e = launch_finalize_bound(ws.partial, nblk, batch, ws.lambda, lambda_out, ws.status, st);
@@ -499,7 +514,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         // Theorem-2 bound (never looser than lambda_F); the real scale below uses it
         rc = ensure_lz(h, npad, batch);
         if (rc != PSD_OK) return rc;
-        e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr, sc[B_X0], nullptr, 0.0, st);
+        e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr, sc[B_X0], nullptr, 0.0, st,
+                                 form);
         if (e != cudaSuccess) return cuda_fail(e, "scale_convert (Lanczos bound)");
         e = launch_lanczos_bound(ws.op, ws.op_buf[B_X0], sc[B_X0], n, npad, batch, h->lz_steps, h->lz_safety,
                                  ws.lz_scratch, ws.lambda, lambda_out, st);
@@ -519,7 +535,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     // (a2) scale + convert; the products-free sign chain finishes here
     e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0],
                              split ? ws.op_buf[B_X0 + B_COUNT] : nullptr, sc[B_X0],
-                             (want_sign && steps.empty()) ? out : nullptr, sign_only, st);
+                             (want_sign && steps.empty()) ? out : nullptr, sign_only, st, form);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
     // (a3-a6) products
@@ -546,6 +562,13 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.ldDf = n;
             ep.strideDf = static_cast<int64_t>(n) * n;
             ep.nDf = n;
+            if (admm) {           // ADMM: the addend is M, and X_next = sigma (S - M) is written too
+                ep.Df2 = admm->form.Xk;
+                ep.df2_scale = admm->form.inv_sigma;
+                ep.ddiag = admm->form.y;
+                ep.outF2 = admm->x_out;
+                ep.outF2_scale = admm->sigma;
+            }
         }
         ep.out_op = s.out_op >= 0 ? ws.op_buf[s.out_op] : nullptr;
         ep.out_lo = (s.out_op >= 0 && split) ? ws.op_buf[s.out_op + B_COUNT] : nullptr;
@@ -1047,6 +1070,24 @@ psd_status_t psd_sign(psd_filter_t h, const float* X, int64_t n, int64_t batch, 
 psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t batch, float* out,
                             const double* lambda_in, double* lambda_out, int want_sign, void* stream) {
     return run(h, X, n, batch, out, lambda_in, lambda_out, want_sign != 0, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, const float* y, double sigma, int64_t n,
+                             int64_t batch, float* S_out, float* X_out, void* stream) {
+    if (!Xk || !X_out) return fail(PSD_EINVAL, "null Xk or X_out");
+    if ((reinterpret_cast<uintptr_t>(Xk) & 15) || (reinterpret_cast<uintptr_t>(X_out) & 15))
+        return fail(PSD_EINVAL, "Xk and X_out must be 16-byte aligned");
+    if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(PSD_EINVAL, "sigma must be finite and > 0");
+    if (S_out == X_out) return fail(PSD_EINVAL, "S_out and X_out must be distinct");
+    if (h && h->bound == PSD_BOUND_USER) return fail(PSD_EUNSUPPORTED, "psd_admm_update needs a device bound");
+    AdmmArgs a;
+    a.form.Xk = Xk;
+    a.form.y = y;
+    a.form.inv_sigma = static_cast<float>(1.0 / sigma);
+    a.sigma = static_cast<float>(sigma);
+    a.x_out = X_out;
+    // no graph cache: sigma and the extra pointers are kernel arguments of every launch
+    return run_body(h, C, n, batch, S_out, nullptr, nullptr, false, static_cast<cudaStream_t>(stream), &a);
 }
 
 psd_status_t psd_status(psd_filter_t h, void* stream) {

@@ -147,6 +147,19 @@ __device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta
     }
 }
 
+__device__ __forceinline__ float4 load_row4(const float* base, int64_t roff, int n, int q) {
+    // columns 4q..4q+3 of a row (zero past n)
+    const float* xr = base + roff;
+    if (n == kN) return __ldg(reinterpret_cast<const float4*>(xr) + q);
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int c = 4 * q;
+    if (c + 0 < n) x.x = __ldg(xr + c + 0);
+    if (c + 1 < n) x.y = __ldg(xr + c + 1);
+    if (c + 2 < n) x.z = __ldg(xr + c + 2);
+    if (c + 3 < n) x.w = __ldg(xr + c + 3);
+    return x;
+}
+
 template <bool kSplit>
 __global__ void __launch_bounds__(kThreadsS, 2)
 small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
@@ -191,15 +204,22 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 const int r = rem >> 4, q = rem & 15;
                 float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (mm < nvalid && r < n) {
-                    const float* xr = X + base + static_cast<int64_t>(mm) * n * n + static_cast<int64_t>(r) * n;
-                    if (n == kN) {
-                        x = __ldg(reinterpret_cast<const float4*>(xr) + q);
-                    } else {
-                        const int c = 4 * q;
-                        if (c + 0 < n) x.x = __ldg(xr + c + 0);
-                        if (c + 1 < n) x.y = __ldg(xr + c + 1);
-                        if (c + 2 < n) x.z = __ldg(xr + c + 2);
-                        if (c + 3 < n) x.w = __ldg(xr + c + 3);
+                    const int64_t roff = base + static_cast<int64_t>(mm) * n * n + static_cast<int64_t>(r) * n;
+                    x = load_row4(X, roff, n, q);
+                    if (plan.form.Xk) {           // ADMM: M = C - X_k / sigma - Diag(y) (R22)
+                        const float4 k = load_row4(plan.form.Xk, roff, n, q);
+                        x.x = __fsub_rn(x.x, __fmul_rn(k.x, plan.form.inv_sigma));
+                        x.y = __fsub_rn(x.y, __fmul_rn(k.y, plan.form.inv_sigma));
+                        x.z = __fsub_rn(x.z, __fmul_rn(k.z, plan.form.inv_sigma));
+                        x.w = __fsub_rn(x.w, __fmul_rn(k.w, plan.form.inv_sigma));
+                        if (plan.form.y && (r >> 2) == q) {
+                            const float yv = plan.form.y[static_cast<int64_t>(2 * pr + mm) * n + r];
+                            const int d = r & 3;
+                            if (d == 0) x.x = __fsub_rn(x.x, yv);
+                            if (d == 1) x.y = __fsub_rn(x.y, yv);
+                            if (d == 2) x.z = __fsub_rn(x.z, yv);
+                            if (d == 3) x.w = __fsub_rn(x.w, yv);
+                        }
                     }
                 }
                 // XOR-swizzle float4 columns by row to keep the transposed reads conflict-light
@@ -325,23 +345,47 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 }
             } else {
                 // final: 1/2 X + 1/2 lambda~ X0 S  (mode 1)  or  S (mode 2); symmetrise via staging
+                // the input element (row, c), c >= row: X, or the ADMM argument M (R22)
+                const int64_t roff = static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
+                const float yv = (plan.form.Xk && plan.form.y && valid && row < n)
+                                     ? plan.form.y[static_cast<int64_t>(b) * n + row] : 0.0f;
+                auto input_at = [&](int c) -> float {
+                    const bool in = valid && row < n && c < n && c >= row;
+                    float x = in ? __ldg(X + roff + c) : 0.0f;
+                    if (plan.form.Xk) {
+                        const float k = in ? __ldg(plan.form.Xk + roff + c) : 0.0f;
+                        x = __fsub_rn(x, __fmul_rn(k, plan.form.inv_sigma));
+                        if (c == row) x = __fsub_rn(x, yv);
+                    }
+                    return x;
+                };
                 if (st.final_mode == 1) {
                     // + beta X[row][c] for c >= row (the lower part is replaced by the mirror below)
                     const float a = static_cast<float>(lam);
-                    const float* xr = X + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        const float x = (valid && row < n && c < n && c >= row) ? __ldg(xr + c) : 0.0f;
-                        v[c] = a * v[c] + st.beta * x;
-                    }
+                    for (int c = 0; c < 64; ++c) v[c] = a * v[c] + st.beta * input_at(c);
                 }
                 float4* srow = reinterpret_cast<float4*>(stage + row * kN);
+                // ADMM: X_next = sigma (P - M) is stored first, while the inputs (which the
+                // outputs may overwrite: in place) are still intact; then P
+                const bool two = st.final_mode == 1 && plan.out2;
+                for (int pass = two ? 1 : 0; pass >= 0; --pass) {
+                if (pass == 1) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    for (int q = 0; q < 16; ++q)
+                        srow[q ^ (row & 15)] = make_float4(plan.sigma2 * (v[4 * q] - input_at(4 * q)),
+                                                           plan.sigma2 * (v[4 * q + 1] - input_at(4 * q + 1)),
+                                                           plan.sigma2 * (v[4 * q + 2] - input_at(4 * q + 2)),
+                                                           plan.sigma2 * (v[4 * q + 3] - input_at(4 * q + 3)));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                }
                 __syncthreads();
+                float* dst = pass == 0 ? out : plan.out2;
                 if (valid && row < n) {
-                    float* orow = out + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
+                    float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
                     if (n == kN) {
 #pragma unroll
                         for (int q = 0; q < 16; ++q) {
@@ -357,6 +401,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     }
                 }
                 __syncthreads();
+                }
             }
         }
     }

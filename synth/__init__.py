@@ -89,6 +89,28 @@ def sdp_shaped(n, seed, avg_degree=8, rank=None, sigma=1.0):
     return _f32(M)
 
 
+def maxcut_admm(n, seed, avg_degree=8, rank=None):
+    """Inputs of one ADMM S-update on a max-cut-like SDP: C = -L/4 of a random
+    graph with average degree ``avg_degree`` (as in ``sdp_shaped``), a low-rank PSD iterate X^k
+    (rank n/20, the paper's solution ranks) and a dual vector y.  Returns
+    (C, Xk, y), fp32-representable float64 arrays.  Holds none of the method's arithmetic."""
+    r = rng(seed)
+    m = int(round(avg_degree * n / 2))
+    i = r.integers(0, n, m)
+    j = r.integers(0, n, m)
+    keep = i != j
+    i, j = i[keep], j[keep]
+    W = np.zeros((n, n))
+    W[i, j] = 1.0
+    W[j, i] = 1.0
+    C = 0.25 * (W - np.diag(W.sum(axis=1)))
+    rank = max(1, n // 20) if rank is None else rank
+    V = r.standard_normal((n, rank)) * np.sqrt(avg_degree / (4.0 * n))
+    Xk = V @ V.T
+    y = r.standard_normal(n) - 0.25 * avg_degree
+    return _f32(C), _f32(0.5 * (Xk + Xk.T)), _f32(y)
+
+
 FAMILIES = {"goe": goe, "haar": haar, "sdp_shaped": sdp_shaped, "dominant": dominant}
 
 
