@@ -64,6 +64,12 @@ def load_traffic(cfg):
     return None, None
 
 
+def pair_kernel(n, batch):
+    """Whether (n, batch) runs on the CTA-pair kernel (mirrors use_pair_kernel in sym_gemm_2cta.cu)."""
+    nt = (n + 255) // 256
+    return n >= 1024 and nt * (nt + 1) // 2 * batch >= 74
+
+
 def product_filter(name):
     from paper_2507_09165_b200 import filters
     return {"half": filters.half_filter, "single": filters.single_filter,
@@ -337,8 +343,9 @@ def run_ours(args, cfg):
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "kernel": ("sym_gemm_2cta_kernel (CTA-pair tcgen05 symmetric product, fused epilogue)"
-                                    if n >= 1024 else ("small_batch_kernel (whole chain on-chip, n <= 64)"
-                                                       if n <= 64 else "sym_gemm_kernel (tcgen05 symmetric product)")),
+                                    if pair_kernel(n, count) else ("small_batch_kernel (whole chain on-chip, n <= 64)"
+                                                       if n <= 64 else "sym_gemm_kernel (1-CTA tcgen05 symmetric "
+                                                                       "product, fused epilogue)")),
                          "per_launch_flops": per_launch, "mma_passes": passes,
                          "avg_launch_ms": launch_ms, "peak_source": peak_note},
             "gpu_launches": kernel_launches,

@@ -204,6 +204,29 @@ __device__ __forceinline__ void load_f32_row(const float* F, int64_t ld, int nF,
     }
 }
 
+// L2 prefetch of this thread's addend row segment(s) [gj0, gj0 + ncols) of row gi, issued before
+// the epilogue waits for its accumulator: the addends (e.g. the fp32 input X of the reconstruction,
+// 2 GB at config c4, not L2-resident) then arrive while the MMAs of the tile still run.
+template <OpType T>
+__device__ __forceinline__ void prefetch_addend_l2(const EpiParams& e, int b, int npad, int gi, int gj0, int ncols) {
+    using Tr = OpTraits<T>;
+    auto pf = [](const void* p) { asm volatile("prefetch.global.L2 [%0];" :: "l"(p)); };
+    if (e.Dop) {
+        const int64_t off = static_cast<int64_t>(b) * npad * npad + static_cast<int64_t>(gi) * npad + gj0;
+        for (int c = 0; c < ncols * Tr::kBytes; c += 128) {
+            pf(reinterpret_cast<const uint8_t*>(e.Dop) + off * Tr::kBytes + c);
+            if (e.Dop_lo) pf(reinterpret_cast<const uint8_t*>(e.Dop_lo) + off * Tr::kBytes + c);
+        }
+    } else if (e.Df && gi < e.nDf) {
+        const int64_t off = static_cast<int64_t>(b) * e.strideDf + static_cast<int64_t>(gi) * e.ldDf + gj0;
+        const int cols = min(ncols, e.nDf - gj0);
+        for (int c = 0; c < cols; c += 32) {
+            pf(e.Df + off + c);
+            if (e.Df2) pf(e.Df2 + off + c);
+        }
+    }
+}
+
 template <OpType T, bool kCg = false>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
                                                bool /*tile_diag*/, const uint32_t (&raw)[32], uint8_t* wsmem,

@@ -256,6 +256,13 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             int b, I, J;
             decode_tile(t, s, b, I, J);
             const int acc = it & 1;
+            {
+                // addend rows of this thread (row gi0 + lane) for the whole tile into L2 while the
+                // tile's MMAs run (first column at or right of the diagonal on a diagonal tile)
+                const int gi = I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32 + (threadIdx.x & 31);
+                const int c_lo = (I == J) ? ((gi - J * kT2) & ~31) : 0;
+                prefetch_addend_l2<T>(e, b, s.npad, gi, J * kT2 + c_lo, kT2 - c_lo);
+            }
             const unsigned long long e0 = (e.dbg && q == 0 && ptx::elect_one()) ? clock64() : 0;
             ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
             const unsigned long long e1 = e0 ? clock64() : 0;
