@@ -13,6 +13,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte aligned start of dynamic shared memory, by pointer arithmetic on the shared pointer
+// itself (a round trip through uintptr_t loses the address space: every access through the result
+// would then be a generic LD/ST instead of LDS/STS)
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* smem_raw) {
+    const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    return smem_raw + pad;
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;
     asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));

@@ -166,7 +166,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                    double* __restrict__ lambda_out, unsigned* __restrict__ status, const SmallPlan plan) {
     using L = SmallLayout<kSplit>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
     double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][4 warps]

@@ -91,7 +91,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, BN);
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint8_t* ring = smem;                                         // stage: A | B | A_lo | B_lo
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes1);
     uint64_t* empty = full + kStages;

@@ -62,7 +62,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
     constexpr uint32_t kTileConsumers = 10;
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint8_t* ring = smem;                                       // stage st: A at +0, B at +16 KB
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
     uint64_t* empty = full + kStages2;
