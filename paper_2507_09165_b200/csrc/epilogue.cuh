@@ -305,6 +305,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         }
     }
     if (diag32) symmetrize_block(v, wsmem);
+    if (e.dbg_nostore) {                             // debug experiment only: keep v live, store nothing
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc += v[i];
+        if (acc == 12345.678f) reinterpret_cast<volatile float*>(wsmem)[0] = acc;
+        return;
+    }
 
     if (packed_off >= 0) {
         // row-panel mode: this warp's 32 x 32 block of the tile, unmirrored, row-major tile slot

@@ -39,6 +39,7 @@ struct EpiParams {
     int packed_f32;
     // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
     unsigned long long* dbg;
+    int dbg_nostore;          // debug experiment (PSD_DEBUG_NOSTORE): skip the epilogue's stores
     // Fused ADMM update (psd_admm_update): the fp32 addend is formed on the fly as
     // m = Df + df2_scale * Df2 - Diag(ddiag) (C - X_k / sigma - Diag(y); Df2 shares Df's layout,
     // ddiag is batch x nDf), and outF2 = outF2_scale * (v - m) = sigma (S - M) is stored like outF.

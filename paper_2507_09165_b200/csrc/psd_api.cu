@@ -116,8 +116,9 @@ struct psd_filter_s {
     // pipelined host-buffer projection (psd_project_host)
     struct HostPipe {
         cudaStream_t s[3] = {nullptr, nullptr, nullptr};   // h2d, compute, d2h
-        float* dx[2] = {nullptr, nullptr};
-        float* dout[2] = {nullptr, nullptr};
+        static constexpr int kSlots = 3;         // chunk buffers in flight (H2D / project / D2H)
+        float* dx[kSlots] = {};
+        float* dout[kSlots] = {};
         size_t chunk_bytes = 0;
     } hp;
     // profiling / launch accounting
@@ -578,6 +579,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.strideF = static_cast<int64_t>(n) * n;
             ep.nF = n;
         }
+        ep.dbg_nostore = std::getenv("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug experiment
         return ep;
     };
     const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
@@ -1145,7 +1147,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
         for (int i = 0; i < 3; ++i)
             if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "cudaStreamCreate");
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < psd_filter_s::HostPipe::kSlots; ++i) {
             if (cudaMalloc(&hp.dx[i], per * mat) != cudaSuccess || cudaMalloc(&hp.dout[i], per * mat) != cudaSuccess) {
                 free_hostpipe(h);
                 return fail(PSD_ENOMEM, "cudaMalloc host-pipeline buffers failed");
@@ -1159,10 +1161,10 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
     cudaEvent_t start = ev();
     cudaEventRecord(start, user);
     for (auto q : hp.s) cudaStreamWaitEvent(q, start, 0);
-    cudaEvent_t freed[2] = {nullptr, nullptr};
+    cudaEvent_t freed[psd_filter_s::HostPipe::kSlots] = {};
     std::vector<cudaEvent_t> used = {start};
     for (int c = 0; c * per < batch; ++c) {
-        const int slot = c & 1;
+        const int slot = c % psd_filter_s::HostPipe::kSlots;
         const int64_t b0 = c * per;
         const int64_t nb = std::min<int64_t>(per, batch - b0);
         if (freed[slot]) cudaStreamWaitEvent(hp.s[0], freed[slot], 0);
@@ -1183,7 +1185,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
         cudaEvent_t outd = ev();
         used.push_back(outd);
         cudaEventRecord(outd, hp.s[2]);
-        freed[slot] = outd;      // chunk c+2 may reuse this slot's X and out buffers after the D2H
+        freed[slot] = outd;      // chunk c+kSlots may reuse this slot's X and out buffers after the D2H
     }
     cudaEvent_t done = ev();
     used.push_back(done);

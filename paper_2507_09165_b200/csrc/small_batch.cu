@@ -160,8 +160,11 @@ __device__ __forceinline__ float4 load_row4(const float* base, int64_t roff, int
     return x;
 }
 
+// resident CTAs per SM: smem allows 3 for the single-pass layout (3 x 66 KB), 2 for the split one
+template <bool kSplit> constexpr int kSmallCtasPerSm = kSplit ? 2 : 3;
+
 template <bool kSplit>
-__global__ void __launch_bounds__(kThreadsS, 2)
+__global__ void __launch_bounds__(kThreadsS, kSmallCtasPerSm<kSplit>)
 small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
                    double* __restrict__ lambda_out, unsigned* __restrict__ status, const SmallPlan plan) {
     using L = SmallLayout<kSplit>;
@@ -427,7 +430,7 @@ cudaError_t launch_small_t(const float* X, float* out, int n, int batch, double*
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int pairs = (batch + 1) / 2;
-    int grid = 2 * num_sms;
+    int grid = kSmallCtasPerSm<kSplit> * num_sms;
     if (grid > pairs) grid = pairs;
     small_batch_kernel<kSplit><<<grid, kThreadsS, L::kBytes, stream>>>(X, out, n, batch, lambda_out, status, plan);
     return cudaGetLastError();
