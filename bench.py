@@ -377,7 +377,9 @@ def run_rowpanel(args, cfg, world, rank, dev):
     from paper_2507_09165_b200 import Filter, dist as pdist
     n = cfg["n"]
     f = Filter(product_filter(cfg["filter"]), precision=args.precision)
-    rp = pdist.RowPanelProjector(f, n)
+    # p2p (default): each product kernel stores its tiles into every rank's region over NVLink
+    # (no collective); nccl: packed tiles all-gathered with NCCL after each product
+    rp = pdist.PeerRowPanelProjector(f, n) if args.rowpanel == "p2p" else pdist.RowPanelProjector(f, n)
     r0, rows = rp.row_range()
     g = synth.rng(synth.SEED_BASE + 5)
     A = g.standard_normal((n, n)).astype(np.float32)          # GOE rows: every rank draws the same A
@@ -410,8 +412,10 @@ def run_rowpanel(args, cfg, world, rank, dev):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic",
-            "config": {"workload": cfg["workload"] + f" -- row panels over {world} GPUs (NCCL all-gather of "
-                                                     "packed upper tiles per product)", "n": n, "global_batch": 1,
+            "config": {"workload": cfg["workload"] + f" -- row panels over {world} GPUs " + (
+                           "(product kernels store their tiles into every rank's operand region, epoch barrier)"
+                           if args.rowpanel == "p2p" else "(NCCL all-gather of packed upper tiles per product)"),
+                       "n": n, "global_batch": 1,
                        "parallelism": f"row-panel tp{world}", "products_per_matrix": G},
             "tflops_algorithmic": float(n) * n * (n + 1) * G * args.steps / (ms / 1000.0) / 1e12,
             "gpu_launches": kernel_launches, "clocks": clk.summary(),
@@ -428,6 +432,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default=None, choices=["fp16", "bf16", "tf32", "tf32x3", "fp16x3", "bf16x3"])
+    ap.add_argument("--rowpanel", default="p2p", choices=["p2p", "nccl"], help="config c5 exchange under torchrun")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -228,6 +228,37 @@ psd_status_t psd_project_rowpanel(psd_filter_t h, const float* X_rows, int64_t n
 psd_status_t psd_project_rowpanel_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
                                           int want_sign, void* stream);
 
+/* Peer-memory row panels (SURVEY section 8(f) NEXT #3, config c5 without a collective on the data
+ * path): the product and its all-gather are ONE kernel.  Every rank holds a device region with
+ * the full operand buffers; each product kernel computes this rank's share of the upper 256-tiles
+ * (round robin, psd_rowpanel_tiles) and its epilogue stores every tile and its mirror straight
+ * into every rank's region through peer pointers (NVLink / NVSwitch), overlapping the transfer
+ * with the next tiles' MMAs; a cross-rank epoch barrier (system-scope release/acquire flags in
+ * the regions) separates consecutive products.  The final product stores each fp32 32-row block
+ * to the rank that owns those rows.  FP16 / BF16 / TF32, Frobenius bound; n % nranks == 0,
+ * (n / nranks) % 32 == 0, nranks <= 8.
+ *
+ * Setup (once per (n, nranks), every rank):
+ *   psd_rowpanel_p2p_region(h, n, nranks, rank, handle)   allocate this rank's region
+ *       (~ 6 n^2 operand bytes + 8 n^2) and return its CUDA IPC handle (64 bytes);
+ *   exchange the handles (e.g. torch.distributed all_gather_object), then
+ *   psd_rowpanel_p2p_attach(h, handles)                    handles: nranks x 64 bytes in rank
+ *       order; opens the peers' regions (cudaIpcOpenMemHandle, lazy peer access).
+ * Run: psd_project_rowpanel_p2p(h, X_rows, n, rank, nranks, out_rows, want_sign, stream): X_rows,
+ *   out_rows = this rank's rows [rank*n/nranks, +n/nranks) x n fp32 (device).  Every rank must
+ *   call it (collective); a rank that never arrives makes the others trap after 10 s.
+ * psd_project_rowpanel_p2p_virtual(h, X, n, nranks, out, want_sign, stream): all nranks regions
+ *   local to this device and every rank's kernels run here (tests of the per-rank code on one
+ *   GPU); X, out full n x n.
+ * psd_rowpanel_p2p_release(h): close / free the regions (also done by psd_filter_destroy). */
+psd_status_t psd_rowpanel_p2p_region(psd_filter_t h, int64_t n, int nranks, int rank, char handle[64]);
+psd_status_t psd_rowpanel_p2p_attach(psd_filter_t h, const char* handles);
+psd_status_t psd_project_rowpanel_p2p(psd_filter_t h, const float* X_rows, int64_t n, int rank, int nranks,
+                                      float* out_rows, int want_sign, void* stream);
+psd_status_t psd_project_rowpanel_p2p_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
+                                              int want_sign, void* stream);
+void psd_rowpanel_p2p_release(psd_filter_t h);
+
 /* Host helper: the upper 256-tiles rank `rank` computes, as (I << 16) | J codes in its packed
  * order, padded with 0xFFFFFFFF to the common per-rank count.  Returns the real count (codes ==
  * NULL: returns the padded per-rank count). */

@@ -195,6 +195,21 @@ class Filter:
               "psd_project_rowpanel_virtual")
         return out
 
+    def project_rowpanel_p2p_virtual(self, X, nranks, out=None, sign=False, stream=None):
+        """Peer-memory row-panel projection (the product kernels store their tiles into every rank's
+        operand region, no collective) with `nranks` virtual ranks whose regions all live on this GPU."""
+        import torch
+        Xb = _check_matrix(X)
+        if Xb.shape[0] != 1:
+            raise ValueError("row panels project one matrix")
+        if out is None:
+            out = torch.empty_like(X)
+        check(self._lib.psd_project_rowpanel_p2p_virtual(self._h, ctypes.c_void_p(Xb.data_ptr()), Xb.shape[-1],
+                                                         int(nranks), ctypes.c_void_p(_check_matrix(out).data_ptr()),
+                                                         1 if sign else 0, _stream_ptr(stream)),
+              "psd_project_rowpanel_p2p_virtual")
+        return out
+
     def sym_product(self, A, B, D=None, alpha=1.0, beta=0.0, out=None, stream=None):
         """C = alpha (A B) + beta D for commuting symmetric A, B (upper triangles read)."""
         import torch

@@ -47,6 +47,13 @@ SIGNATURES = [
                                         _c.c_int, _c.c_void_p, _c.c_void_p]),
     ("psd_project_rowpanel_virtual", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_void_p,
                                                 _c.c_int, _c.c_void_p]),
+    ("psd_rowpanel_p2p_region", _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int, _c.c_int, _c.c_char_p]),
+    ("psd_rowpanel_p2p_attach", _c.c_int, [_c.c_void_p, _c.c_char_p]),
+    ("psd_project_rowpanel_p2p", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int, _c.c_void_p,
+                                            _c.c_int, _c.c_void_p]),
+    ("psd_project_rowpanel_p2p_virtual", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_void_p,
+                                                    _c.c_int, _c.c_void_p]),
+    ("psd_rowpanel_p2p_release", None, [_c.c_void_p]),
     ("psd_rowpanel_tiles", _c.c_int, [_c.c_int64, _c.c_int, _c.c_int, _c.c_void_p, _c.c_int]),
     ("psd_sym_product", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_double, _c.c_double,
                                    _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),

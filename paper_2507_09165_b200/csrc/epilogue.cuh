@@ -93,6 +93,68 @@ __device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int np
 
 // kCg: load through L2 only (ld.global.cg) -- the persistent chain kernel rewrites the addend
 // buffers between its products, so a line this SM cached in L1 earlier may be stale.
+// Same block stored into every destination of `dsts` (peer-memory row-panel mode): the values are
+// converted and transposed once, then written npeers times (direct + mirrored 16-byte row segments).
+template <OpType T>
+__device__ __forceinline__ void store_op_block_peers(void* const* dsts, int nd, int64_t opBase, int npad, int gi0,
+                                                     int gj0, bool diag32, const float (&v)[32], uint8_t* wsmem) {
+    using Tr = OpTraits<T>;
+    using op_t = typename Tr::type;
+    const int lane = threadIdx.x & 31;
+    constexpr int kW = 2 * Tr::kBytes;              // 16-byte words per 32-element row segment
+    uint4 dw[kW], mw[kW];
+    if constexpr (Tr::kBytes == 2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) w[h] = Tr::pack2(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
+            dw[q] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (!diag32) {
+            uint16_t* S = reinterpret_cast<uint16_t*>(wsmem);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const op_t cv = Tr::cvt(v[c]);
+                S[c * 40 + lane] = *reinterpret_cast<const uint16_t*>(&cv);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mw[q] = reinterpret_cast<const uint4*>(S + lane * 40)[q];
+            __syncwarp();
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            dw[q] = make_uint4(__float_as_uint(Tr::cvt(v[4 * q])), __float_as_uint(Tr::cvt(v[4 * q + 1])),
+                               __float_as_uint(Tr::cvt(v[4 * q + 2])), __float_as_uint(Tr::cvt(v[4 * q + 3])));
+        if (!diag32) {
+            float* S = reinterpret_cast<float*>(wsmem);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[c * 36 + lane] = Tr::cvt(v[c]);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mw[q] = reinterpret_cast<const uint4*>(S + lane * 36)[q];
+            __syncwarp();
+        }
+    }
+    const int64_t drow = opBase + static_cast<int64_t>(gi0 + lane) * npad + gj0;
+    const int64_t mrow = opBase + static_cast<int64_t>(gj0 + lane) * npad + gi0;
+    for (int p = 0; p < nd; ++p) {
+        op_t* base = reinterpret_cast<op_t*>(dsts[p]);
+        uint4* dd = reinterpret_cast<uint4*>(base + drow);
+#pragma unroll
+        for (int q = 0; q < kW; ++q) __stcs(dd + q, dw[q]);
+        if (!diag32) {
+            uint4* md = reinterpret_cast<uint4*>(base + mrow);
+#pragma unroll
+            for (int q = 0; q < kW; ++q) __stcs(md + q, mw[q]);
+        }
+    }
+}
+
 template <OpType T, bool kCg = false>
 __device__ __forceinline__ void add_op_row(const void* D, int64_t opBase, int npad, int gi, int gj0, float beta,
                                            float (&v)[32]) {
@@ -180,6 +242,40 @@ __device__ __forceinline__ void store_f32_block(float* F, int64_t ld, int nF, in
             if (gj >= nF) continue;
             F[static_cast<int64_t>(gi) * ld + gj] = v[i];
             if (!diag32) F[static_cast<int64_t>(gj) * ld + gi] = v[i];
+        }
+    }
+}
+
+// store_f32_block with separate bases for the direct block (rows gi0..) and the mirrored one
+// (rows gj0..): the peer-memory row-panel path sends each to the rank owning the rows.
+__device__ __forceinline__ void store_f32_block_split(float* Fd, float* Fm, int64_t ld, int nF, int gi0, int gj0,
+                                                      bool diag32, const float (&v)[32], uint8_t* wsmem) {
+    const int lane = threadIdx.x & 31;
+    const int gi = gi0 + lane;
+    const bool fast = (ld & 3) == 0 && gi0 + 32 <= nF && gj0 + 32 <= nF;
+    if (fast) {
+        float4* dst = reinterpret_cast<float4*>(Fd + static_cast<int64_t>(gi) * ld + gj0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) __stcs(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        if (!diag32) {
+            float* S = reinterpret_cast<float*>(wsmem);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) S[c * 36 + lane] = v[c];
+            __syncwarp();
+            const float4* src = reinterpret_cast<const float4*>(S + lane * 36);
+            float4* tdst = reinterpret_cast<float4*>(Fm + static_cast<int64_t>(gj0 + lane) * ld + gi0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcs(tdst + q, src[q]);
+            __syncwarp();
+        }
+    } else if (gi < nF) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int gj = gj0 + i;
+            if (gj >= nF) continue;
+            Fd[static_cast<int64_t>(gi) * ld + gj] = v[i];
+            if (!diag32) Fm[static_cast<int64_t>(gj) * ld + gi] = v[i];
         }
     }
 }
@@ -356,10 +452,20 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             }
             store_op_block<T>(e.out_lo, opBase, npad, gi0, gj0, diag32, lo, wsmem);
         }
-        store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem);
+        if (e.npeers > 0)
+            store_op_block_peers<T>(e.out_peers, e.npeers, opBase, npad, gi0, gj0, diag32, w, wsmem);
+        else
+            store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem);
     }
 
-    if (e.outF) store_f32_block(e.outF + static_cast<int64_t>(b) * e.strideF, e.ldF, e.nF, gi0, gj0, diag32, v, wsmem);
+    if (e.peer_rows > 0) {
+        // peer-memory row panels: each 32-row block goes to the rank owning those rows
+        // (rows past n -- padding -- are never stored; clamp the owner index for them)
+        const int od = min(gi0 / e.peer_rows, kMaxPeers - 1), om = min(gj0 / e.peer_rows, kMaxPeers - 1);
+        store_f32_block_split(e.outF_peers[od], e.outF_peers[om], e.ldF, e.nF, gi0, gj0, diag32, v, wsmem);
+    } else if (e.outF) {
+        store_f32_block(e.outF + static_cast<int64_t>(b) * e.strideF, e.ldF, e.nF, gi0, gj0, diag32, v, wsmem);
+    }
 }
 
 }  // namespace psd

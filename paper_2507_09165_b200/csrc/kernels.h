@@ -15,6 +15,8 @@ constexpr int kTile = 128;
 constexpr int kBlockKBytes = 128;
 constexpr int kPadTo = 128;   // padded matrix dimension multiple
 
+constexpr int kMaxPeers = 8;   // ranks of the peer-memory row-panel path
+
 // Epilogue of one symmetric product C = alpha_eff * (A B) + beta * D over the upper
 // tiles (I <= J) of each matrix; see sym_gemm.cu for which elements go where.
 struct EpiParams {
@@ -40,6 +42,13 @@ struct EpiParams {
     // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
     unsigned long long* dbg;
     int dbg_nostore;          // debug experiment (PSD_DEBUG_NOSTORE): skip the epilogue's stores
+    // Peer-memory row-panel mode (the product and its all-gather in one kernel): the operand copy
+    // goes to out_peers[0..npeers) -- the same buffer of every rank, mapped into this process --
+    // and fp32 output row r to outF_peers[r / peer_rows] (its owner rank's buffer, ld ldF).
+    void* out_peers[kMaxPeers];
+    float* outF_peers[kMaxPeers];
+    int npeers;
+    int peer_rows;
     // Fused ADMM update (psd_admm_update): the fp32 addend is formed on the fly as
     // m = Df + df2_scale * Df2 - Diag(ddiag) (C - X_k / sigma - Diag(y); Df2 shares Df's layout,
     // ddiag is batch x nDf), and outF2 = outF2_scale * (v - m) = sigma (S - M) is stored like outF.
@@ -142,6 +151,13 @@ cudaError_t launch_small_batch(bool split, const float* X, float* out, int n, in
 cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
                                 int64_t ld, cudaStream_t stream);
 int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap);
+// Cross-rank epoch barrier of the peer-memory path: signal stores `epoch` into slot `rank` of every
+// rank's flag array (system-scope release after a system fence); wait spins until every slot of
+// this rank's flags reaches `epoch` (system-scope acquire; traps after 10 s instead of hanging).
+cudaError_t launch_peer_signal(unsigned long long* const* flags_dev, int nranks, int rank, unsigned long long epoch,
+                               cudaStream_t stream);
+cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, unsigned long long epoch,
+                             cudaStream_t stream);
 
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.

@@ -93,6 +93,23 @@ struct psd_filter_s {
         uint32_t* codes = nullptr;      // [nranks][per] tile codes (gather order)
         std::vector<int> counts;        // real tiles per rank
     } rp;
+    // peer-memory row-panel path (multi-GPU without a collective on the data path): every rank
+    // holds a region with the full operand buffers; each product kernel stores its tiles into
+    // every rank's region (peer pointers over NVLink), an epoch barrier separates the products
+    struct PeerPath {
+        int n = 0, npad = 0, nranks = 0, rank = 0;
+        bool is_virtual = false, attached = false;
+        OpType op = OpType::F16;
+        size_t region_bytes = 0, op_bytes_buf = 0, pfull_off = 0, xg_off = 0, flags_off = 0;
+        std::vector<uint8_t*> base;          // [nranks]: own (cudaMalloc), peers (IPC-mapped) or all local (virtual)
+        std::vector<char> ipc_opened;        // which bases were opened with cudaIpcOpenMemHandle
+        std::vector<std::vector<CUtensorMap>> tmaps;   // [local region][B_COUNT]
+        unsigned long long** flags_dev = nullptr;       // device array [nranks] of the flag arrays
+        unsigned long long epoch = 0;
+        uint32_t* codes = nullptr;           // [nranks][per] upper-tile codes
+        std::vector<int> counts;
+        int per = 0;
+    } pp;
     // CUDA-graph cache of whole psd_project sequences (host launch overhead dominates small n)
     struct GraphEntry {
         const void* X;
@@ -212,6 +229,7 @@ int64_t ws_bytes(OpType op, bool split, int64_t npad, int64_t batch) {
 }
 
 void free_graphs(psd_filter_s* h);
+void free_peerpath(psd_filter_s* h);
 
 // Lanczos-bound scratch, grown on demand (never inside a graph capture)
 psd_status_t ensure_lz(psd_filter_s* h, int npad, int batch) {
@@ -967,6 +985,188 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
     return PSD_OK;
 }
 
+// ------------------------------------------------------------------ peer-memory row panels
+void free_peerpath(psd_filter_s* h) {
+    auto& pp = h->pp;
+    if (pp.base.empty() && !pp.codes && !pp.flags_dev) return;
+    cudaDeviceSynchronize();
+    for (size_t q = 0; q < pp.base.size(); ++q) {
+        if (!pp.base[q]) continue;
+        if (pp.ipc_opened[q]) cudaIpcCloseMemHandle(pp.base[q]);
+        else cudaFree(pp.base[q]);
+    }
+    if (pp.flags_dev) cudaFree(pp.flags_dev);
+    if (pp.codes) cudaFree(pp.codes);
+    pp = psd_filter_s::PeerPath();
+}
+
+// Region layout: [B_COUNT operand buffers npad^2][pfull npad^2 fp32][X n^2 fp32][flags 64 x u64]
+psd_status_t peer_layout(psd_filter_s* h, int n, int nranks, int rank, bool is_virtual) {
+    auto& pp = h->pp;
+    if (n < 256 || n > 65536 || nranks < 1 || nranks > kMaxPeers || n % nranks || rank < 0 || rank >= nranks)
+        return fail(PSD_EINVAL, "peer row panels: 256 <= n, 1 <= nranks <= 8, n % nranks == 0");
+    if ((n / nranks) % 32) return fail(PSD_EINVAL, "peer row panels: rows per rank must be a multiple of 32");
+    if (split_of(h->prec)) return fail(PSD_EUNSUPPORTED, "row panels: FP16, BF16, TF32 only");
+    if (h->bound != PSD_BOUND_FROBENIUS) return fail(PSD_EUNSUPPORTED, "row panels: Frobenius bound only");
+    free_peerpath(h);
+    pp.n = n;
+    pp.npad = (n + 255) / 256 * 256;
+    pp.nranks = nranks;
+    pp.rank = rank;
+    pp.is_virtual = is_virtual;
+    pp.op = op_of(h->prec);
+    auto up = [](size_t x) { return (x + 4095) / 4096 * 4096; };
+    pp.op_bytes_buf = up(static_cast<size_t>(pp.npad) * pp.npad * op_bytes(pp.op));
+    pp.pfull_off = B_COUNT * pp.op_bytes_buf;
+    pp.xg_off = pp.pfull_off + up(static_cast<size_t>(pp.npad) * pp.npad * 4);
+    pp.flags_off = pp.xg_off + up(static_cast<size_t>(n) * n * 4);
+    pp.region_bytes = pp.flags_off + 4096;
+    pp.base.assign(nranks, nullptr);
+    pp.ipc_opened.assign(nranks, 0);
+    return PSD_OK;
+}
+
+psd_status_t peer_alloc_local(psd_filter_s* h, int q) {
+    auto& pp = h->pp;
+    void* p = nullptr;
+    if (cudaMalloc(&p, pp.region_bytes) != cudaSuccess) return fail(PSD_ENOMEM, "cudaMalloc peer region failed");
+    cudaMemset(p, 0, pp.region_bytes);        // zero padding of every operand; zero flags
+    pp.base[q] = static_cast<uint8_t*>(p);
+    std::vector<CUtensorMap> maps(B_COUNT);
+    for (int i = 0; i < B_COUNT; ++i)
+        if (!make_operand_tmap(&maps[i], pp.base[q] + i * pp.op_bytes_buf, pp.op, pp.npad, 1))
+            return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
+    if (pp.tmaps.size() < static_cast<size_t>(pp.nranks)) pp.tmaps.resize(pp.nranks);
+    pp.tmaps[q] = maps;
+    return PSD_OK;
+}
+
+// tile codes + the device table of flag arrays, once every base is known
+psd_status_t peer_finish(psd_filter_s* h) {
+    auto& pp = h->pp;
+    const int nt = pp.npad / 256;
+    pp.per = rowpanel_tiles(nt, pp.nranks, 0, nullptr, 0);
+    std::vector<uint32_t> codes(static_cast<size_t>(pp.nranks) * std::max(pp.per, 1));
+    pp.counts.assign(pp.nranks, 0);
+    for (int r = 0; r < pp.nranks; ++r) pp.counts[r] = rowpanel_tiles(nt, pp.nranks, r, codes.data() + r * pp.per, pp.per);
+    std::vector<unsigned long long*> fl(pp.nranks);
+    for (int q = 0; q < pp.nranks; ++q) fl[q] = reinterpret_cast<unsigned long long*>(pp.base[q] + pp.flags_off);
+    if (cudaMalloc(&pp.codes, codes.size() * 4) != cudaSuccess ||
+        cudaMalloc(&pp.flags_dev, fl.size() * sizeof(void*)) != cudaSuccess)
+        return fail(PSD_ENOMEM, "cudaMalloc peer tables failed");
+    cudaMemcpy(pp.codes, codes.data(), codes.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(pp.flags_dev, fl.data(), fl.size() * sizeof(void*), cudaMemcpyHostToDevice);
+    pp.attached = true;
+    return PSD_OK;
+}
+
+// Algorithm 2 over row panels with the product-and-gather fused into the product kernels:
+// X rows -> every rank's X copy (peer copies), barrier, bound + scale on every rank, then per
+// product: this rank's upper tiles, the epilogue storing each tile (and its mirror) into every
+// rank's operand buffer, barrier; the final product stores each fp32 block to the rank owning
+// its rows.  Virtual mode: all `nranks` regions are local and every rank's kernels run here.
+psd_status_t run_rowpanel_p2p(psd_filter_s* h, const float* X, float* out, bool want_sign, cudaStream_t st) {
+    auto& pp = h->pp;
+    if (!pp.attached) return fail(PSD_EINVAL, "peer row panels: region not set up / attached");
+    const int n = pp.n, npad = pp.npad, P = pp.nranks, rows = n / P;
+    psd_status_t rc = ensure_ws(h, npad, 1);
+    if (rc != PSD_OK) return rc;
+    Workspace& ws = h->ws;
+    cudaError_t e;
+    const int r_lo = pp.is_virtual ? 0 : pp.rank, r_hi = pp.is_virtual ? P : pp.rank + 1;
+    auto region = [&](int q, size_t off) { return static_cast<void*>(pp.base[q] + off); };
+    auto xg = [&](int q) { return reinterpret_cast<float*>(pp.base[q] + pp.xg_off); };
+    auto barrier = [&]() -> psd_status_t {
+        ++pp.epoch;
+        for (int r = r_lo; r < r_hi; ++r) {
+            if ((e = launch_peer_signal(pp.flags_dev, P, r, pp.epoch, st)) != cudaSuccess) return cuda_fail(e, "peer signal");
+        }
+        for (int r = r_lo; r < r_hi; ++r) {
+            const auto* fl = reinterpret_cast<const unsigned long long*>(pp.base[r] + pp.flags_off);
+            if ((e = launch_peer_wait(fl, P, pp.epoch, st)) != cudaSuccess) return cuda_fail(e, "peer wait");
+        }
+        h->kernel_launches += 2 * (r_hi - r_lo);
+        return PSD_OK;
+    };
+    // (1) X rows into every rank's X copy
+    for (int r = r_lo; r < r_hi; ++r)
+        for (int q = 0; q < P; ++q) {
+            const float* src = pp.is_virtual ? X + static_cast<int64_t>(r) * rows * n : X;
+            e = cudaMemcpyAsync(xg(q) + static_cast<int64_t>(r) * rows * n, src, static_cast<size_t>(rows) * n * 4,
+                                cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "X rows to peers");
+        }
+    if ((rc = barrier()) != PSD_OK) return rc;
+    // (2) bound (identical on every rank) and (3) X_0 into every local region
+    const int nblk = bound_blocks_per_matrix(n);
+    e = launch_frobenius_partials(xg(r_lo), n, 1, ws.partial, nblk, st);
+    if (e == cudaSuccess) e = launch_finalize_bound(ws.partial, nblk, 1, ws.lambda, nullptr, ws.status, st);
+    for (int r = r_lo; r < r_hi && e == cudaSuccess; ++r)
+        e = launch_scale_convert(pp.op, xg(r), n, npad, 1, ws.lambda, 1.0, region(r, B_X0 * pp.op_bytes_buf), nullptr,
+                                 1.0, nullptr, 0.0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bound / scale");
+    h->kernel_launches += 2 + (r_hi - r_lo);
+    double sign_only = 0.0;
+    std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
+    if (steps.empty()) return fail(PSD_EUNSUPPORTED, "row panels: filter without products");
+    if (steps.size() * P > static_cast<size_t>(kMaxSteps)) return fail(PSD_EUNSUPPORTED, "too many products");
+    e = cudaMemsetAsync(ws.counters, 0, steps.size() * P * sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    // (4) the products, each fused with its all-gather
+    for (size_t si = 0; si < steps.size(); ++si) {
+        const Step& s = steps[si];
+        for (int r = r_lo; r < r_hi; ++r) {
+            if (pp.counts[r] == 0) continue;
+            EpiParams ep{};
+            ep.alpha = static_cast<float>(s.alpha);
+            ep.alpha_dev = s.alpha_lambda ? ws.lambda : nullptr;
+            ep.beta = static_cast<float>(s.beta);
+            ep.out_scale = 1.0f;
+            if (s.D >= 0) {
+                ep.Dop = region(r, s.D * pp.op_bytes_buf);
+            } else if (s.D == D_XIN) {
+                ep.Df = xg(r);
+                ep.ldDf = n;
+                ep.strideDf = static_cast<int64_t>(n) * n;
+                ep.nDf = n;
+            }
+            if (s.out_op >= 0) {
+                ep.npeers = P;
+                for (int q = 0; q < P; ++q) ep.out_peers[q] = region(q, s.out_op * pp.op_bytes_buf);
+                ep.out_op = ep.out_peers[r];
+            }
+            if (s.outF) {
+                ep.peer_rows = rows;
+                for (int q = 0; q < P; ++q) ep.outF_peers[q] = reinterpret_cast<float*>(region(q, pp.pfull_off));
+                ep.outF = ep.outF_peers[r];
+                ep.ldF = npad;
+                ep.strideF = 0;
+                ep.nF = n;
+            }
+            OperandMaps m;
+            m.a = pp.tmaps[r][s.A];
+            m.b = pp.tmaps[r][s.B];
+            m.a_lo = m.a;
+            m.b_lo = m.b;
+            GemmShape shape{npad, 1, pp.codes + static_cast<size_t>(r) * pp.per, pp.counts[r],
+                            ws.counters + si * P + r};
+            e = launch_sym_gemm_2cta(pp.op, false, m, shape, ep, st);
+            if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (peer row panel)");
+            h->kernel_launches += 1;
+        }
+        if ((rc = barrier()) != PSD_OK) return rc;
+    }
+    // (5) this rank's rows of the result (every rank's rows in virtual mode)
+    for (int r = r_lo; r < r_hi; ++r) {
+        float* dst = pp.is_virtual ? out + static_cast<int64_t>(r) * rows * n : out;
+        const float* src = reinterpret_cast<const float*>(region(r, pp.pfull_off)) + static_cast<size_t>(r) * rows * npad;
+        e = cudaMemcpy2DAsync(dst, static_cast<size_t>(n) * 4, src, static_cast<size_t>(npad) * 4,
+                              static_cast<size_t>(n) * 4, rows, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "result rows");
+    }
+    return PSD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1009,6 +1209,7 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
 
 void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
+    free_peerpath(h);
     free_rowpanel(h);
     free_hostpipe(h);
     free_graphs(h);
@@ -1228,6 +1429,62 @@ psd_status_t psd_project_rowpanel(psd_filter_t h, const float* X_rows, int64_t n
 psd_status_t psd_project_rowpanel_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
                                           int want_sign, void* stream) {
     return run_rowpanel(h, X, n, 0, nranks, out, want_sign != 0, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_rowpanel_p2p_region(psd_filter_t h, int64_t n, int nranks, int rank, char handle[64]) {
+    if (!h || !handle) return fail(PSD_EINVAL, "null handle / IPC handle buffer");
+    psd_status_t rc = peer_layout(h, static_cast<int>(n), nranks, rank, false);
+    if (rc != PSD_OK) return rc;
+    if ((rc = peer_alloc_local(h, rank)) != PSD_OK) return rc;
+    cudaIpcMemHandle_t ih;
+    cudaError_t e = cudaIpcGetMemHandle(&ih, h->pp.base[rank]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(handle, &ih, 64);
+    return PSD_OK;
+}
+
+psd_status_t psd_rowpanel_p2p_attach(psd_filter_t h, const char* handles) {
+    if (!h || !handles) return fail(PSD_EINVAL, "null handle / handles");
+    auto& pp = h->pp;
+    if (pp.base.empty() || pp.is_virtual || !pp.base[pp.rank]) return fail(PSD_EINVAL, "psd_rowpanel_p2p_region first");
+    if (pp.attached) return PSD_OK;
+    for (int q = 0; q < pp.nranks; ++q) {
+        if (q == pp.rank) continue;
+        cudaIpcMemHandle_t ih;
+        std::memcpy(&ih, handles + 64 * q, 64);
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        pp.base[q] = static_cast<uint8_t*>(p);
+        pp.ipc_opened[q] = 1;
+    }
+    return peer_finish(h);
+}
+
+psd_status_t psd_project_rowpanel_p2p(psd_filter_t h, const float* X_rows, int64_t n, int rank, int nranks,
+                                      float* out_rows, int want_sign, void* stream) {
+    if (!h || !X_rows || !out_rows) return fail(PSD_EINVAL, "null handle / X / out");
+    if (h->pp.is_virtual || h->pp.n != n || h->pp.nranks != nranks || h->pp.rank != rank)
+        return fail(PSD_EINVAL, "peer row panels: (n, nranks, rank) differ from psd_rowpanel_p2p_region");
+    return run_rowpanel_p2p(h, X_rows, out_rows, want_sign != 0, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_project_rowpanel_p2p_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
+                                              int want_sign, void* stream) {
+    if (!h || !X || !out) return fail(PSD_EINVAL, "null handle / X / out");
+    auto& pp = h->pp;
+    if (!(pp.is_virtual && pp.attached && pp.n == n && pp.nranks == nranks && pp.op == op_of(h->prec))) {
+        psd_status_t rc = peer_layout(h, static_cast<int>(n), nranks, 0, true);
+        if (rc != PSD_OK) return rc;
+        for (int q = 0; q < nranks; ++q)
+            if ((rc = peer_alloc_local(h, q)) != PSD_OK) return rc;
+        if ((rc = peer_finish(h)) != PSD_OK) return rc;
+    }
+    return run_rowpanel_p2p(h, X, out, want_sign != 0, static_cast<cudaStream_t>(stream));
+}
+
+void psd_rowpanel_p2p_release(psd_filter_t h) {
+    if (h) free_peerpath(h);
 }
 
 int psd_rowpanel_tiles(int64_t n, int nranks, int rank, uint32_t* codes, int cap) {

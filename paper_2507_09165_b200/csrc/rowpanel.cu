@@ -67,7 +67,46 @@ unpack_tiles_kernel(const E* __restrict__ packed, const uint32_t* __restrict__ c
     }
 }
 
+__global__ void peer_signal_kernel(unsigned long long* const* __restrict__ flags, int nranks, int rank,
+                                   unsigned long long epoch) {
+    // every store of this rank's previous kernels (the product epilogue's peer stores) is ordered
+    // before the flag by the system-scope fence; the flag store itself is a release
+    __threadfence_system();
+    const int p = threadIdx.x;
+    if (p < nranks)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(flags[p] + rank), "l"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(const unsigned long long* __restrict__ my_flags, int nranks, unsigned long long epoch) {
+    const int p = threadIdx.x;
+    if (p < nranks) {
+        unsigned long long t0, t, v;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + p) : "memory");
+            if (v >= epoch) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000ull) __trap();      // a peer never arrived: fail, never hang the GPU
+        }
+    }
+    __syncthreads();
+    // the next kernels read the peers' stores through TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 }  // namespace
+
+cudaError_t launch_peer_signal(unsigned long long* const* flags_dev, int nranks, int rank, unsigned long long epoch,
+                               cudaStream_t stream) {
+    peer_signal_kernel<<<1, 32, 0, stream>>>(flags_dev, nranks, rank, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, unsigned long long epoch,
+                             cudaStream_t stream) {
+    peer_wait_kernel<<<1, 32, 0, stream>>>(my_flags, nranks, epoch);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
                                 int64_t ld, cudaStream_t stream) {

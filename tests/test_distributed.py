@@ -169,3 +169,96 @@ def test_rowpanel_nccl_world1():
         assert np.linalg.norm(out - ref[r0:r0 + rows]) / np.linalg.norm(ref) < 5e-3
     finally:
         tdist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- peer-memory row panels
+
+def _handles_worker(rank, world, port, q):
+    import torch.distributed as tdist
+    from paper_2507_09165_b200 import dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes([rank]) * 64
+        got = dist.exchange_ipc_handles(mine)
+        q.put((rank, got == [bytes([r]) * 64 for r in range(world)]))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_ipc_handle_exchange_gloo_world2():
+    """Setup of the peer-memory path: every rank receives all ranks' 64-byte IPC handles in rank
+    order (the bytes psd_rowpanel_p2p_attach consumes), over a gloo world-2 process group."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,P,prec", [(512, 2, "fp16"), (768, 3, "fp16"), (1024, 4, "tf32"), (2048, 8, "fp16"),
+                                      (1024, 1, "bf16")])
+def test_rowpanel_p2p_virtual_parity(n, P, prec):
+    """Peer-memory row panels (each product kernel stores its tiles into every rank's region,
+    epoch barrier between products) with P virtual ranks on one GPU: vs the oracle, exactly
+    symmetric, and bit-identical to the NCCL row-panel path (same tiles, same kernel)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2507_09165_b200 as pkg
+    X = synth.goe(n, synth.SEED_BASE + n + P)
+    f = pkg.Filter(pkg.filters.half_filter(), precision=prec)
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    P_gpu = f.project_rowpanel_p2p_virtual(Xd, P).double().cpu().numpy()
+    assert f.status() == "PSD_OK"
+    lam = chain.frobenius_bound(X)
+    ref, _ = chain.project(X, tables.F_HALF_REFINED, tables.half_kappas(7), lam=lam)
+    tol = {"fp16": 5e-3, "tf32": 5e-3, "bf16": 3e-2}[prec]
+    assert np.linalg.norm(P_gpu - ref) / np.linalg.norm(ref) <= tol
+    assert np.array_equal(P_gpu, P_gpu.T)
+    P_nccl = f.project_rowpanel_virtual(Xd, P).double().cpu().numpy()
+    assert np.array_equal(P_gpu, P_nccl)
+    S = f.project_rowpanel_p2p_virtual(Xd, P, sign=True).double().cpu().numpy()
+    refS, _ = chain.sign(X, tables.F_HALF_REFINED, tables.half_kappas(7), lam=lam)
+    assert np.linalg.norm(S - refS) / np.linalg.norm(refS) <= tol
+    # repeated calls: the epoch counters keep growing, results stay identical
+    again = f.project_rowpanel_p2p_virtual(Xd, P).double().cpu().numpy()
+    assert np.array_equal(again, P_gpu)
+
+
+@pytest.mark.gpu
+def test_rowpanel_p2p_world1():
+    """The real peer-memory code path (region + IPC handle, attach, system-scope epoch barrier
+    kernels, owner-row fp32 stores) with a world-size-1 process group on this GPU, vs the oracle."""
+    torch = pytest.importorskip("torch")
+    import torch.distributed as tdist
+    import paper_2507_09165_b200 as pkg
+    from paper_2507_09165_b200 import dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    tdist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        n = 1024
+        X = synth.goe(n, 78)
+        f = pkg.Filter(pkg.filters.half_filter())
+        rp = dist.PeerRowPanelProjector(f, n)
+        r0, rows = rp.row_range()
+        Xd = torch.tensor(X[r0:r0 + rows], dtype=torch.float32, device="cuda").contiguous()
+        out = rp.project(Xd).double().cpu().numpy()
+        out2 = rp.project(Xd).double().cpu().numpy()
+        torch.cuda.synchronize()
+        rp.close()
+        lam = chain.frobenius_bound(X)
+        ref, _ = chain.project(X, tables.F_HALF_REFINED, tables.half_kappas(7), lam=lam)
+        assert np.linalg.norm(out - ref[r0:r0 + rows]) / np.linalg.norm(ref) < 5e-3
+        assert np.array_equal(out, out2)
+    finally:
+        tdist.destroy_process_group()
