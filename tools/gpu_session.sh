@@ -11,6 +11,9 @@ fi
 if [[ $WHAT == all || $WHAT == bench ]]; then
   timeout 900 python bench.py "$@" > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 fi
+if [[ $WHAT == all || $WHAT == bench ]]; then
+  timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $OUT/launches.csv \
       python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline "$@" > $OUT/ncu_bench.txt 2>&1
