@@ -72,6 +72,24 @@ def structured_project(blocks, stages, kappas, lam):
     return hadamard_conjugate(blockdiag(pb))
 
 
+def structured_project_rows(blocks, stages, kappas, lam, rows):
+    """Rows `rows` of P(H B H^T) = H P(B) H^T without forming the n x n matrix: row i is
+    (H e_i)^T P(B) H (H symmetric), i.e. the Hadamard transform of h_i^T blockdiag(P(B)) with
+    h_i = H e_i -- O(n log n) per row (for the n = 16384 checks)."""
+    pb = [chain.project(b, stages, kappas, lam=lam)[0] for b in blocks]
+    n = sum(b.shape[0] for b in blocks)
+    E = np.zeros((len(rows), n))
+    E[np.arange(len(rows)), list(rows)] = 1.0
+    Hr = fwht_rows(E)                               # rows of H (H = H^T)
+    U = np.empty_like(Hr)
+    i = 0
+    for b in pb:
+        k = b.shape[0]
+        U[:, i:i + k] = Hr[:, i:i + k] @ b
+        i += k
+    return fwht_rows(U)
+
+
 def structured_sign(blocks, stages, kappas, lam):
     sb = [chain.sign(b, stages, kappas, lam=lam)[0] for b in blocks]
     return hadamard_conjugate(blockdiag(sb))

@@ -411,3 +411,35 @@ def test_chain_kernel_parity(pkg, n, batch, which, prec, cs):
     assert np.array_equal(lam, lam2)
     for b in range(batch):
         assert _rel(P[b], P2[b]) <= 1e-6, (b, _rel(P[b], P2[b]))
+
+
+@pytest.mark.parametrize("mode", ["single_gpu", "p2p_virtual_8"])
+def test_c5_full_size_structured(pkg, mode):
+    """Config c5 at its full size (one n = 16384 matrix, fp16, f~*_half+kappa): on one GPU through
+    the CTA-pair kernel, and in the launch configuration of the 8-GPU bench -- 8 row-panel ranks of
+    the peer-memory path, all regions on this GPU.  Sampled rows vs the exact structured oracle
+    P(H B H^T) = H P(B) H^T (oracle/spectral.py, row-sampled form); output exactly symmetric on a
+    sampled block."""
+    import gc
+    n = 16384
+    X, blocks = synth.structured(n, synth.SEED_BASE + 16384, block=64, family="goe")
+    lam = chain.frobenius_bound(X)
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    del X
+    gc.collect()
+    f = pkg.Filter(_product_filter("half", pkg), precision="fp16")
+    if mode == "single_gpu":
+        lam_d = torch.zeros(1, dtype=torch.float64, device="cuda")
+        P = f.project(Xd[None], lambda_out=lam_d)[0]
+        torch.cuda.synchronize()
+        assert abs(float(lam_d[0]) - lam) <= 1e-9 * lam
+    else:
+        P = f.project_rowpanel_p2p_virtual(Xd, 8)
+        torch.cuda.synchronize()
+    assert f.status() == "PSD_OK"
+    rows = [0, 1, 2047, 2048, 5000, 8191, 12345, 16383]
+    Pr = P[rows].double().cpu().numpy()
+    ref = spectral.structured_project_rows(blocks, *HALF, lam, rows)
+    assert _rel(Pr, ref) <= TOL["fp16"], _rel(Pr, ref)
+    blk = P[8000:8200, 3000:3200].cpu().numpy()
+    assert np.array_equal(blk, P[3000:3200, 8000:8200].cpu().numpy().T)

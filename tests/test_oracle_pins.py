@@ -232,6 +232,11 @@ def test_structured_oracle_matches_dense():
     assert np.linalg.norm(P - Ps) / np.linalg.norm(P) < 1e-6      # fp32 rounding of X only
     H = spectral.hadamard_conjugate(np.eye(8))
     assert np.allclose(H @ H, np.eye(8), atol=1e-15) and np.allclose(H, H.T)
+    # the row-sampled form (used at n = 16384) against the dense conjugation and Algorithm 2 itself
+    rows = [0, 1, 77, 128, 255]
+    Pr = spectral.structured_project_rows(blocks, st, k, lam, rows)
+    assert np.allclose(Pr, Ps[rows], atol=1e-13 * np.abs(Ps).max())
+    assert np.linalg.norm(P[rows] - Pr) / np.linalg.norm(P[rows]) < 1e-6
 
 
 def test_bound_is_upper_bound():
