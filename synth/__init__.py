@@ -111,6 +111,35 @@ def maxcut_admm(n, seed, avg_degree=8, rank=None):
     return _f32(C), _f32(0.5 * (Xk + Xk.T)), _f32(y)
 
 
+def structured_torch(n, seed, block=64, family="goe", device="cuda"):
+    """``structured`` computed with torch on `device` (same blocks, same butterflies in the same
+    order in float64, so the same fp32 values) -- for n = 16384, where the numpy transform takes
+    minutes.  Returns (X as an fp32 torch tensor on `device`, blocks)."""
+    import torch
+    assert n & (n - 1) == 0 and n % block == 0
+    blocks = [make(family, block, seed + 31 * k) for k in range(n // block)]
+    B = torch.zeros((n, n), dtype=torch.float64, device=device)
+    for k, b in enumerate(blocks):
+        B[k * block:(k + 1) * block, k * block:(k + 1) * block] = torch.from_numpy(b)
+
+    def fwht_rows(A):
+        h = 1
+        while h < n:
+            A = A.reshape(n, n // (2 * h), 2, h)
+            a0 = A[:, :, 0, :].clone()
+            a1 = A[:, :, 1, :]
+            A[:, :, 0, :] = a0 + a1
+            A[:, :, 1, :] = a0 - a1
+            A = A.reshape(n, n)
+            h *= 2
+        return A / np.sqrt(n)
+
+    X = fwht_rows(fwht_rows(B).T.contiguous()).T.contiguous()
+    del B
+    X = (0.5 * (X + X.T)).to(torch.float32)
+    return X, blocks
+
+
 FAMILIES = {"goe": goe, "haar": haar, "sdp_shaped": sdp_shaped, "dominant": dominant}
 
 

@@ -413,20 +413,24 @@ def test_chain_kernel_parity(pkg, n, batch, which, prec, cs):
         assert _rel(P[b], P2[b]) <= 1e-6, (b, _rel(P[b], P2[b]))
 
 
+@pytest.fixture(scope="module")
+def c5_input(pkg):
+    """One n = 16384 structured input on the GPU (synth.structured_torch), its blocks and the
+    oracle's Frobenius bound, shared by the c5 full-size tests."""
+    n = 16384
+    Xd, blocks = synth.structured_torch(n, synth.SEED_BASE + 16384, block=64, family="goe")
+    lam = chain.frobenius_bound(Xd.cpu().numpy())
+    return Xd, blocks, lam
+
+
 @pytest.mark.parametrize("mode", ["single_gpu", "p2p_virtual_8"])
-def test_c5_full_size_structured(pkg, mode):
+def test_c5_full_size_structured(pkg, c5_input, mode):
     """Config c5 at its full size (one n = 16384 matrix, fp16, f~*_half+kappa): on one GPU through
     the CTA-pair kernel, and in the launch configuration of the 8-GPU bench -- 8 row-panel ranks of
     the peer-memory path, all regions on this GPU.  Sampled rows vs the exact structured oracle
     P(H B H^T) = H P(B) H^T (oracle/spectral.py, row-sampled form); output exactly symmetric on a
     sampled block."""
-    import gc
-    n = 16384
-    X, blocks = synth.structured(n, synth.SEED_BASE + 16384, block=64, family="goe")
-    lam = chain.frobenius_bound(X)
-    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
-    del X
-    gc.collect()
+    Xd, blocks, lam = c5_input
     f = pkg.Filter(_product_filter("half", pkg), precision="fp16")
     if mode == "single_gpu":
         lam_d = torch.zeros(1, dtype=torch.float64, device="cuda")

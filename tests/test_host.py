@@ -123,3 +123,15 @@ def test_c2_coefficients_are_remez_output():
     from paper_2507_09165_b200 import filters
     st, _ = remez.sequential_remez(1e-3, [7] * 4)
     assert np.allclose(np.array(filters.c2_filter()), np.array(st), rtol=1e-12, atol=0)
+
+
+def test_structured_torch_generator_matches_numpy():
+    """synth.structured_torch (the n = 16384 input generator) gives the same fp32 values as
+    synth.structured (same blocks, same butterflies)."""
+    import numpy as np
+    import synth
+    torch = pytest.importorskip("torch")
+    X, blocks = synth.structured(512, 9, block=64, family="sdp_shaped")
+    Xt, blocks2 = synth.structured_torch(512, 9, block=64, family="sdp_shaped", device="cpu")
+    assert np.array_equal(X, Xt.double().numpy())
+    assert all(np.array_equal(a, b) for a, b in zip(blocks, blocks2))
