@@ -161,6 +161,21 @@ def test_zero_nan_and_upper_triangle(pkg):
     assert np.array_equal(Pl, P)
 
 
+@pytest.mark.parametrize("n,batch,prec", [(60, 3, "fp16x3"), (300, 2, "fp16"), (1024, 8, "fp16"), (640, 2, "tf32")])
+def test_lower_triangle_never_read(pkg, n, batch, prec):
+    """Reading R10 on every kernel path: NaN / Inf below the diagonal changes nothing, bitwise
+    (the host pipeline relies on it: it copies only the upper panels host-to-device)."""
+    X = synth.batch("goe", n, batch, synth.SEED_BASE + 21 * n)
+    P, lam, f = _gpu(pkg, _product_filter("half", pkg), X, prec)
+    Xg = X.copy()
+    il = np.tril_indices(n, -1)
+    for b in range(batch):
+        Xg[b][il] = np.where(np.arange(il[0].size) % 2, np.nan, np.inf)
+    Pg, lamg, fg = _gpu(pkg, _product_filter("half", pkg), Xg, prec)
+    assert fg.status() == "PSD_OK" and np.array_equal(lam, lamg)
+    assert np.array_equal(P, Pg)
+
+
 def test_psd_and_exact_projection_accuracy(pkg):
     """Method accuracy vs the exact Pi(X) (Higham) at n=512 fp16 is at the
     level the paper reports for FP16 (~1e-3, Table 3) on GOE."""
