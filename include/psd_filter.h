@@ -165,6 +165,17 @@ psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t b
 psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, const float* y, double sigma,
                              int64_t n, int64_t batch, float* S_out, float* X_out, void* stream);
 
+/* The filter's certificate, computed on the device over EVERY float32 in [0, 1] (s is odd, so
+ * [-1, 1] reduces to [0, 1]), in fp64, for the chain s = f_T o ... o f_1 this handle holds:
+ *   relu_err = max 1/2 x |1 - s(x)|   (Eq. comp:error-approx; the paper prints
+ *              2 x relu_err under Tables 1-2, reading R3),
+ *   sign_err = max over x in [eps, 1] of |s(x) - 1|   (Eq. comp:minimax-sign; eps of
+ *              psd_filter_create -- its only use, reading R15),
+ * and the maximising x of each (ties: the smaller x).  Any pointer may be NULL.  Synchronous
+ * (about 2 x 1.07e9 chain evaluations, a few ms); deterministic. */
+psd_status_t psd_filter_certificate(psd_filter_t h, double* sign_err, double* relu_err, double* sign_argmax,
+                                    double* relu_argmax);
+
 /* Synchronises `stream`, then returns and clears the handle's device status word:
  * PSD_OK or PSD_ENONFINITE (some input had a non-finite entry). */
 psd_status_t psd_status(psd_filter_t h, void* stream);

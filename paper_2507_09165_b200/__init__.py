@@ -140,6 +140,13 @@ class Filter:
                                         _stream_ptr(stream)), "psd_admm_update")
         return S_out, X_out
 
+    def certificate(self):
+        """{'relu_err', 'relu_argmax', 'sign_err', 'sign_argmax'}: the scalar worst cases of this
+        chain over every float32 in [0, 1], computed on the device (psd_filter_certificate)."""
+        v = [ctypes.c_double() for _ in range(4)]
+        check(self._lib.psd_filter_certificate(self._h, *(ctypes.byref(x) for x in v)), "psd_filter_certificate")
+        return {"sign_err": v[0].value, "relu_err": v[1].value, "sign_argmax": v[2].value, "relu_argmax": v[3].value}
+
     def status(self, stream=None):
         """Synchronise and return 'PSD_OK' or 'PSD_ENONFINITE' (device numeric status)."""
         from ._lib import STATUS_NAMES

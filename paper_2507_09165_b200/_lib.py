@@ -33,6 +33,8 @@ SIGNATURES = [
                                   _c.c_void_p, _c.c_int, _c.c_void_p]),
     ("psd_admm_update", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_double, _c.c_int64,
                                    _c.c_int64, _c.c_void_p, _c.c_void_p, _c.c_void_p]),
+    ("psd_filter_certificate", _c.c_int, [_c.c_void_p, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double),
+                                          _c.POINTER(_c.c_double), _c.POINTER(_c.c_double)]),
     ("psd_status", _c.c_int, [_c.c_void_p, _c.c_void_p]),
     ("psd_workspace_bytes", _c.c_int64, [_c.c_void_p, _c.c_int64, _c.c_int64]),
     ("psd_profile", _c.c_int, [_c.c_void_p, _c.c_int]),

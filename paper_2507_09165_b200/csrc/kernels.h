@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <vector>
 
 namespace psd {
 
@@ -146,6 +147,11 @@ struct SmallPlan {
 int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U
 cudaError_t launch_small_batch(bool split, const float* X, float* out, int n, int batch, double* lambda_out,
                                unsigned* status, const SmallPlan& plan, cudaStream_t stream);
+
+// The filter's scalar worst-case errors over every float32 in [0, 1] (certificate.cu): relu_err =
+// max 1/2 x |1 - s(x)|, sign_err = max over x >= eps of |s(x) - 1| (synchronous, fp64).
+cudaError_t certify_chain(const std::vector<std::vector<double>>& coeffs, double eps, double* relu_err,
+                          double* relu_argmax, double* sign_err, double* sign_argmax);
 
 // Row-panel multi-GPU path (rowpanel.cu).
 cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,

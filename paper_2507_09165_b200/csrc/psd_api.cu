@@ -1293,6 +1293,14 @@ psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, co
     return run_body(h, C, n, batch, S_out, nullptr, nullptr, false, static_cast<cudaStream_t>(stream), &a);
 }
 
+psd_status_t psd_filter_certificate(psd_filter_t h, double* sign_err, double* relu_err, double* sign_argmax,
+                                    double* relu_argmax) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    cudaError_t e = certify_chain(h->coeffs, h->eps, relu_err, relu_argmax, sign_err, sign_argmax);
+    if (e != cudaSuccess) return cuda_fail(e, "certificate");
+    return PSD_OK;
+}
+
 psd_status_t psd_status(psd_filter_t h, void* stream) {
     if (!h) return fail(PSD_EINVAL, "null handle");
     if (!h->ws.status) return PSD_OK;

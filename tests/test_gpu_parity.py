@@ -462,3 +462,18 @@ def test_c5_full_size_structured(pkg, c5_input, mode):
     assert _rel(Pr, ref) <= TOL["fp16"], _rel(Pr, ref)
     blk = P[8000:8200, 3000:3200].cpu().numpy()
     assert np.array_equal(blk, P[3000:3200, 8000:8200].cpu().numpy().T)
+
+
+@pytest.mark.parametrize("which", ["half", "single", "c2", "c3"])
+def test_certificate_on_device(pkg, which):
+    """psd_filter_certificate (every float32 in [0, 1] on the device, fp64, the folded chain the
+    handle holds) vs the oracle's C certificate (raw tables, literal kappa; oracle/certify.c)."""
+    from oracle import certify
+    st, kap = _oracle_filter(which)
+    f = pkg.Filter(_product_filter(which, pkg), eps=1e-3)
+    c = f.certificate()
+    e, am, _ = certify.relu_err(st, kap)
+    s, sam = certify.sign_err(st, 1e-3, kap)
+    assert abs(c["relu_err"] - e) <= 1e-9 * e, (c["relu_err"], e)
+    assert abs(c["sign_err"] - s) <= 1e-9 * s, (c["sign_err"], s)
+    assert 0.0 < c["relu_argmax"] <= 1.0 and 1e-3 <= c["sign_argmax"] <= 1.0
