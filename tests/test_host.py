@@ -135,3 +135,31 @@ def test_structured_torch_generator_matches_numpy():
     Xt, blocks2 = synth.structured_torch(512, 9, block=64, family="sdp_shaped", device="cpu")
     assert np.array_equal(X, Xt.double().numpy())
     assert all(np.array_equal(a, b) for a, b in zip(blocks, blocks2))
+
+
+def test_admm_and_peer_arguments_rejected_before_any_device_work(lib):
+    """psd_admm_update and the peer-memory row-panel setup validate their arguments on the host
+    (no GPU needed): bad sigma, aliasing, misalignment, unsupported shapes -> PSD_EINVAL /
+    PSD_EUNSUPPORTED with a message."""
+    from paper_2507_09165_b200 import filters
+    rc, h = _create(lib, filters.half_filter())
+    assert rc == 0
+    fake = ctypes.c_void_p(0x10000)                      # 16-byte aligned, never dereferenced
+    other = ctypes.c_void_p(0x20000)
+    assert lib.psd_admm_update(h, fake, fake, None, -1.0, 64, 1, fake, other, None) == 1
+    assert b"sigma" in lib.psd_last_error()
+    assert lib.psd_admm_update(h, fake, fake, None, float("inf"), 64, 1, fake, other, None) == 1
+    assert lib.psd_admm_update(h, fake, fake, None, 1.0, 64, 1, other, other, None) == 1      # S_out == X_out
+    assert lib.psd_admm_update(h, fake, None, None, 1.0, 64, 1, fake, other, None) == 1       # null X_k
+    assert lib.psd_admm_update(h, fake, ctypes.c_void_p(0x10004), None, 1.0, 64, 1, fake, other, None) == 1
+    hb = ctypes.create_string_buffer(64)
+    assert lib.psd_rowpanel_p2p_region(h, 1000, 3, 0, hb) == 1                 # n % nranks
+    assert lib.psd_rowpanel_p2p_region(h, 1024, 16, 0, hb) == 1                # more than 8 ranks
+    assert lib.psd_rowpanel_p2p_region(h, 1040, 2, 0, hb) == 1                 # rows per rank % 32
+    assert lib.psd_rowpanel_p2p_region(h, 1024, 2, 2, hb) == 1                 # rank out of range
+    assert lib.psd_rowpanel_p2p_attach(h, b"\0" * 128) == 1                    # no region yet
+    assert lib.psd_project_rowpanel_p2p(h, fake, 1024, 0, 2, fake, 0, None) == 1
+    assert lib.psd_filter_set_precision(h, 4) == 0                             # FP16X3
+    assert lib.psd_rowpanel_p2p_region(h, 1024, 2, 0, hb) == 6                 # split: unsupported
+    lib.psd_rowpanel_p2p_release(h)
+    lib.psd_filter_destroy(h)
