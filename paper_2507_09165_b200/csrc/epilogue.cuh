@@ -93,7 +93,7 @@ __device__ __forceinline__ void stage_op_cols(const float (&v)[32], uint8_t* wsm
 // (gj0.., gi0..) unless it is a (symmetrised) diagonal block -- both through the coalesced drain.
 template <OpType T>
 __device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int npad, int gi0, int gj0, bool diag32,
-                                               const float (&v)[32], uint8_t* wsmem) {
+                                               const float (&v)[32], uint8_t* wsmem, bool mirror = true) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     op_t* out_op = reinterpret_cast<op_t*>(out);
@@ -104,7 +104,7 @@ __device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int np
     drain_staged_block<Tr::kBytes>(wsmem, kStride, [&](int r) {
         return out_op + opBase + static_cast<int64_t>(gi0 + r) * npad + gj0;
     });
-    if (!diag32) {
+    if (!diag32 && mirror) {
         __syncwarp();
         stage_op_cols<T>(v, wsmem, kStride);
         __syncwarp();
@@ -317,7 +317,7 @@ __device__ __forceinline__ void prefetch_addend_l2(const EpiParams& e, int b, in
 
 template <OpType T, bool kCg = false>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, int b, int npad, int gi0, int gj0,
-                                               bool /*tile_diag*/, const uint32_t (&raw)[32], uint8_t* wsmem,
+                                               bool tile_diag, const uint32_t (&raw)[32], uint8_t* wsmem,
                                                int64_t packed_off = -1, const uint4* pre = nullptr) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
@@ -447,7 +447,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         if (e.npeers > 0)
             store_op_block_peers<T>(e.out_peers, e.npeers, opBase, npad, gi0, gj0, diag32, w, wsmem);
         else
-            store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem);
+            store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem, !(e.upper_only && !tile_diag));
     }
 
     if (e.peer_rows > 0) {

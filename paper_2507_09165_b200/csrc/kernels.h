@@ -43,6 +43,7 @@ struct EpiParams {
     // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
     unsigned long long* dbg;
     int dbg_nostore;          // debug experiment (PSD_DEBUG_NOSTORE): skip the epilogue's stores
+    int upper_only;           // store off-diagonal tiles of the operand copy without their mirror
     // Peer-memory row-panel mode (the product and its all-gather in one kernel): the operand copy
     // goes to out_peers[0..npeers) -- the same buffer of every rank, mapped into this process --
     // and fp32 output row r to outF_peers[r / peer_rows] (its owner rank's buffer, ld ldF).
@@ -74,6 +75,11 @@ struct GemmShape {
     const uint32_t* tiles;    // CTA-pair kernel: upper-tile visiting order, (I << 16) | J, one matrix
     int tiles_per_matrix;     // = nt (nt + 1) / 2 for nt = npad / 256
     int* counter;             // CTA-pair kernel: zeroed global tile counter (dynamic scheduler)
+    // CTA-pair kernel, 16-bit single pass: the operands hold only their upper 256-tiles (+ the full
+    // diagonal tiles); the part of a row panel left of its diagonal tile is loaded transposed
+    // (MN-major) from the stored upper tile, and the epilogue skips the mirrored stores of
+    // off-diagonal tiles (half the operand stores and DRAM writes)
+    int upper_only;
 };
 
 // Visiting order of the upper 256-tiles of one matrix (host side), by name:
@@ -89,6 +95,8 @@ int sym_gemm_bn(int npad, int batch);
 // low parts (A*B ~= Ahi Bhi + Ahi Blo + Alo Bhi, three tcgen05.mma passes, one accumulator).
 struct OperandMaps {
     CUtensorMap a, b, a_lo, b_lo;
+    // 64 x 64 boxes of A and B: the transposed (MN-major) loads of the upper-only storage mode
+    CUtensorMap a_t, b_t;
 };
 
 // C = alpha*(A B) + beta*D on the upper tiles.

@@ -161,6 +161,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128_kmajor(uint32_t smem_addr) {
     d |= static_cast<uint64_t>(2) << 61;
     return d;
 }
+// MN-major operand, 128B-swizzled: each 128-byte row holds 64 MN-contiguous 16-bit elements of
+// one K index; 8 rows form a 1 KB swizzle atom (SBO = stride between 8-row K groups) and the
+// 64-element MN chunks sit LBO bytes apart (two TMA boxes of 64 x 64).  Verified on the GPU by
+// tools/micro/mn_major.cu (LBO 8192, SBO 1024 exact).
+__device__ __forceinline__ uint64_t smem_desc_sw128_mnmajor(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
 // Instruction descriptor, kind::f16 / kind::tf32, dense, fp32 accumulator, both K-major:
 //   [4,6) D format (1 = f32)   [7,10) A format   [10,13) B format (f16 0, bf16 1, tf32 2)
 //   [15] A major (0 = K)   [16] B major   [17,23) N >> 3   [24,29) M >> 4

@@ -152,8 +152,24 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     uint8_t* sa = ring + st * kStageBytes;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
-                    ptx::tma_load_2d_pair_nohint(sa, &tm.a, full_leader, kb * kBK, rowA);
-                    ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b, full_leader, kb * kBK, rowB);
+                    const int k0 = kb * kBK;
+                    if (!kSplit && Tr::kBytes == 2 && s.upper_only && k0 < I * kT2) {
+                        // left of row block I's diagonal tile: A[rows, k0..] = (stored tile rows k0.., cols
+                        // of this CTA's rows)^T, two 64x64 boxes -> MN-major operand
+                        const int x = I * kT2 + static_cast<int>(rank) * kRowsPerCta;
+                        ptx::tma_load_2d_pair_nohint(sa, &tm.a_t, full_leader, x, b * s.npad + k0);
+                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1 / 2, &tm.a_t, full_leader, x + 64, b * s.npad + k0);
+                    } else {
+                        ptx::tma_load_2d_pair_nohint(sa, &tm.a, full_leader, k0, rowA);
+                    }
+                    if (!kSplit && Tr::kBytes == 2 && s.upper_only && k0 < J * kT2) {
+                        const int x = J * kT2 + static_cast<int>(rank) * kRowsPerCta;
+                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b_t, full_leader, x, b * s.npad + k0);
+                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1 + kTileBytes1 / 2, &tm.b_t, full_leader, x + 64,
+                                                     b * s.npad + k0);
+                    } else {
+                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b, full_leader, k0, rowB);
+                    }
                     if constexpr (kSplit) {
                         ptx::tma_load_2d_pair_nohint(sa + 2 * kTileBytes1, &tm.a_lo, full_leader, kb * kBK, rowA);
                         ptx::tma_load_2d_pair_nohint(sa + 3 * kTileBytes1, &tm.b_lo, full_leader, kb * kBK, rowB);
@@ -181,6 +197,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                 release_tile(it);
                 if (e.dbg) { const unsigned long long c1 = clock64(); w_tile += c1 - c0; c0 = c1; }
                 if (t >= total_tiles) break;
+                int tb, tI, tJ;
+                decode_tile(t, s, tb, tI, tJ);
                 const int acc = it & 1;
                 const uint32_t acc_ph = (it >> 1) & 1;
                 ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
@@ -197,18 +215,27 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     }
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
-                    const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
-                    const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + kTileBytes1);
+                    // upper-only storage: operands left of their diagonal tile arrive transposed
+                    // (MN-major: 64-element MN chunks 8 KB apart = LBO, 8-row K groups 1 KB apart = SBO;
+                    // one K step of 16 = 2 KB); the instruction descriptor says which is which
+                    const bool a_mn = !kSplit && Tr::kBytes == 2 && s.upper_only && kb * kBK < tI * kT2;
+                    const bool b_mn = !kSplit && Tr::kBytes == 2 && s.upper_only && kb * kBK < tJ * kT2;
+                    const uint64_t adesc = a_mn ? ptx::smem_desc_sw128_mnmajor(sa, kTileBytes1 / 2, 1024)
+                                                : ptx::smem_desc_sw128_kmajor(sa);
+                    const uint64_t bdesc = b_mn ? ptx::smem_desc_sw128_mnmajor(sa + kTileBytes1, kTileBytes1 / 2, 1024)
+                                                : ptx::smem_desc_sw128_kmajor(sa + kTileBytes1);
+                    const uint32_t idesc = kIdesc | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
+                    const uint64_t astep = a_mn ? (2048 >> 4) : (32 >> 4), bstep = b_mn ? (2048 >> 4) : (32 >> 4);
                     auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
                         if constexpr (T == OpType::TF32)
                             ptx::mma_tf32_pair(d_tmem, a, bb, kIdesc, accumulate);
                         else
-                            ptx::mma_f16_pair(d_tmem, a, bb, kIdesc, accumulate);
+                            ptx::mma_f16_pair(d_tmem, a, bb, idesc, accumulate);
                     };
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k) {
                         const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
-                        mma(adesc + koff, bdesc + koff, (kb | k) != 0);
+                        mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
                         if constexpr (kSplit) {
                             const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes1);
                             const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes1);
