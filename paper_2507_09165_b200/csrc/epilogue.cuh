@@ -442,7 +442,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
                 lo[i] = w[i] - h;
                 w[i] = h;
             }
-            store_op_block<T>(e.out_lo, opBase, npad, gi0, gj0, diag32, lo, wsmem);
+            store_op_block<T>(e.out_lo, opBase, npad, gi0, gj0, diag32, lo, wsmem, !(e.upper_only && !tile_diag));
         }
         if (e.npeers > 0)
             store_op_block_peers<T>(e.out_peers, e.npeers, opBase, npad, gi0, gj0, diag32, w, wsmem);

@@ -75,7 +75,7 @@ struct GemmShape {
     const uint32_t* tiles;    // CTA-pair kernel: upper-tile visiting order, (I << 16) | J, one matrix
     int tiles_per_matrix;     // = nt (nt + 1) / 2 for nt = npad / 256
     int* counter;             // CTA-pair kernel: zeroed global tile counter (dynamic scheduler)
-    // CTA-pair kernel, 16-bit single pass: the operands hold only their upper 256-tiles (+ the full
+    // CTA-pair kernel, 16-bit operands: the operands hold only their upper 256-tiles (+ the full
     // diagonal tiles); the part of a row panel left of its diagonal tile is loaded transposed
     // (MN-major) from the stored upper tile, and the epilogue skips the mirrored stores of
     // off-diagonal tiles (half the operand stores and DRAM writes)
@@ -95,8 +95,9 @@ int sym_gemm_bn(int npad, int batch);
 // low parts (A*B ~= Ahi Bhi + Ahi Blo + Alo Bhi, three tcgen05.mma passes, one accumulator).
 struct OperandMaps {
     CUtensorMap a, b, a_lo, b_lo;
-    // 64 x 64 boxes of A and B: the transposed (MN-major) loads of the upper-only storage mode
-    CUtensorMap a_t, b_t;
+    // 64 x 64 boxes of A and B (and their low parts): the transposed (MN-major) loads of the
+    // upper-only storage mode
+    CUtensorMap a_t, b_t, a_lo_t, b_lo_t;
 };
 
 // C = alpha*(A B) + beta*D on the upper tiles.

@@ -551,6 +551,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         m.b_lo = bmaps[split ? B + B_COUNT : B];
         m.a_t = ws.tmap64[A];
         m.b_t = ws.tmap64[B];
+        m.a_lo_t = ws.tmap64[split ? A + B_COUNT : A];
+        m.b_lo_t = ws.tmap64[split ? B + B_COUNT : B];
         return m;
     };
     // (a2) scale + convert; the products-free sign chain finishes here
@@ -600,13 +602,13 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.nF = n;
         }
         ep.dbg_nostore = std::getenv("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug experiment
-        ep.upper_only = (npad % 256 == 0 && use_pair_kernel(n, batch) && !split && ws.op != OpType::TF32 &&
+        ep.upper_only = (npad % 256 == 0 && use_pair_kernel(n, batch) && ws.op != OpType::TF32 &&
                          std::getenv("PSD_NO_UPPER_ONLY") == nullptr) ? 1 : 0;
         return ep;
     };
     const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
-    // the chain's operand copies hold only their upper tiles (CTA-pair kernel, 16-bit single pass)
-    const bool upper_only = pair && !split && ws.op != OpType::TF32 && std::getenv("PSD_NO_UPPER_ONLY") == nullptr;
+    // the chain's operand copies hold only their upper tiles (CTA-pair kernel, 16-bit operands)
+    const bool upper_only = pair && ws.op != OpType::TF32 && std::getenv("PSD_NO_UPPER_ONLY") == nullptr;
     shape.upper_only = upper_only ? 1 : 0;
     const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
                              ? chain_cluster_size(ws.op, split, npad, batch)

@@ -153,26 +153,23 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
                     const int k0 = kb * kBK;
-                    if (!kSplit && Tr::kBytes == 2 && s.upper_only && k0 < I * kT2) {
-                        // left of row block I's diagonal tile: A[rows, k0..] = (stored tile rows k0.., cols
-                        // of this CTA's rows)^T, two 64x64 boxes -> MN-major operand
-                        const int x = I * kT2 + static_cast<int>(rank) * kRowsPerCta;
-                        ptx::tma_load_2d_pair_nohint(sa, &tm.a_t, full_leader, x, b * s.npad + k0);
-                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1 / 2, &tm.a_t, full_leader, x + 64, b * s.npad + k0);
-                    } else {
-                        ptx::tma_load_2d_pair_nohint(sa, &tm.a, full_leader, k0, rowA);
-                    }
-                    if (!kSplit && Tr::kBytes == 2 && s.upper_only && k0 < J * kT2) {
-                        const int x = J * kT2 + static_cast<int>(rank) * kRowsPerCta;
-                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b_t, full_leader, x, b * s.npad + k0);
-                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1 + kTileBytes1 / 2, &tm.b_t, full_leader, x + 64,
-                                                     b * s.npad + k0);
-                    } else {
-                        ptx::tma_load_2d_pair_nohint(sa + kTileBytes1, &tm.b, full_leader, k0, rowB);
-                    }
+                    // upper-only storage: left of block `blk`'s diagonal tile the panel is the stored
+                    // upper tile transposed -- two 64x64 boxes (rows k0.., this CTA's 128 columns) that
+                    // the MMA reads as an MN-major operand
+                    auto load = [&](uint8_t* dst, const CUtensorMap* mk, const CUtensorMap* mt, int blk, int row) {
+                        if (Tr::kBytes == 2 && s.upper_only && k0 < blk * kT2) {
+                            const int x = blk * kT2 + static_cast<int>(rank) * kRowsPerCta;
+                            ptx::tma_load_2d_pair_nohint(dst, mt, full_leader, x, b * s.npad + k0);
+                            ptx::tma_load_2d_pair_nohint(dst + kTileBytes1 / 2, mt, full_leader, x + 64, b * s.npad + k0);
+                        } else {
+                            ptx::tma_load_2d_pair_nohint(dst, mk, full_leader, k0, row);
+                        }
+                    };
+                    load(sa, &tm.a, &tm.a_t, I, rowA);
+                    load(sa + kTileBytes1, &tm.b, &tm.b_t, J, rowB);
                     if constexpr (kSplit) {
-                        ptx::tma_load_2d_pair_nohint(sa + 2 * kTileBytes1, &tm.a_lo, full_leader, kb * kBK, rowA);
-                        ptx::tma_load_2d_pair_nohint(sa + 3 * kTileBytes1, &tm.b_lo, full_leader, kb * kBK, rowB);
+                        load(sa + 2 * kTileBytes1, &tm.a_lo, &tm.a_lo_t, I, rowA);
+                        load(sa + 3 * kTileBytes1, &tm.b_lo, &tm.b_lo_t, J, rowB);
                     }
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
@@ -218,8 +215,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     // upper-only storage: operands left of their diagonal tile arrive transposed
                     // (MN-major: 64-element MN chunks 8 KB apart = LBO, 8-row K groups 1 KB apart = SBO;
                     // one K step of 16 = 2 KB); the instruction descriptor says which is which
-                    const bool a_mn = !kSplit && Tr::kBytes == 2 && s.upper_only && kb * kBK < tI * kT2;
-                    const bool b_mn = !kSplit && Tr::kBytes == 2 && s.upper_only && kb * kBK < tJ * kT2;
+                    const bool a_mn = Tr::kBytes == 2 && s.upper_only && kb * kBK < tI * kT2;
+                    const bool b_mn = Tr::kBytes == 2 && s.upper_only && kb * kBK < tJ * kT2;
                     const uint64_t adesc = a_mn ? ptx::smem_desc_sw128_mnmajor(sa, kTileBytes1 / 2, 1024)
                                                 : ptx::smem_desc_sw128_kmajor(sa);
                     const uint64_t bdesc = b_mn ? ptx::smem_desc_sw128_mnmajor(sa + kTileBytes1, kTileBytes1 / 2, 1024)
@@ -234,13 +231,14 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     };
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k) {
-                        const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
                         mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
                         if constexpr (kSplit) {
-                            const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes1);
-                            const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes1);
-                            mma(adesc + koff, blo + koff, 1u);        // A_hi B_lo
-                            mma(alo + koff, bdesc + koff, 1u);        // A_lo B_hi
+                            const uint64_t alo = a_mn ? ptx::smem_desc_sw128_mnmajor(sa + 2 * kTileBytes1, kTileBytes1 / 2, 1024)
+                                                      : ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes1);
+                            const uint64_t blo = b_mn ? ptx::smem_desc_sw128_mnmajor(sa + 3 * kTileBytes1, kTileBytes1 / 2, 1024)
+                                                      : ptx::smem_desc_sw128_kmajor(sa + 3 * kTileBytes1);
+                            mma(adesc + k * astep, blo + k * bstep, 1u);        // A_hi B_lo
+                            mma(alo + k * astep, bdesc + k * bstep, 1u);        // A_lo B_hi
                         }
                     }
                     ptx::mma_commit_pair(&empty[st], 0x3);

@@ -9,10 +9,11 @@ import bench
 import synth
 from paper_2507_09165_b200 import Filter, filters
 var = sys.argv[1]
+prec = sys.argv[2] if len(sys.argv) > 2 else "fp16"
 cfg = bench.CONFIGS["c4"]
 X = bench.make_inputs(cfg, 0, 32, synth.SEED_BASE).cuda()
 out = torch.empty_like(X)
-f = Filter(filters.half_filter())
+f = Filter(filters.half_filter(), precision=prec)
 for _ in range(3):
     f.project(X, out=out)
 torch.cuda.synchronize()
@@ -31,10 +32,10 @@ for rnd in range(3):
         a, b = torch.cuda.Event(True), torch.cuda.Event(True)
         with bench.ClockSampler(0) as clk:
             a.record()
-            for _ in range(10):
+            for _ in range(10 if prec == "fp16" else 3):
                 f.project(X, out=out)
             b.record(); torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / 10
+        ms = a.elapsed_time(b) / (10 if prec == "fp16" else 3)
         res[mode].append(ms)
         print(f"round {rnd} {var}={mode}: {ms:.2f} ms/step, clocks {clk.summary()['sm_mhz']}", flush=True)
 print({k: min(v) for k, v in res.items()})
