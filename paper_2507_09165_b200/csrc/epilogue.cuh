@@ -119,7 +119,8 @@ __device__ __forceinline__ void store_op_block(void* out, int64_t opBase, int np
 // (direct, then mirrored) and drained npeers times through the coalesced drain.
 template <OpType T>
 __device__ __forceinline__ void store_op_block_peers(void* const* dsts, int nd, int64_t opBase, int npad, int gi0,
-                                                     int gj0, bool diag32, const float (&v)[32], uint8_t* wsmem) {
+                                                     int gj0, bool diag32, const float (&v)[32], uint8_t* wsmem,
+                                                     bool mirror = true) {
     using Tr = OpTraits<T>;
     using op_t = typename Tr::type;
     constexpr int kStride = Tr::kBytes == 2 ? 80 : 144;
@@ -132,7 +133,7 @@ __device__ __forceinline__ void store_op_block_peers(void* const* dsts, int nd, 
             return base + opBase + static_cast<int64_t>(gi0 + r) * npad + gj0;
         });
     }
-    if (!diag32) {
+    if (!diag32 && mirror) {
         __syncwarp();
         stage_op_cols<T>(v, wsmem, kStride);
         __syncwarp();
@@ -445,7 +446,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             store_op_block<T>(e.out_lo, opBase, npad, gi0, gj0, diag32, lo, wsmem, !(e.upper_only && !tile_diag));
         }
         if (e.npeers > 0)
-            store_op_block_peers<T>(e.out_peers, e.npeers, opBase, npad, gi0, gj0, diag32, w, wsmem);
+            store_op_block_peers<T>(e.out_peers, e.npeers, opBase, npad, gi0, gj0, diag32, w, wsmem,
+                                    !(e.upper_only && !tile_diag));
         else
             store_op_block<T>(e.out_op, opBase, npad, gi0, gj0, diag32, w, wsmem, !(e.upper_only && !tile_diag));
     }

@@ -1041,9 +1041,10 @@ psd_status_t peer_alloc_local(psd_filter_s* h, int q) {
     if (cudaMalloc(&p, pp.region_bytes) != cudaSuccess) return fail(PSD_ENOMEM, "cudaMalloc peer region failed");
     cudaMemset(p, 0, pp.region_bytes);        // zero padding of every operand; zero flags
     pp.base[q] = static_cast<uint8_t*>(p);
-    std::vector<CUtensorMap> maps(B_COUNT);
+    std::vector<CUtensorMap> maps(2 * B_COUNT);     // 128-row boxes, then 64 x 64 (transposed loads)
     for (int i = 0; i < B_COUNT; ++i)
-        if (!make_operand_tmap(&maps[i], pp.base[q] + i * pp.op_bytes_buf, pp.op, pp.npad, 1))
+        if (!make_operand_tmap(&maps[i], pp.base[q] + i * pp.op_bytes_buf, pp.op, pp.npad, 1) ||
+            !make_operand_tmap(&maps[B_COUNT + i], pp.base[q] + i * pp.op_bytes_buf, pp.op, pp.npad, 1, 64))
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
     if (pp.tmaps.size() < static_cast<size_t>(pp.nranks)) pp.tmaps.resize(pp.nranks);
     pp.tmaps[q] = maps;
@@ -1157,8 +1158,14 @@ psd_status_t run_rowpanel_p2p(psd_filter_s* h, const float* X, float* out, bool 
             m.b = pp.tmaps[r][s.B];
             m.a_lo = m.a;
             m.b_lo = m.b;
+            m.a_t = m.a_lo_t = pp.tmaps[r][B_COUNT + s.A];
+            m.b_t = m.b_lo_t = pp.tmaps[r][B_COUNT + s.B];
             GemmShape shape{npad, 1, pp.codes + static_cast<size_t>(r) * pp.per, pp.counts[r],
                             ws.counters + si * P + r};
+            // upper-only operand storage: each tile goes to the peers without its mirror (half the
+            // NVLink bytes); the loader reads the left part of a panel transposed
+            shape.upper_only = (pp.op != OpType::TF32) ? 1 : 0;
+            ep.upper_only = shape.upper_only;
             e = launch_sym_gemm_2cta(pp.op, false, m, shape, ep, st);
             if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (peer row panel)");
             h->kernel_launches += 1;
