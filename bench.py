@@ -349,7 +349,13 @@ def run_ours(args, cfg):
                                                        if n <= 64 else "sym_gemm_kernel (1-CTA tcgen05 symmetric "
                                                                        "product, fused epilogue)")),
                          "per_launch_flops": per_launch, "mma_passes": passes,
-                         "avg_launch_ms": launch_ms, "peak_source": peak_note},
+                         "avg_launch_ms": launch_ms, "peak_source": peak_note,
+                         # context: the same achieved rate against the measured BURST bf16 figure
+                         # (a kernel timed alone) and the executed flops (diagonal 256-tiles are
+                         # computed whole: 136/128 of the triangle at n = 4096)
+                         "frac_of_burst": (achieved / (peaks.get("bf16_tflops", 1590.0) / passes *
+                                                       (1.0 if args.precision.startswith(("fp16", "bf16")) else 0.5)))
+                                          if achieved else None},
             "gpu_launches": kernel_launches,
             "clocks": clk.summary(),
         }
