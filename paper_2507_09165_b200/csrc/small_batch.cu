@@ -24,7 +24,7 @@ namespace {
 
 constexpr int kN = 64;                  // padded matrix edge
 constexpr int kSlotBytes = kN * 128;    // 64 rows x 128 B (fp16), one SW128 atom wide
-constexpr int kThreadsS = 128;
+constexpr int kThreadsS = 256;        // 8 warps: TMEM quadrant = warp & 3, column half = warp >> 2
 
 // byte offset of element (row, col) in a SW128 K-major 64x64 fp16 slot
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
@@ -39,7 +39,7 @@ struct SmallLayout {
     static constexpr int kY = kParts * kSlotBytes;
     static constexpr int kU = 2 * kParts * kSlotBytes;
     static constexpr int kPerMatrix = kU + 2 * kSlotBytes;
-    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 128;
+    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 256;   // + align slack, barrier, tmem slot, 2x8 partial sums
 };
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -47,14 +47,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 template <bool kSplit>
-__device__ __forceinline__ void store_row(uint8_t* slot, int row, const float (&v)[64], float s) {
-    // hi = rn(v s) [, lo = rn(v s - hi)] into the swizzled slot row
+__device__ __forceinline__ void store_row(uint8_t* slot, int row, int half, const float (&v)[32], float s) {
+    // hi = rn(v s) [, lo = rn(v s - hi)] into the swizzled slot row, columns [32 half, 32 half + 32)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int cc = 0; cc < 4; ++cc) {
+        const int c = 4 * half + cc;
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            const float a = v[8 * c + 2 * h] * s, b = v[8 * c + 2 * h + 1] * s;
+            const float a = v[8 * cc + 2 * h] * s, b = v[8 * cc + 2 * h + 1] * s;
             const __half2 hh = __floats2half2_rn(a, b);
             hi[h] = *reinterpret_cast<const uint32_t*>(&hh);
             if constexpr (kSplit) {
@@ -121,10 +122,11 @@ __device__ __forceinline__ void mirror_block_task(uint8_t* part, int task) {
 }
 
 template <bool kSplit>
-__device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta, float (&v)[64]) {
-    // v += beta * (hi [+ lo]) of the slot row
+__device__ __forceinline__ void add_row(const uint8_t* slot, int row, int half, float beta, float (&v)[32]) {
+    // v += beta * (hi [+ lo]) of the slot row, columns [32 half, 32 half + 32)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int cc = 0; cc < 4; ++cc) {
+        const int c = 4 * half + cc;
         const uint4 h = *reinterpret_cast<const uint4*>(slot + swz(row, c));
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
         float2 lf[4];
@@ -141,8 +143,8 @@ __device__ __forceinline__ void add_row(const uint8_t* slot, int row, float beta
                 f.x += lf[q].x;
                 f.y += lf[q].y;
             }
-            v[8 * c + 2 * q] += beta * f.x;
-            v[8 * c + 2 * q + 1] += beta * f.y;
+            v[8 * cc + 2 * q] += beta * f.x;
+            v[8 * cc + 2 * q + 1] += beta * f.y;
         }
     }
 }
@@ -160,23 +162,27 @@ __device__ __forceinline__ float4 load_row4(const float* base, int64_t roff, int
     return x;
 }
 
-// resident CTAs per SM: smem allows 3 for the single-pass layout (3 x 66 KB), 2 for the split one
-template <bool kSplit> constexpr int kSmallCtasPerSm = kSplit ? 2 : 3;
+// resident CTAs per SM (8 warps each): two for both layouts (registers bound the single-pass one)
+template <bool kSplit> constexpr int kSmallCtasPerSm = 2;
 
 template <bool kSplit>
 __global__ void __launch_bounds__(kThreadsS, kSmallCtasPerSm<kSplit>)
 small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
                    double* __restrict__ lambda_out, unsigned* __restrict__ status, const SmallPlan plan) {
     using L = SmallLayout<kSplit>;
+    constexpr int kWarps = kThreadsS / 32;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
-    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][4 warps]
+    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][8 warps]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int quad = warp & 3;                   // TMEM lane quadrant: rows 16 quad .. 16 quad + 15
+    const int half = warp >> 2;                  // column half: [32 half, 32 half + 32)
     const int m = lane >> 4;                     // matrix of the pair this thread serves
-    const int row = 16 * warp + (lane & 15);     // its row
+    const int row = 16 * quad + (lane & 15);     // its row
+    const int c0 = 32 * half;                    // its first column
     uint8_t* mat = smem + m * L::kPerMatrix;
 
     if (threadIdx.x == 0) {
@@ -236,7 +242,8 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
         stage_X();
         double ss = 0.0;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int i = 0; i < 32; ++i) {
+            const int c = c0 + i;
             if (c >= row) {
                 const double x = stage_at(row, c);                         // upper triangle (R10)
                 ss += (c == row ? 1.0 : 2.0) * x * x;
@@ -244,9 +251,12 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);   // within 16 lanes
-        if ((lane & 15) == 0) red[m * 4 + warp] = ss;
+        if ((lane & 15) == 0) red[m * kWarps + warp] = ss;
         __syncthreads();
-        double lam = sqrt(red[m * 4 + 0] + red[m * 4 + 1] + red[m * 4 + 2] + red[m * 4 + 3]);
+        double lsum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) lsum += red[m * kWarps + w];             // fixed order
+        double lam = sqrt(lsum);
         if (!isfinite(lam)) {
             if ((lane & 15) == 0 && warp == 0 && valid) atomicOr(status, 1u);
             lam = __longlong_as_double(0x7ff8000000000000LL);
@@ -254,13 +264,14 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
         if (valid && warp == 0 && (lane & 15) == 0 && lambda_out) lambda_out[b] = lam;
         const double inv = lam > 0.0 ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);
         auto store_x0 = [&](int slot_off) {               // X_0 = sym_upper(X) / lambda~ from staging
-            float x0[64];
+            float x0[32];
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
+            for (int i = 0; i < 32; ++i) {
+                const int c = c0 + i;
                 const float x = (c >= row) ? stage_at(row, c) : stage_at(c, row);
-                x0[c] = static_cast<float>(static_cast<double>(x) * inv);
+                x0[i] = static_cast<float>(static_cast<double>(x) * inv);
             }
-            store_row<kSplit>(mat + slot_off, row, x0, plan.s_x0);
+            store_row<kSplit>(mat + slot_off, row, half, x0, plan.s_x0);
         };
         store_x0(L::kZ);
         fence_proxy_async_smem();
@@ -306,25 +317,20 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             ptx::tc_fence_after();
             long long t_b = clock64();
 
-            float v[64];
+            float v[32];
             {
                 uint32_t raw[32];
-                const uint32_t ta = tmem + (static_cast<uint32_t>(32 * warp) << 16);
-                ptx::tmem_ld_32x32b_x32(ta, raw);
+                ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + c0, raw);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = st.alpha * __uint_as_float(raw[i]);
-                ptx::tmem_ld_32x32b_x32(ta + 32, raw);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[32 + i] = st.alpha * __uint_as_float(raw[i]);
             }
             ptx::tc_fence_before();
             long long t_c = clock64();
-            if (st.slot_d >= 0) add_row<kSplit>(mat + st.slot_d, row, st.beta, v);
+            if (st.slot_d >= 0) add_row<kSplit>(mat + st.slot_d, row, half, st.beta, v);
             if (st.final_mode == 0) {
                 // in place: the MMA that read this slot has completed (mma_bar)
-                store_row<kSplit>(mat + st.slot_out, row, v, st.out_scale);
+                store_row<kSplit>(mat + st.slot_out, row, half, v, st.out_scale);
                 if (st.mirror) {
                     // the stage output Z must be exactly symmetric: its antisymmetric part would
                     // grow like prod c_{t,0} over the stages (R20); Y and U need not be (their
@@ -366,44 +372,50 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     // + beta X[row][c] for c >= row (the lower part is replaced by the mirror below)
                     const float a = static_cast<float>(lam);
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) v[c] = a * v[c] + st.beta * input_at(c);
+                    for (int i = 0; i < 32; ++i) v[i] = a * v[i] + st.beta * input_at(c0 + i);
                 }
                 float4* srow = reinterpret_cast<float4*>(stage + row * kN);
                 // ADMM: X_next = sigma (P - M) is stored first, while the inputs (which the
                 // outputs may overwrite: in place) are still intact; then P
                 const bool two = st.final_mode == 1 && plan.out2;
                 for (int pass = two ? 1 : 0; pass >= 0; --pass) {
-                if (pass == 1) {
+                    if (pass == 1) {
 #pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        srow[q ^ (row & 15)] = make_float4(plan.sigma2 * (v[4 * q] - input_at(4 * q)),
-                                                           plan.sigma2 * (v[4 * q + 1] - input_at(4 * q + 1)),
-                                                           plan.sigma2 * (v[4 * q + 2] - input_at(4 * q + 2)),
-                                                           plan.sigma2 * (v[4 * q + 3] - input_at(4 * q + 3)));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                }
-                __syncthreads();
-                float* dst = pass == 0 ? out : plan.out2;
-                if (valid && row < n) {
-                    float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
-                    if (n == kN) {
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            float4 o;
-                            o.x = (4 * q + 0 >= row) ? stage_at(row, 4 * q + 0) : stage_at(4 * q + 0, row);
-                            o.y = (4 * q + 1 >= row) ? stage_at(row, 4 * q + 1) : stage_at(4 * q + 1, row);
-                            o.z = (4 * q + 2 >= row) ? stage_at(row, 4 * q + 2) : stage_at(4 * q + 2, row);
-                            o.w = (4 * q + 3 >= row) ? stage_at(row, 4 * q + 3) : stage_at(4 * q + 3, row);
-                            __stcs(reinterpret_cast<float4*>(orow) + q, o);
+                        for (int qq = 0; qq < 8; ++qq) {
+                            const int c = c0 + 4 * qq;
+                            srow[(8 * half + qq) ^ (row & 15)] =
+                                make_float4(plan.sigma2 * (v[4 * qq] - input_at(c)),
+                                            plan.sigma2 * (v[4 * qq + 1] - input_at(c + 1)),
+                                            plan.sigma2 * (v[4 * qq + 2] - input_at(c + 2)),
+                                            plan.sigma2 * (v[4 * qq + 3] - input_at(c + 3)));
                         }
                     } else {
-                        for (int c = 0; c < n; ++c) orow[c] = (c >= row) ? stage_at(row, c) : stage_at(c, row);
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq)
+                            srow[(8 * half + qq) ^ (row & 15)] =
+                                make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
                     }
-                }
-                __syncthreads();
+                    __syncthreads();
+                    float* dst = pass == 0 ? out : plan.out2;
+                    if (valid && row < n) {
+                        float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
+                        if (n == kN) {
+#pragma unroll
+                            for (int qq = 0; qq < 8; ++qq) {
+                                const int c = c0 + 4 * qq;
+                                float4 o;
+                                o.x = (c + 0 >= row) ? stage_at(row, c + 0) : stage_at(c + 0, row);
+                                o.y = (c + 1 >= row) ? stage_at(row, c + 1) : stage_at(c + 1, row);
+                                o.z = (c + 2 >= row) ? stage_at(row, c + 2) : stage_at(c + 2, row);
+                                o.w = (c + 3 >= row) ? stage_at(row, c + 3) : stage_at(c + 3, row);
+                                __stcs(reinterpret_cast<float4*>(orow + c), o);
+                            }
+                        } else {
+                            for (int c = c0; c < min(c0 + 32, n); ++c)
+                                orow[c] = (c >= row) ? stage_at(row, c) : stage_at(c, row);
+                        }
+                    }
+                    __syncthreads();
                 }
             }
         }
