@@ -383,6 +383,16 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
     return steps;
 }
 
+// Whether the chain of run_body keeps its operand copies upper-only (see GemmShape::upper_only):
+// 16-bit operands, on the CTA-pair kernel or on the 1-CTA kernel without split-K; not when the
+// opt-in chain kernel takes the products.
+bool upper_only_mode(const psd_filter_s* h, int n, int batch, int npad) {
+    if (op_of(h->prec) == OpType::TF32 || std::getenv("PSD_NO_UPPER_ONLY")) return false;
+    if (npad % 256 == 0 && use_pair_kernel(n, batch)) return true;
+    if (h->use_chain) return false;
+    return sym_gemm_split_k(npad, batch, op_of(h->prec)) == 1;
+}
+
 psd_status_t check_args(psd_filter_t h, const void* X, int64_t n, int64_t batch, const void* out) {
     if (!h) return fail(PSD_EINVAL, "null handle");
     if (!X || !out) return fail(PSD_EINVAL, "null X or out");
@@ -602,13 +612,13 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.nF = n;
         }
         ep.dbg_nostore = std::getenv("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug experiment
-        ep.upper_only = (npad % 256 == 0 && use_pair_kernel(n, batch) && ws.op != OpType::TF32 &&
-                         std::getenv("PSD_NO_UPPER_ONLY") == nullptr) ? 1 : 0;
+        ep.upper_only = upper_only_mode(h, n, batch, npad) ? 1 : 0;
         return ep;
     };
     const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
-    // the chain's operand copies hold only their upper tiles (CTA-pair kernel, 16-bit operands)
-    const bool upper_only = pair && ws.op != OpType::TF32 && std::getenv("PSD_NO_UPPER_ONLY") == nullptr;
+    // the chain's operand copies hold only their upper tiles (16-bit operands; the 1-CTA kernel
+    // without split-K; not the opt-in chain kernel)
+    const bool upper_only = upper_only_mode(h, n, batch, npad);
     shape.upper_only = upper_only ? 1 : 0;
     const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
                              ? chain_cluster_size(ws.op, split, npad, batch)

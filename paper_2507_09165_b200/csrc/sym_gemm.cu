@@ -145,11 +145,23 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 uint8_t* sa = ring + st * kStageBytes;
                 const int kx = (kb0 + kb) * kBK;
                 ptx::mbar_arrive_expect_tx(&full[st], kStageBytes);
-                ptx::tma_load_2d(sa, &tm.a, &full[st], kx, rowA, pol);
-                ptx::tma_load_2d(sa + kTileBytes, &tm.b, &full[st], kx, rowB, pol);
+                // upper-only storage (16-bit, no split-K): left of the 128-row block's diagonal block a
+                // panel is the stored upper block transposed -- 64 x 64 boxes read as an MN-major operand
+                auto load = [&](uint8_t* dst, const CUtensorMap* mk, const CUtensorMap* mt, int rows, int row0,
+                                int diag0, int row) {
+                    if (Tr::kBytes == 2 && KS == 1 && s.upper_only && kx < diag0) {
+                        for (int c = 0; c < rows; c += 64)
+                            ptx::tma_load_2d(dst + c * kBlockKBytes, mt, &full[st], row0 + c, b * s.npad + kx, pol);
+                    } else {
+                        ptx::tma_load_2d(dst, mk, &full[st], kx, row, pol);
+                    }
+                };
+                const int jdiag = (J * BN / kTile) * kTile;          // 128-row block holding B's rows
+                load(sa, &tm.a, &tm.a_t, kTile, I * kTile, I * kTile, rowA);
+                load(sa + kTileBytes, &tm.b, &tm.b_t, BN, J * BN, jdiag, rowB);
                 if constexpr (kSplit) {
-                    ptx::tma_load_2d(sa + kTileBytes + kBBytes, &tm.a_lo, &full[st], kx, rowA, pol);
-                    ptx::tma_load_2d(sa + 2 * kTileBytes + kBBytes, &tm.b_lo, &full[st], kx, rowB, pol);
+                    load(sa + kTileBytes + kBBytes, &tm.a_lo, &tm.a_lo_t, kTile, I * kTile, I * kTile, rowA);
+                    load(sa + 2 * kTileBytes + kBBytes, &tm.b_lo, &tm.b_lo_t, BN, J * BN, jdiag, rowB);
                 }
             }
         }
@@ -162,23 +174,33 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 ptx::mbar_wait(&full[st], ph);
                 ptx::tc_fence_after();
                 const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
-                const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
-                const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + kTileBytes);
+                const int kx = (kb0 + kb) * kBK;
+                const bool up = Tr::kBytes == 2 && KS == 1 && s.upper_only;
+                const bool a_mn = up && kx < I * kTile;
+                const bool b_mn = up && kx < (J * BN / kTile) * kTile;
+                // MN-major (transposed) operands: 64-element MN chunks 8 KB apart, 8-row K groups 1 KB
+                // apart, one K step of 16 = 2 KB (tools/micro/mn_major.cu)
+                auto desc = [&](uint32_t addr, bool mn) {
+                    return mn ? ptx::smem_desc_sw128_mnmajor(addr, 8192, 1024) : ptx::smem_desc_sw128_kmajor(addr);
+                };
+                const uint64_t adesc = desc(sa, a_mn);
+                const uint64_t bdesc = desc(sa + kTileBytes, b_mn);
+                const uint32_t idesc = kIdesc | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
+                const uint64_t astep = a_mn ? (2048 >> 4) : (32 >> 4), bstep = b_mn ? (2048 >> 4) : (32 >> 4);
                 auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
                     if constexpr (T == OpType::TF32)
                         ptx::mma_tf32(tmem_base, a, bb, kIdesc, accumulate);
                     else
-                        ptx::mma_f16(tmem_base, a, bb, kIdesc, accumulate);
+                        ptx::mma_f16(tmem_base, a, bb, idesc, accumulate);
                 };
 #pragma unroll
                 for (int k = 0; k < kBK / kUmmaK; ++k) {
-                    const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);   // 32 B per K step
-                    mma(adesc + koff, bdesc + koff, (kb | k) != 0);
+                    mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
                     if constexpr (kSplit) {
-                        const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + kTileBytes + kBBytes);
-                        const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes + kBBytes);
-                        mma(adesc + koff, blo + koff, 1u);            // A_hi B_lo
-                        mma(alo + koff, bdesc + koff, 1u);            // A_lo B_hi
+                        const uint64_t alo = desc(sa + kTileBytes + kBBytes, a_mn);
+                        const uint64_t blo = desc(sa + 2 * kTileBytes + kBBytes, b_mn);
+                        mma(adesc + k * astep, blo + k * bstep, 1u);            // A_hi B_lo
+                        mma(alo + k * astep, bdesc + k * bstep, 1u);            // A_lo B_hi
                     }
                 }
                 ptx::mma_commit(&empty[st]);
