@@ -147,6 +147,7 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                     const int b = t / tpm;
                     int I, J;
                     upper128(t - b * tpm, nt, I, J);
+                    const bool up = CS == 2 && !kSplit && Tr::kBytes == 2 && p.upper_only;
                     const int rowA = b * npad + I * kTile + static_cast<int>(rank) * C::kRowsA;
                     const int rowB = b * npad + J * kTile + static_cast<int>(rank) * BN;
                     const int offA = static_cast<int>(rank) * C::kRowsA * kBlockKBytes;
@@ -154,8 +155,19 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                         ptx::mbar_wait(&empty[pst], pph ^ 1);
                         uint8_t* sa = ring + pst * C::kStageBytes;
                         ptx::mbar_arrive_expect_tx(&full[pst], C::kStageBytes);
-                        ptx::tma_load_2d_multicast(sa + offA, ma, &full[pst], kb * kBK, rowA, C::kMask);
-                        ptx::tma_load_2d(sa + C::kA, mb, &full[pst], kb * kBK, rowB, pol);
+                        const int k0 = kb * kBK;
+                        // upper-only storage: left of a 128-row block's diagonal tile the slice is the
+                        // stored upper block transposed (a 64 x 64 box = one MN chunk, 8 KB per rank)
+                        if (up && k0 < I * kTile)
+                            ptx::tma_load_2d_multicast(sa + offA, ma, &full[pst], I * kTile + static_cast<int>(rank) * 64,
+                                                       b * npad + k0, C::kMask);
+                        else
+                            ptx::tma_load_2d_multicast(sa + offA, ma, &full[pst], k0, rowA, C::kMask);
+                        if (up && k0 < J * kTile)
+                            ptx::tma_load_2d(sa + C::kA, mb, &full[pst], J * kTile + static_cast<int>(rank) * BN,
+                                             b * npad + k0, pol);
+                        else
+                            ptx::tma_load_2d(sa + C::kA, mb, &full[pst], k0, rowB, pol);
                         if (kb == 0 && t == cluster) stamp(s, 1);
                         if constexpr (kSplit) {
                             ptx::tma_load_2d_multicast(sa + C::kA + C::kB + offA, ma_lo, &full[pst], kb * kBK, rowA,
@@ -171,6 +183,10 @@ chain_kernel(const __grid_constant__ ChainParams p) {
             // ------------------------------------------------ MMA issuer
             if (ptx::elect_one()) {
                 for (int t = cluster; t < total; t += nclusters) {
+                    const int tb = t / tpm;
+                    int tI, tJ;
+                    upper128(t - tb * tpm, nt, tI, tJ);
+                    const bool up = CS == 2 && !kSplit && Tr::kBytes == 2 && p.upper_only;
                     const int acc = mit & 1;
                     ptx::mbar_wait(&tmem_empty[acc], ((mit >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
@@ -180,18 +196,24 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                         ptx::tc_fence_after();
                         if (kb == 0 && t == cluster) stamp(s, 2);
                         const uint32_t sa = ptx::smem_u32(ring + mst * C::kStageBytes);
-                        const uint64_t adesc = ptx::smem_desc_sw128_kmajor(sa);
-                        const uint64_t bdesc = ptx::smem_desc_sw128_kmajor(sa + C::kA);
+                        const bool a_mn = up && kb * kBK < tI * kTile;
+                        const bool b_mn = up && kb * kBK < tJ * kTile;
+                        const uint64_t adesc = a_mn ? ptx::smem_desc_sw128_mnmajor(sa, 8192, 1024)
+                                                    : ptx::smem_desc_sw128_kmajor(sa);
+                        const uint64_t bdesc = b_mn ? ptx::smem_desc_sw128_mnmajor(sa + C::kA, 8192, 1024)
+                                                    : ptx::smem_desc_sw128_kmajor(sa + C::kA);
+                        const uint32_t idesc = kIdesc | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
+                        const uint64_t astep = a_mn ? (2048 >> 4) : (32 >> 4), bstep = b_mn ? (2048 >> 4) : (32 >> 4);
                         auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
                             if constexpr (T == OpType::TF32)
                                 ptx::mma_tf32(d_tmem, a, bb, kIdesc, accumulate);
                             else
-                                ptx::mma_f16(d_tmem, a, bb, kIdesc, accumulate);
+                                ptx::mma_f16(d_tmem, a, bb, idesc, accumulate);
                         };
 #pragma unroll
                         for (int k = 0; k < kBK / kUmmaK; ++k) {
                             const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
-                            mma(adesc + koff, bdesc + koff, (kb | k) != 0);
+                            mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
                             if constexpr (kSplit) {
                                 const uint64_t alo = ptx::smem_desc_sw128_kmajor(sa + C::kA + C::kB);
                                 const uint64_t blo = ptx::smem_desc_sw128_kmajor(sa + 2 * C::kA + C::kB);

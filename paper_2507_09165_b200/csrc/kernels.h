@@ -129,6 +129,7 @@ struct ChainParams {
     unsigned* barrier;              // zeroed grid-barrier counter
     unsigned long long* dbg;        // debug: %globaltimer phase stamps of CTA 0 [step][8] (NULL in production)
     int flags;                      // debug bits (PSD_CHAIN_FLAGS): 1 = no addend prefetch, 2 = no tensormap prefetch
+    int upper_only;                 // CS = 2, 16-bit single pass: upper-only operand storage (see GemmShape)
     ChainStep steps[kChainMaxSteps];
 };
 // Cluster size for (npad, batch): 4 or 2, or 0 when the chain kernel cannot run it.

@@ -383,13 +383,12 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
     return steps;
 }
 
-// Whether the chain of run_body keeps its operand copies upper-only (see GemmShape::upper_only):
-// 16-bit operands, on the CTA-pair kernel or on the 1-CTA kernel without split-K; not when the
-// opt-in chain kernel takes the products.
+// Whether the per-product launches of run_body keep the operand copies upper-only (see
+// GemmShape::upper_only): 16-bit operands, on the CTA-pair kernel or on the 1-CTA kernel without
+// split-K.
 bool upper_only_mode(const psd_filter_s* h, int n, int batch, int npad) {
     if (op_of(h->prec) == OpType::TF32 || std::getenv("PSD_NO_UPPER_ONLY")) return false;
     if (npad % 256 == 0 && use_pair_kernel(n, batch)) return true;
-    if (h->use_chain) return false;
     return sym_gemm_split_k(npad, batch, op_of(h->prec)) == 1;
 }
 
@@ -581,6 +580,16 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
     }
+    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+    const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
+                             ? chain_cluster_size(ws.op, split, npad, batch)
+                             : 0;
+    // the chain's operand copies hold only their upper tiles (16-bit operands; CTA-pair kernel,
+    // 1-CTA kernel without split-K, chain kernel with 2-CTA clusters)
+    const bool upper_only = chain_cs ? (chain_cs == 2 && !split && ws.op != OpType::TF32 &&
+                                        std::getenv("PSD_NO_UPPER_ONLY") == nullptr)
+                                     : upper_only_mode(h, n, batch, npad);
+    shape.upper_only = upper_only ? 1 : 0;
     auto make_ep = [&](const Step& s) {
         EpiParams ep{};
         ep.alpha = static_cast<float>(s.alpha / (sc[s.A] * sc[s.B]));
@@ -612,17 +621,9 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.nF = n;
         }
         ep.dbg_nostore = std::getenv("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug experiment
-        ep.upper_only = upper_only_mode(h, n, batch, npad) ? 1 : 0;
+        ep.upper_only = upper_only ? 1 : 0;
         return ep;
     };
-    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
-    // the chain's operand copies hold only their upper tiles (16-bit operands; the 1-CTA kernel
-    // without split-K; not the opt-in chain kernel)
-    const bool upper_only = upper_only_mode(h, n, batch, npad);
-    shape.upper_only = upper_only ? 1 : 0;
-    const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
-                             ? chain_cluster_size(ws.op, split, npad, batch)
-                             : 0;
     if (chain_cs) {
         // (a3-a6) every product in one persistent launch (chain.cu)
         std::unique_ptr<ChainParams> cp(new ChainParams());
@@ -635,6 +636,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         cp->batch = batch;
         cp->nsteps = static_cast<int>(steps.size());
         cp->flags = std::getenv("PSD_CHAIN_FLAGS") ? std::atoi(std::getenv("PSD_CHAIN_FLAGS")) : 0;
+        cp->upper_only = upper_only ? 1 : 0;
         cp->barrier = reinterpret_cast<unsigned*>(ws.counters + (kMaxSteps - 1));
         for (size_t si = 0; si < steps.size(); ++si) {
             cp->steps[si].a = steps[si].A;
