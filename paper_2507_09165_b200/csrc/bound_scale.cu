@@ -38,17 +38,44 @@ frobenius_partials_kernel(const float* __restrict__ X, int n, int nblk, double* 
     const float* Kb = form.Xk ? form.Xk + static_cast<int64_t>(b) * n * n : nullptr;
     double acc = 0.0;
     // rows i == blockIdx.x (mod nblk), one warp per row, upper part j >= i
+    const bool vec = (n & 3) == 0;                   // rows 16-byte aligned: float4 loads
     for (int i = blockIdx.x + nblk * warp; i < n; i += nblk * (kBoundThreads / 32)) {
         const float* row = Xb + static_cast<int64_t>(i) * n;
+        const float* krow = Kb ? Kb + static_cast<int64_t>(i) * n : nullptr;
         const float yi = (Kb && form.y) ? form.y[static_cast<int64_t>(b) * n + i] : 0.0f;
-        for (int j = i + lane; j < n; j += 32) {
-            float m = row[j];
-            if (Kb) {
-                m = form_m(m, Kb[static_cast<int64_t>(i) * n + j], form.inv_sigma);
-                if (j == i) m = __fsub_rn(m, yi);
+        if (vec) {
+            // 4 columns per lane per step (independent accumulations), from the float4 holding i
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int c = (i & ~3) + 4 * lane; c < n; c += 128) {
+                float4 x4 = __ldg(reinterpret_cast<const float4*>(row + c));
+                if (krow) {
+                    const float4 k4 = __ldg(reinterpret_cast<const float4*>(krow + c));
+                    x4.x = form_m(x4.x, k4.x, form.inv_sigma);
+                    x4.y = form_m(x4.y, k4.y, form.inv_sigma);
+                    x4.z = form_m(x4.z, k4.z, form.inv_sigma);
+                    x4.w = form_m(x4.w, k4.w, form.inv_sigma);
+                }
+                const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = c + q;
+                    float m = xs[q];
+                    if (krow && j == i) m = __fsub_rn(m, yi);
+                    const double x = m;
+                    a4[q] += (j < i) ? 0.0 : (j == i ? 1.0 : 2.0) * x * x;
+                }
             }
-            const double x = m;
-            acc += (j == i ? 1.0 : 2.0) * x * x;
+            acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        } else {
+            for (int j = i + lane; j < n; j += 32) {
+                float m = row[j];
+                if (krow) {
+                    m = form_m(m, krow[j], form.inv_sigma);
+                    if (j == i) m = __fsub_rn(m, yi);
+                }
+                const double x = m;
+                acc += (j == i ? 1.0 : 2.0) * x * x;
+            }
         }
     }
     acc = warp_sum(acc);
@@ -222,8 +249,14 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
 
 }  // namespace
 
-int bound_blocks_per_matrix(int n) {
+int bound_blocks_per_matrix(int n, int batch) {
+    // about 16 rows per block, but at least two blocks per SM over the whole batch (small batches:
+    // one row per warp in flight), at most 256 partial sums per matrix (the workspace) and one
+    // row per block
     int k = (n + 15) / 16;
+    const int fill = (2 * 148 + batch - 1) / batch;
+    if (k < fill) k = fill;
+    if (k > n) k = n;
     return k < 1 ? 1 : (k > 256 ? 256 : k);
 }
 

@@ -178,7 +178,7 @@ cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, uns
 
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
-int bound_blocks_per_matrix(int n);
+int bound_blocks_per_matrix(int n, int batch);
 cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
                                       cudaStream_t stream, const InputForm& form = InputForm());
 

@@ -515,7 +515,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     // (a1) bound
     const double* lam = nullptr;
     if (h->bound == PSD_BOUND_FROBENIUS || h->bound == PSD_BOUND_LANCZOS) {
-        const int nblk = bound_blocks_per_matrix(n);
+        const int nblk = bound_blocks_per_matrix(n, batch);
         e = launch_frobenius_partials(X, n, batch, ws.partial, nblk, st, form);
         if (e != cudaSuccess) return cuda_fail(e, "frobenius_partials");
         h->kernel_launches += 2;
@@ -936,7 +936,7 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
         Xf = rp.xg;
     }
     // (2) bound (identical on every rank) and (3) scale + convert into the full X_0
-    const int nblk = bound_blocks_per_matrix(n);
+    const int nblk = bound_blocks_per_matrix(n, 1);
     e = launch_frobenius_partials(Xf, n, 1, ws.partial, nblk, st);
     if (e == cudaSuccess) e = launch_finalize_bound(ws.partial, nblk, 1, ws.lambda, nullptr, ws.status, st);
     if (e == cudaSuccess)
@@ -1120,7 +1120,7 @@ psd_status_t run_rowpanel_p2p(psd_filter_s* h, const float* X, float* out, bool 
         }
     if ((rc = barrier()) != PSD_OK) return rc;
     // (2) bound (identical on every rank) and (3) X_0 into every local region
-    const int nblk = bound_blocks_per_matrix(n);
+    const int nblk = bound_blocks_per_matrix(n, 1);
     e = launch_frobenius_partials(xg(r_lo), n, 1, ws.partial, nblk, st);
     if (e == cudaSuccess) e = launch_finalize_bound(ws.partial, nblk, 1, ws.lambda, nullptr, ws.status, st);
     for (int r = r_lo; r < r_hi && e == cudaSuccess; ++r)
