@@ -1400,10 +1400,25 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
     for (auto q : hp.s) cudaStreamWaitEvent(q, start, 0);
     cudaEvent_t freed[psd_filter_s::HostPipe::kSlots] = {};
     std::vector<cudaEvent_t> used = {start};
-    for (int c = 0; c * per < batch; ++c) {
-        const int slot = c % psd_filter_s::HostPipe::kSlots;
-        const int64_t b0 = c * per;
-        const int64_t nb = std::min<int64_t>(per, batch - b0);
+    // chunk boundaries: the first and the last chunk are half-size (the pipeline's fill -- the first
+    // host-to-device copy -- and its drain -- the last device-to-host copy -- are not overlapped)
+    std::vector<std::pair<int64_t, int64_t>> parts;
+    {
+        int64_t b0 = 0;
+        const int64_t edge = (chunks >= 4 && per >= 2) ? per / 2 : per;
+        while (b0 < batch) {
+            const bool first = parts.empty();
+            int64_t nb = first ? edge : per;
+            if (batch - b0 - nb > 0 && batch - b0 - nb < per) nb = batch - b0 - edge;   // leave a half-size tail
+            if (nb <= 0 || nb > batch - b0) nb = batch - b0;
+            parts.emplace_back(b0, nb);
+            b0 += nb;
+        }
+    }
+    for (size_t c = 0; c < parts.size(); ++c) {
+        const int slot = static_cast<int>(c % psd_filter_s::HostPipe::kSlots);
+        const int64_t b0 = parts[c].first;
+        const int64_t nb = parts[c].second;
         if (freed[slot]) cudaStreamWaitEvent(hp.s[0], freed[slot], 0);
         e = cudaMemcpyAsync(hp.dx[slot], X_host + b0 * n * n, nb * mat, cudaMemcpyHostToDevice, hp.s[0]);
         if (e != cudaSuccess) return cuda_fail(e, "H2D");
