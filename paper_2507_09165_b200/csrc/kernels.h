@@ -166,7 +166,7 @@ cudaError_t certify_chain(const std::vector<std::vector<double>>& coeffs, double
 
 // Row-panel multi-GPU path (rowpanel.cu).
 cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
-                                int64_t ld, cudaStream_t stream);
+                                int64_t ld, cudaStream_t stream, bool mirror = true);
 int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap);
 // Cross-rank epoch barrier of the peer-memory path: signal stores `epoch` into slot `rank` of every
 // rank's flag array (system-scope release after a system fence); wait spins until every slot of

@@ -973,6 +973,11 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
         m.b = ws.tmap[s.B];
         m.a_lo = m.a;
         m.b_lo = m.b;
+        m.a_t = m.a_lo_t = ws.tmap64[s.A];
+        m.b_t = m.b_lo_t = ws.tmap64[s.B];
+        // upper-only operand storage (16-bit): the unpack writes each gathered tile without its
+        // mirror and the loader reads the left part of a panel transposed
+        const bool upper_only = ws.op != OpType::TF32 && std::getenv("PSD_NO_UPPER_ONLY") == nullptr;
         const int r0 = comm ? rank : 0, r1 = comm ? rank + 1 : nranks;
         for (int vr = r0; vr < r1; ++vr) {
             const size_t slot0 = static_cast<size_t>(vr) * rp.per * tile_elems;
@@ -980,6 +985,7 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
                                : static_cast<void*>(static_cast<uint8_t*>(rp.packed_op) + slot0 * ob);
             GemmShape shape{npad, 1, rp.codes + static_cast<size_t>(vr) * rp.per, rp.counts[vr],
                             ws.counters + si * nranks + vr};
+            shape.upper_only = upper_only ? 1 : 0;
             if (rp.counts[vr] == 0) continue;
             e = launch_sym_gemm_2cta(ws.op, false, m, shape, ep, st);
             if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (row panel)");
@@ -993,7 +999,8 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
             if (r != 0) return nccl_fail(r, "ncclAllGather(tiles)");
         }
         e = launch_unpack_tiles(s.outF ? 4 : ob, gathered, rp.codes, nranks * rp.per,
-                                s.outF ? static_cast<void*>(rp.pfull) : ws.op_buf[s.out_op], npad, st);
+                                s.outF ? static_cast<void*>(rp.pfull) : ws.op_buf[s.out_op], npad, st,
+                                s.outF || !upper_only);
         if (e != cudaSuccess) return cuda_fail(e, "unpack");
         h->kernel_launches += 1;
     }

@@ -25,7 +25,7 @@ constexpr int kBand = 32;        // rows of a tile per block
 template <typename E>
 __global__ void __launch_bounds__(256)
 unpack_tiles_kernel(const E* __restrict__ packed, const uint32_t* __restrict__ codes, int ntiles, E* __restrict__ full,
-                    int64_t ld) {
+                    int64_t ld, bool mirror) {
     __shared__ E S[kBand][kT + 16 / sizeof(E)];
     const int tile = blockIdx.x / (kT / kBand);
     const int band = blockIdx.x % (kT / kBand);
@@ -46,6 +46,7 @@ unpack_tiles_kernel(const E* __restrict__ packed, const uint32_t* __restrict__ c
 #pragma unroll
             for (int k = 0; k < kVec; ++k) S[r][q * kVec + k] = xe[k];
         }
+        if (!mirror) return;             // upper-only operand storage: no transposed band
         __syncthreads();
         // transposed: output row J*256 + c, columns I*256 + r0 .. + kBand
         constexpr int kOutVecs = kBand / kVec;
@@ -109,15 +110,15 @@ cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, uns
 }
 
 cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32_t* codes, int ntiles, void* full,
-                                int64_t ld, cudaStream_t stream) {
+                                int64_t ld, cudaStream_t stream, bool mirror) {
     const int blocks = ntiles * (kT / kBand);
     if (blocks == 0) return cudaSuccess;
     if (elem_bytes == 2)
         unpack_tiles_kernel<uint16_t><<<blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(packed), codes, ntiles,
-                                                                  static_cast<uint16_t*>(full), ld);
+                                                                  static_cast<uint16_t*>(full), ld, mirror);
     else
         unpack_tiles_kernel<float><<<blocks, 256, 0, stream>>>(static_cast<const float*>(packed), codes, ntiles,
-                                                               static_cast<float*>(full), ld);
+                                                               static_cast<float*>(full), ld, mirror);
     return cudaGetLastError();
 }
 
