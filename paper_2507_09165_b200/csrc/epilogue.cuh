@@ -6,14 +6,17 @@
 //     v = alpha * acc + beta * D[gi][gj]         D: the operand-precision copy of the addend
 //                                                (Z or Y; hi + lo on the split path) or, for
 //                                                the reconstruction, the fp32 input X
-//     operand copy: out_op[gi][gj] = out_op[gj][gi] = v   (mirrored -> exactly symmetric)
+//     operand copy: out_op[gi][gj] = v, and out_op[gj][gi] = v unless upper-only storage
+//                   skips the mirror of an off-diagonal tile (the loaders then read the lower
+//                   triangle as the transpose of the stored upper tile: exactly symmetric either way)
 //     final output: outF[gi][gj]  = outF[gj][gi]  = v     (fp32, masked to n)
 // Chunks are 32-aligned, so a chunk is either strictly above the diagonal (gj0 > gi0: direct
 // rows + the mirrored block through a per-warp 32x32 smem transpose) or a diagonal 32x32
 // block (gj0 == gi0: the block is symmetrised from its upper triangle through smem and
-// written as full rows).  Callers skip blocks below the diagonal.  Every store is a 16-byte
-// row segment.  This is where the polynomial's axpy terms (c_j Y, c_0 Z) and the reconstruction
-// 1/2 X + 1/2 lambda~ X_0 S of Algorithm 2 are fused: no separate elementwise
+// written as full rows).  Callers skip blocks below the diagonal.  Blocks are staged in the
+// warp's smem and drained with coalesced row-segment stores.  This is where the polynomial's
+// axpy terms (c_j Y, c_0 Z) and the reconstruction 1/2 X + 1/2 lambda~ X_0 S of Algorithm 2
+// are fused -- and the ADMM formation / X update -- so no separate elementwise
 // pass touches HBM.
 #pragma once
 #include "kernels.h"

@@ -3,8 +3,11 @@
 //
 // Every product of the composite filter (Algorithm 2) multiplies two commuting
 // symmetric matrices (powers/polynomials of the same X), so C is symmetric: only
-// upper tiles (I <= J) are computed and each is stored twice (direct + transposed).  A and B
-// are symmetric, so both operands are read as row panels ("K-major").
+// upper tiles (I <= J) are computed.  A and B are symmetric, so both operands are read as row
+// panels: K-major from the stored tiles, or -- with upper-only storage (GemmShape::upper_only,
+// 16-bit, KS = 1), where each tile is stored once and only the 128x128 diagonal blocks whole --
+// transposed (MN-major, 64 x 64 TMA boxes) left of the row block's diagonal block.  Tiles
+// (128 x 128, or 128 x 64 for few-tile problems) meeting the diagonal are stored mirrored.
 //
 // A cluster of KS CTAs (KS = 1, 2, 4; cluster split-K) owns one 128x128 upper tile:
 //   warp 0 / elected lane : TMA producer over this CTA's K slice -> kStages smem ring

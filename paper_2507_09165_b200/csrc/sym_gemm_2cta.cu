@@ -1,7 +1,7 @@
 // sym_gemm_2cta.cu -- persistent CTA-pair (cta_group::2) symmetric product for large n.
 //
-// Same product and epilogue as sym_gemm.cu (C = alpha A B + beta D over upper tiles,
-// mirrored stores; Algorithm 2's products), re-tiled for full tensor-core
+// Same product and epilogue as sym_gemm.cu (C = alpha A B + beta D over upper tiles;
+// Algorithm 2's products), re-tiled for full tensor-core
 // rate on sm_100a:
 //   * a cluster of 2 CTAs (one TPC) owns a 256 x 256 upper output tile; tcgen05.mma
 //     .cta_group::2 with M = 256, N = 256, K = 16: CTA r holds A rows [r*128, r*128+128)
@@ -13,7 +13,12 @@
 //     w4..w7 epilogue (one TMEM lane quadrant each);
 //   * TMEM holds two 256-column fp32 accumulators (all 512 columns), so the epilogue of
 //     tile i overlaps the mainloop of tile i+1;
-//   * kStages-deep smem ring, 32 KB per stage per CTA (A 16 KB + B 16 KB, SW128 K-major).
+//   * kStages-deep smem ring, 32 KB per stage per CTA (A 16 KB + B 16 KB, SW128);
+//   * dynamic tile scheduler: the leader's producer takes tile ids from a global counter and
+//     broadcasts them to both CTAs through an mbarrier-guarded smem ring;
+//   * upper-only operand storage (GemmShape::upper_only, 16-bit): K blocks left of a row block's
+//     diagonal tile are loaded transposed (two 64 x 64 boxes of the stored upper tile) and fed to
+//     tcgen05 as MN-major operands; the epilogue then skips the mirror of off-diagonal tiles.
 #include "epilogue.cuh"
 #include "kernels.h"
 #include "optraits.cuh"
