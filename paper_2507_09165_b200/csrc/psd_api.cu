@@ -289,7 +289,11 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
         ws.tiles_per_matrix = nt * (nt + 1) / 2;
         if (ws.tiles_per_matrix > 0) {
             std::vector<uint32_t> order(ws.tiles_per_matrix);
-            make_tile_order(nt, std::getenv("PSD_TILE_ORDER"), order.data());
+            // visiting order of the upper 256-tiles: row-major up to 16 tile rows (n <= 4096: the
+            // panels in flight fit L2 either way), 8 x 8 super-tiles beyond (n = 16384: 79-82 vs
+            // 91-97 ms per projection, tools/gemm_probe.py); PSD_TILE_ORDER overrides
+            const char* env_order = std::getenv("PSD_TILE_ORDER");
+            make_tile_order(nt, env_order ? env_order : (nt > 16 ? "grouped8" : "row"), order.data());
             if (cudaMalloc(&ws.tiles, order.size() * 4) != cudaSuccess) {
                 free_ws(ws);
                 return fail(PSD_ENOMEM, "cudaMalloc tile order failed");
