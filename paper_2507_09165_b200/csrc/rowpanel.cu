@@ -13,6 +13,8 @@
 
 #include "kernels.h"
 
+#include <vector>
+
 namespace psd {
 
 namespace {
@@ -128,10 +130,13 @@ int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap) {
     const int T = nt * (nt + 1) / 2;
     const int per = (T + nranks - 1) / nranks;
     if (!codes) return per;
-    int t = 0, k = 0;
-    for (int I = 0; I < nt; ++I)
-        for (int J = I; J < nt; ++J, ++t)
-            if (t % nranks == rank && k < cap) codes[k++] = (static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(J);
+    // the upper tiles in the single-GPU visiting order (8 x 8 super-tiles beyond 16 tile rows, for
+    // L2 reuse of the panels), dealt round robin: every rank's list keeps that locality
+    std::vector<uint32_t> order(T);
+    make_tile_order(nt, nt > 16 ? "grouped8" : "row", order.data());
+    int k = 0;
+    for (int t = 0; t < T; ++t)
+        if (t % nranks == rank && k < cap) codes[k++] = order[t];
     const int actual = k;
     while (k < per && k < cap) codes[k++] = 0xFFFFFFFFu;
     return actual;
