@@ -480,3 +480,25 @@ def test_certificate_on_device(pkg, which):
     assert abs(c["relu_err"] - e) <= 1e-9 * e, (c["relu_err"], e)
     assert abs(c["sign_err"] - s) <= 1e-9 * s, (c["sign_err"], s)
     assert 0.0 < c["relu_argmax"] <= 1.0 and 1e-3 <= c["sign_argmax"] <= 1.0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 128, 129, 255, 256, 1023, 1025])
+def test_boundary_sizes(pkg, n):
+    """Every padding / path boundary: n = 1..3 and around 64 (small-n kernel / tile kernels), 128
+    and 256 (tile multiples) and 1024 (CTA-pair threshold): parity, exact symmetry, and a
+    positive-semidefinite result up to the certified error."""
+    batch = 3
+    X = synth.batch("goe", n, batch, synth.SEED_BASE + 7 * n)
+    P, lam, f = _gpu(pkg, _product_filter("half", pkg), X, "fp16x3")
+    assert f.status() == "PSD_OK"
+    for b in range(batch):
+        lo = _lam(X[b], lam[b])
+        ref, _ = chain.project(X[b], *HALF, lam=lo)
+        # error on the problem's own scale lambda~ = ||X||_F: for n = 1, 2 every eigenvalue can be
+        # negative, and then ||P|| itself is filter-error sized (1/2 x (1 - s(1))) and a relative
+        # error says nothing
+        err = np.linalg.norm(P[b] - ref) / lo
+        assert err <= 1e-5, (b, err)
+        assert np.array_equal(P[b], P[b].T)
+        if n == 1:                                     # the scalar case: P = relu(x) up to the filter error
+            assert abs(P[b][0, 0] - max(X[b][0, 0], 0.0)) <= 1e-2 * abs(X[b][0, 0])
