@@ -356,6 +356,12 @@ def run_ours(args, cfg):
                          "frac_of_burst": (achieved / (peaks.get("bf16_tflops", 1590.0) / passes *
                                                        (1.0 if args.precision.startswith(("fp16", "bf16")) else 0.5)))
                                           if achieved else None},
+            # config c2 sits at the ridge: the small-n kernel's HBM fraction too -- one
+            # launch reads every X once and writes every P once (8 n^2 bytes per matrix)
+            **({"roofline_hbm": {"bound": "hbm", "achieved": 8.0 * n * n * count / (launch_ms / 1e3) / 1e9,
+                                 "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
+                                 "frac": 8.0 * n * n * count / (launch_ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}}
+               if (n <= 64 and launch_ms) else {}),
             "gpu_launches": kernel_launches,
             "clocks": clk.summary(),
         }
