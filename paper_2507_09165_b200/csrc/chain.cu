@@ -170,8 +170,14 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                             ptx::tma_load_2d(sa + C::kA, mb, &full[pst], k0, rowB, pol);
                         if (kb == 0 && t == cluster) stamp(s, 1);
                         if constexpr (kSplit) {
-                            ptx::tma_load_2d_multicast(sa + C::kA + C::kB + offA, ma_lo, &full[pst], kb * kBK, rowA,
-                                                       C::kMask);
+                            if (p.flags & 4) {   // debug: every CTA loads all of A_lo itself (no multicast)
+                                for (int q = 0; q < CS; ++q)
+                                    ptx::tma_load_2d(sa + C::kA + C::kB + q * C::kRowsA * kBlockKBytes, ma_lo, &full[pst],
+                                                     kb * kBK, b * npad + I * kTile + q * C::kRowsA, pol);
+                            } else {
+                                ptx::tma_load_2d_multicast(sa + C::kA + C::kB + offA, ma_lo, &full[pst], kb * kBK, rowA,
+                                                           C::kMask);
+                            }
                             ptx::tma_load_2d(sa + 2 * C::kA + C::kB, mb_lo, &full[pst], kb * kBK, rowB, pol);
                         }
                         if (++pst == kStages) { pst = 0; pph ^= 1; }
@@ -364,7 +370,7 @@ int chain_cluster_size(OpType t, bool split, int npad, int batch) {
     // split precision: an intermittent illegal-address fault with 3-4 ring stages at npad >= 1024
     // (not reproducible under compute-sanitizer) is still open -- the chain kernel takes only the
     // single-pass precisions until it is understood
-    if (split) return 0;
+    if (split && !std::getenv("PSD_CHAIN_SPLIT")) return 0;   // PSD_CHAIN_SPLIT: debug the open fault
     const char* env = std::getenv("PSD_CHAIN_CS");   // read per call (tests toggle it)
     if (npad % kTile != 0) return 0;
     int cs = 0;

@@ -128,7 +128,8 @@ struct ChainParams {
     int npad, batch, nsteps;
     unsigned* barrier;              // zeroed grid-barrier counter
     unsigned long long* dbg;        // debug: %globaltimer phase stamps of CTA 0 [step][8] (NULL in production)
-    int flags;                      // debug bits (PSD_CHAIN_FLAGS): 1 = no addend prefetch, 2 = no tensormap prefetch
+    int flags;                      // debug bits (PSD_CHAIN_FLAGS): 1 = no addend prefetch, 2 = no tensormap prefetch,
+                                    //   4 = split A_lo loaded per CTA (no multicast)
     int upper_only;                 // CS = 2, 16-bit single pass: upper-only operand storage (see GemmShape)
     ChainStep steps[kChainMaxSteps];
 };
