@@ -132,6 +132,12 @@ chain_kernel(const __grid_constant__ ChainParams p) {
 
     unsigned long long* dbg = (p.dbg && blockIdx.x == 0) ? p.dbg : nullptr;
     auto stamp = [&](int s, int k) { if (dbg) dbg[s * 8 + k] = ptx::globaltimer(); };
+    // debug: per-CTA progress words in host-mapped memory (survive a fault): [512 + 4 cta + role]
+    volatile unsigned long long* prog = p.dbg ? reinterpret_cast<volatile unsigned long long*>(p.dbg) + 512 + 4 * blockIdx.x : nullptr;
+    auto progress = [&](int role, int s, int kb, int extra) {
+        if (prog && !(role < 2 && (p.flags & 8))) { prog[role] = (1ull << 60) | (static_cast<unsigned long long>(s) << 40) |
+                                 (static_cast<unsigned long long>(kb & 0xFFFFF) << 20) | (extra & 0xFFFFF); __threadfence_system(); }
+    };
     for (int s = 0; s < p.nsteps; ++s) {
         const ChainStep& S = p.steps[s];
         if (threadIdx.x == 0) stamp(s, 0);
@@ -169,6 +175,7 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                         else
                             ptx::tma_load_2d(sa + C::kA, mb, &full[pst], k0, rowB, pol);
                         if (kb == 0 && t == cluster) stamp(s, 1);
+                        progress(0, s, kb, pst);
                         if constexpr (kSplit) {
                             if (p.flags & 4) {   // debug: every CTA loads all of A_lo itself (no multicast)
                                 for (int q = 0; q < CS; ++q)
@@ -200,6 +207,7 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                     for (int kb = 0; kb < num_kb; ++kb) {
                         ptx::mbar_wait(&full[mst], mph);
                         ptx::tc_fence_after();
+                        progress(1, s, kb, mst);
                         if (kb == 0 && t == cluster) stamp(s, 2);
                         const uint32_t sa = ptx::smem_u32(ring + mst * C::kStageBytes);
                         const bool a_mn = up && kb * kBK < tI * kTile;
@@ -272,11 +280,14 @@ chain_kernel(const __grid_constant__ ChainParams p) {
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tmem_empty[acc]);
+                if (threadIdx.x == 0) progress(2, s, 0, 0);
                 if (threadIdx.x == 0 && t == cluster) stamp(s, 5);
                 ++eit;
             }
         }
+        if (threadIdx.x == 0) progress(3, s, 0, 1);
         if (s + 1 < p.nsteps) grid_sync(p.barrier, static_cast<unsigned>(s + 1) * gridDim.x, dbg ? dbg + s * 8 + 6 : nullptr);
+        if (threadIdx.x == 0) progress(3, s, 0, 2);
     }
 
     // producer tail: every stage released by every cluster CTA (no remote arrive still in flight)

@@ -651,8 +651,10 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         if (e != cudaSuccess) return cuda_fail(e, "chain barrier reset");
         const bool dbg = !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
         unsigned long long* dbg_buf = nullptr;
-        if (dbg && cudaMalloc(&dbg_buf, kChainMaxSteps * 8 * 8) == cudaSuccess) {
-            cudaMemsetAsync(dbg_buf, 0, kChainMaxSteps * 8 * 8, st);
+        unsigned long long* dbg_host = nullptr;
+        if (dbg && cudaHostAlloc(&dbg_host, (512 + 4 * 512) * 8, cudaHostAllocMapped) == cudaSuccess) {
+            std::memset(dbg_host, 0, (512 + 4 * 512) * 8);
+            cudaHostGetDevicePointer(&dbg_buf, dbg_host, 0);
             cp->dbg = dbg_buf;
         }
         h->last_products = 1;
@@ -660,9 +662,23 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         if (e != cudaSuccess) return cuda_fail(e, "chain kernel");
         if (dbg_buf) {       // debug only: per-step phase stamps of CTA 0 (us since the step start)
             std::vector<unsigned long long> t(kChainMaxSteps * 8);
-            cudaStreamSynchronize(st);
-            cudaMemcpy(t.data(), dbg_buf, t.size() * 8, cudaMemcpyDeviceToHost);
-            cudaFree(dbg_buf);
+            cudaError_t se = cudaStreamSynchronize(st);
+            std::memcpy(t.data(), dbg_host, t.size() * 8);
+            {   // per-CTA progress words (host-mapped: readable after a fault)
+                int ctas = 0;
+                for (int c = 0; c < 512; ++c)
+                    if (dbg_host[512 + 4 * c] || dbg_host[512 + 4 * c + 1] || dbg_host[512 + 4 * c + 2] || dbg_host[512 + 4 * c + 3]) ctas = c + 1;
+                std::fprintf(stderr, "chain progress (sync: %s), %d CTAs:\n", cudaGetErrorString(se), ctas);
+                for (int c = 0; c < ctas; ++c) {
+                    std::fprintf(stderr, "  cta %3d:", c);
+                    const char* nm[4] = {"prod", "mma", "epi", "bar"};
+                    for (int r = 0; r < 4; ++r) {
+                        const unsigned long long w = dbg_host[512 + 4 * c + r];
+                        std::fprintf(stderr, " %s s%llu kb%llu x%llu", nm[r], (w >> 40) & 0xFFFFF, (w >> 20) & 0xFFFFF, w & 0xFFFFF);
+                    }
+                    std::fprintf(stderr, "\n");
+                }
+            }
             for (size_t si = 0; si < steps.size(); ++si) {
                 const unsigned long long* q = &t[si * 8];
                 auto d = [&](int k) { return q[k] ? (double(q[k]) - double(q[0])) * 1e-3 : -1.0; };
