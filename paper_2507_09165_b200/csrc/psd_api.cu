@@ -133,9 +133,10 @@ struct psd_filter_s {
     // pipelined host-buffer projection (psd_project_host)
     struct HostPipe {
         cudaStream_t s[3] = {nullptr, nullptr, nullptr};   // h2d, compute, d2h
-        static constexpr int kSlots = 3;         // chunk buffers in flight (H2D / project / D2H)
-        float* dx[kSlots] = {};
-        float* dout[kSlots] = {};
+        static constexpr int kMaxSlots = 8;      // chunk buffers in flight (H2D / project / D2H)
+        float* dx[kMaxSlots] = {};
+        float* dout[kMaxSlots] = {};
+        int nslots = 0;
         size_t chunk_bytes = 0;
     } hp;
     // profiling / launch accounting
@@ -882,6 +883,7 @@ void free_hostpipe(psd_filter_s* h) {
     for (auto& p : hp.dout) { if (p) cudaFree(p); p = nullptr; }
     for (auto& q : hp.s) { if (q) cudaStreamDestroy(q); q = nullptr; }
     hp.chunk_bytes = 0;
+    hp.nslots = 0;
 }
 
 void free_rowpanel(psd_filter_s* h) {
@@ -1407,12 +1409,18 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
     auto& hp = h->hp;
     const size_t mat = static_cast<size_t>(n) * n * sizeof(float);
     cudaError_t e;
-    if (hp.chunk_bytes < per * mat) {
+    // chunk buffers: enough that the host-to-device copies never wait for a device-to-host copy to
+    // free a slot (both copy directions are the bound at c4, profiles/r1s3_e2e_bound.md)
+    int slots = std::min<int>(6, chunks + 1);
+    if (const char* v = std::getenv("PSD_HOST_SLOTS")) slots = std::atoi(v);   // A/B only
+    slots = std::max(1, std::min(slots, psd_filter_s::HostPipe::kMaxSlots));
+    if (hp.chunk_bytes < per * mat || hp.nslots != slots) {
         free_hostpipe(h);
         for (int i = 0; i < 3; ++i)
             if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "cudaStreamCreate");
-        for (int i = 0; i < psd_filter_s::HostPipe::kSlots; ++i) {
+        hp.nslots = slots;
+        for (int i = 0; i < slots; ++i) {
             if (cudaMalloc(&hp.dx[i], per * mat) != cudaSuccess || cudaMalloc(&hp.dout[i], per * mat) != cudaSuccess) {
                 free_hostpipe(h);
                 return fail(PSD_ENOMEM, "cudaMalloc host-pipeline buffers failed");
@@ -1426,7 +1434,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
     cudaEvent_t start = ev();
     cudaEventRecord(start, user);
     for (auto q : hp.s) cudaStreamWaitEvent(q, start, 0);
-    cudaEvent_t freed[psd_filter_s::HostPipe::kSlots] = {};
+    cudaEvent_t freed[psd_filter_s::HostPipe::kMaxSlots] = {};
     std::vector<cudaEvent_t> used = {start};
     // chunk boundaries: the first and the last chunk are half-size (the pipeline's fill -- the first
     // host-to-device copy -- and its drain -- the last device-to-host copy -- are not overlapped)
@@ -1444,7 +1452,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
         }
     }
     for (size_t c = 0; c < parts.size(); ++c) {
-        const int slot = static_cast<int>(c % psd_filter_s::HostPipe::kSlots);
+        const int slot = static_cast<int>(c % hp.nslots);
         const int64_t b0 = parts[c].first;
         const int64_t nb = parts[c].second;
         if (freed[slot]) cudaStreamWaitEvent(hp.s[0], freed[slot], 0);
@@ -1465,7 +1473,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
         cudaEvent_t outd = ev();
         used.push_back(outd);
         cudaEventRecord(outd, hp.s[2]);
-        freed[slot] = outd;      // chunk c+kSlots may reuse this slot's X and out buffers after the D2H
+        freed[slot] = outd;      // chunk c+nslots may reuse this slot's X and out buffers after the D2H
     }
     cudaEvent_t done = ev();
     used.push_back(done);
