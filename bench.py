@@ -105,7 +105,35 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
+    # NVML clocks-event reason bits (nvml.h): sw_power_cap 0x4, hw_slowdown 0x8,
+    # sw_thermal_slowdown 0x20, hw_thermal_slowdown 0x40
+    NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+
+    def _nvml_loop(self, handle, nv):
+        # polled every 2 ms so that short timed regions (c3: ~16 ms) still get samples
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
+                self.nvml_samples.append((sm, bits))
+            except Exception:
+                return
+            self.stop.wait(0.002)
+
     def __enter__(self):
+        self.nvml_samples = []
+        self.stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            handle = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.nvml_max = nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._nvml_loop, args=(handle, nv), daemon=True)
+            self.t.start()
+            self.nvml = True
+            return self
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -121,6 +149,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if getattr(self, "nvml", False):
+            self.stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -129,6 +161,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if getattr(self, "nvml", False) and self.nvml_samples:
+            reasons = {nm for _, bits in self.nvml_samples for nm, b in self.NVML_BITS.items() if bits & b}
+            sm = [float(c) for c, _ in self.nvml_samples]
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(self.nvml_max), "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml"}
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:

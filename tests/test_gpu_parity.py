@@ -318,6 +318,21 @@ def test_project_host_pipeline(pkg):
     assert torch.equal(Xh2, ref)
 
 
+@pytest.mark.parametrize("slots", [1, 2, 8])
+def test_project_host_slot_reuse(pkg, monkeypatch, slots):
+    """Fewer chunk buffers than chunks: a chunk's host-to-device copy waits for the device-to-host
+    copy of the chunk that last used its buffer (the `freed` events) -- results bitwise equal."""
+    X = synth.batch("goe", 256, 7, 37)
+    f = pkg.Filter(pkg.filters.half_filter())
+    Xh = torch.tensor(X, dtype=torch.float32).pin_memory()
+    ref = f.project(Xh.cuda()).cpu()
+    monkeypatch.setenv("PSD_HOST_SLOTS", str(slots))
+    for _ in range(2):
+        out = f.project_host(Xh, chunks=7)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+
+
 # Lanczos bound (Algorithm 2 line 1 + Theorem 2, P:L704-743; reading R21).  The GPU runs the
 # Krylov iteration on the operand copy of X / ||X||_F in fp32 vectors: lambda~ agrees with the
 # float64 oracle (oracle/bound.py) to the operand rounding (fp16: u = 2^-11 per entry; tf32 op
@@ -502,3 +517,15 @@ def test_boundary_sizes(pkg, n):
         assert np.array_equal(P[b], P[b].T)
         if n == 1:                                     # the scalar case: P = relu(x) up to the filter error
             assert abs(P[b][0, 0] - max(X[b][0, 0], 0.0)) <= 1e-2 * abs(X[b][0, 0])
+
+
+@pytest.mark.parametrize("prec", ["fp16", "fp16x3"])
+def test_small_scale_fold_bitwise(pkg, monkeypatch, prec):
+    """The small-n kernel folds each operand scale (a power of two) into alpha and beta; the
+    unfolded order (PSD_SMALL_NOFOLD) must give bitwise the same projection."""
+    X = torch.tensor(synth.batch("goe", 64, 9, 41), dtype=torch.float32).cuda()
+    folded = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
+    monkeypatch.setenv("PSD_SMALL_NOFOLD", "1")
+    unfolded = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
+    torch.cuda.synchronize()
+    assert torch.equal(folded, unfolded)
