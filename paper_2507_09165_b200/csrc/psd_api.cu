@@ -458,6 +458,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         }
         sp_plan.s_x0 = static_cast<float>(sz);
         sp_plan.nofold = std::getenv("PSD_SMALL_NOFOLD") != nullptr ? 1 : 0;
+        sp_plan.mirror_scalar = std::getenv("PSD_SMALL_MIRROR_SCALAR") != nullptr ? 1 : 0;
         for (size_t i = 0; i < steps.size(); ++i) {
             const Step& s = steps[i];
             SmallStep& q = sp_plan.steps[i];

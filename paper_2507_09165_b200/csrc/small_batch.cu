@@ -123,6 +123,42 @@ __device__ __forceinline__ void mirror_block_task(uint8_t* part, int task) {
     }
 }
 
+// The same mirror, four 8x8 blocks per warp instruction: ldmatrix.x4.trans reads upper blocks
+// (bj, bi) transposed and stmatrix.x4 writes them as blocks (bi, bj); lanes 8q..8q+7 address the
+// rows of block q.  Group g of a 64x64 part: g < 7 the off-diagonal blocks 4g..4g+3 (row-major over
+// the strict lower block triangle), g = 7, 8 the diagonal blocks 4(g-7)..+3, which merge their
+// plain and transposed loads (upper part kept).  The 8 row addresses of a block hit 8 distinct
+// 16-byte chunks of the SW128 rows: conflict-free.  Fragment of lane t: row t/4, columns 2(t%4)+{0,1}.
+constexpr int kMirrorGroups = 9;
+__device__ __forceinline__ void mirror_group_warp(uint8_t* part, int g, int lane) {
+    const int q = lane >> 3, rr = lane & 7;
+    int bi, bj;
+    if (g < 7) {
+        const int k = 4 * g + q;                       // 0..27
+        bi = 1;
+        while (k >= bi * (bi + 1) / 2) ++bi;
+        bj = k - bi * (bi - 1) / 2;
+    } else {
+        bi = bj = 4 * (g - 7) + q;
+    }
+    const uint32_t src = ptx::smem_u32(part + swz(8 * bj + rr, bi));
+    const uint32_t dst = ptx::smem_u32(part + swz(8 * bi + rr, bj));
+    uint32_t t[4];
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]) : "r"(src) : "memory");
+    if (g >= 7) {
+        uint32_t nrm[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(nrm[0]), "=r"(nrm[1]), "=r"(nrm[2]), "=r"(nrm[3]) : "r"(src) : "memory");
+        const int r = lane >> 2, c = 2 * (lane & 3);
+        const uint32_t mask = ((c >= r) ? 0xFFFFu : 0u) | ((c + 1 >= r) ? 0xFFFF0000u : 0u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] = (nrm[i] & mask) | (t[i] & ~mask);
+    }
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};"
+                 :: "r"(dst), "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]) : "memory");
+}
+
 template <bool kSplit>
 __device__ __forceinline__ void add_row(const uint8_t* slot, int row, int half, float beta, float (&v)[32]) {
     // v += beta * (hi [+ lo]) of the slot row, columns [32 half, 32 half + 32)
@@ -348,10 +384,19 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     // rounding-level asymmetry is not amplified -- rounding model)
                     __syncthreads();
                     constexpr int kParts = kSplit ? 2 : 1;
-                    for (int task = threadIdx.x; task < 2 * kParts * 36; task += kThreadsS) {
-                        const int mm = task / (kParts * 36);
-                        const int part = (task / 36) % kParts;
-                        mirror_block_task(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes, task % 36);
+                    if (plan.mirror_scalar) {     // A/B baseline (PSD_SMALL_MIRROR_SCALAR)
+                        for (int task = threadIdx.x; task < 2 * kParts * 36; task += kThreadsS) {
+                            const int mm = task / (kParts * 36);
+                            const int part = (task / 36) % kParts;
+                            mirror_block_task(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes, task % 36);
+                        }
+                    } else {
+                        for (int task = warp; task < 2 * kParts * kMirrorGroups; task += kWarps) {
+                            const int mm = task / (kParts * kMirrorGroups);
+                            const int part = (task / kMirrorGroups) % kParts;
+                            mirror_group_warp(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes,
+                                              task % kMirrorGroups, lane);
+                        }
                     }
                 }
                 fence_proxy_async_smem();

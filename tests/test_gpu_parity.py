@@ -529,3 +529,16 @@ def test_small_scale_fold_bitwise(pkg, monkeypatch, prec):
     unfolded = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
     torch.cuda.synchronize()
     assert torch.equal(folded, unfolded)
+
+
+@pytest.mark.parametrize("prec", ["fp16", "fp16x3"])
+def test_small_mirror_ldmatrix_bitwise(pkg, monkeypatch, prec):
+    """The stage-output mirror of the small-n kernel (one warp per 8x8 block, ldmatrix.trans /
+    stmatrix) moves the same bits as the per-thread block mirror (PSD_SMALL_MIRROR_SCALAR)."""
+    X = torch.tensor(synth.batch("goe", 61, 11, 43), dtype=torch.float32).cuda()
+    warp = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
+    monkeypatch.setenv("PSD_SMALL_MIRROR_SCALAR", "1")
+    scalar = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
+    torch.cuda.synchronize()
+    assert torch.equal(warp, scalar)
+    assert torch.equal(warp, warp.transpose(1, 2))
