@@ -322,9 +322,10 @@ def run_ours(args, cfg):
     host_out = torch.empty_like(host_in, pin_memory=True)
     if not args.no_e2e:
         e2e_steps = max(1, min(args.steps, 5))
-        # 16 chunks (2 matrices each at c4): pipeline fill/drain is 1/16 of a step (measured,
-        # tools/e2e_probe.py: 4 chunks 511, 8 570, 16 625 matrices/s; pinned copies 55.6 GB/s)
-        chunks = min(16, count)
+        # 32 chunks (one matrix each at c4): the host path is PCIe-duplex-bound and the
+        # pipeline's fill/drain shrinks with the chunk (tools/e2e_probe.py: 4 chunks 511, 8 570,
+        # 16 625 matrices/s; tools/ab_host_slots.py: 32 vs 16 chunks 49.2 vs 50.0 ms median)
+        chunks = min(32, count)
         del X, out
         torch.cuda.empty_cache()
         f.project_host(host_in, host_out, chunks=chunks)

@@ -18,10 +18,10 @@ def timed(fn, reps=3):
     for _ in range(reps): fn()
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
-variants = [(3, 16), (6, 16), (8, 16), (6, 32), (8, 32)]
+variants = [tuple(map(int, v.split(","))) for v in (sys.argv[1:] or ["3,16", "6,16", "8,16", "6,32", "8,32"])]
 res = {v: [] for v in variants}
 ref = None
-for rnd in range(3):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "3"))):
     for slots, chunks in variants:
         os.environ["PSD_HOST_SLOTS"] = str(slots)
         res[(slots, chunks)].append(timed(lambda: f.project_host(Xh, out=Oh, chunks=chunks)))
