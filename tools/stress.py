@@ -13,13 +13,19 @@ from paper_2507_09165_b200 import Filter, filters
 TOL = {"fp16": 5e-3, "bf16": 3e-2, "tf32": 5e-3, "fp16x3": 1e-5, "bf16x3": 1e-4}
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 2025)
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+small = len(sys.argv) > 3 and sys.argv[3] == "small"     # n <= 64 sweep
 t0 = time.time()
 worst = {}
 fails = 0
 for c in range(cases):
-    n = int(rng.choice([65, 96, 130, 255, 257, 384, 511, 640, 777, 1000, 1024, 1100, 1280, 1536, 2048]))
-    batch = int(rng.integers(1, 13 if n <= 1100 else 6))
-    prec = str(rng.choice(["fp16", "fp16", "bf16", "tf32", "fp16x3", "bf16x3"]))
+    if small:   # the batched small-n kernel (n <= 64, fp16 / fp16x3) and its neighbours
+        n = int(rng.choice([3, 8, 17, 31, 33, 48, 63, 64, 64]))
+        batch = int(rng.integers(1, 600))
+    else:
+        n = int(rng.choice([65, 96, 130, 255, 257, 384, 511, 640, 777, 1000, 1024, 1100, 1280, 1536, 2048]))
+        batch = int(rng.integers(1, 13 if n <= 1100 else 6))
+    prec = str(rng.choice(["fp16", "fp16x3", "fp16", "fp16x3", "bf16", "tf32"] if small else
+                          ["fp16", "fp16", "bf16", "tf32", "fp16x3", "bf16x3"]))
     fam = str(rng.choice(["goe", "haar", "sdp_shaped", "dominant"]))
     mode = str(rng.choice(["project", "project", "sign", "admm"]))
     single = prec.endswith("x3")
@@ -52,7 +58,9 @@ for c in range(cases):
             errs.append(np.linalg.norm(P[b] - ref) / np.linalg.norm(ref))
             assert np.array_equal(P[b], P[b].T)
     e = max(errs)
-    bar = TOL[prec] * (10 if mode == "sign" and single else 1) * (2 if n < 96 else 1)
+    # n < 64: the test suite's small-n bar (4x, TOL_SMALL_N: the fp16 rounding model of this
+    # algorithm reaches 1.6e-2 on 8x8 inputs)
+    bar = TOL[prec] * (10 if mode == "sign" and single else 1) * (2 if n < 96 else 1) * (4 if n < 64 else 1)
     if mode == "sign" and fam == "dominant" and not single:
         # the paper's failure family: eigenvalues ~1e-3 sit in the filter's transition
         # region, where S is ill-conditioned -- the bar is the rounding model: 3 x the change of the
