@@ -1,5 +1,5 @@
 """A/B of an epilogue switch at c4 on the same GPU, alternating (graphs off so the env var is read
-per call): python tools/ab_probe.py ENV_VAR  -- runs with and without ENV_VAR=1, 3 rounds each."""
+per call): python tools/ab_probe.py ENV_VAR[=VALUE]  -- runs with and without ENV_VAR=1, 3 rounds each."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -8,7 +8,8 @@ import torch
 import bench
 import synth
 from paper_2507_09165_b200 import Filter, filters
-var = sys.argv[1]
+var, _, val = sys.argv[1].partition("=")   # VAR or VAR=VALUE
+val = val or "1"
 prec = sys.argv[2] if len(sys.argv) > 2 else "fp16"
 cfg = bench.CONFIGS["c4"]
 X = bench.make_inputs(cfg, 0, 32, synth.SEED_BASE).cuda()
@@ -22,7 +23,7 @@ res = {"off": [], "on": []}
 for rnd in range(3):
     for mode in ["off", "on"]:
         if mode == "on":
-            os.environ[var] = "1"
+            os.environ[var] = val
         else:
             os.environ.pop(var, None)
         f.project(X, out=out)
