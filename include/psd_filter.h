@@ -61,9 +61,12 @@ typedef enum {
  * *X3 (split precision, the FP32-class path standing in for the paper's FP32 /
  * BF16x9-emulated products): every operand is stored as hi + lo in the
  * operand type (fp16 with a per-buffer power-of-two scale that keeps lo in the normal
- * range) and each product is hi*hi + hi*lo + lo*hi, three tcgen05.mma passes into one fp32
- * accumulator.  FP16X3 runs at the fp16 rate (3 passes), TF32X3 at the tf32 rate.
- * Readings R11, R17, R19 in DESIGN.md. */
+ * range) and each product is hi*hi + hi*lo + lo*hi, three tcgen05.mma passes into fp32
+ * accumulators.  The tensor cores' fp32 accumulator loses ~2^-24 relative per accumulating
+ * MMA (error linear in K: 1.7e-5 for one n = 4096 product), so the split precisions
+ * accumulate K in runs of psd_filter_set_accum_chunk elements (default 512), each from zero,
+ * summed with round-to-nearest fp32 adds (reading R23).  FP16X3 runs at the fp16 rate
+ * (3 passes), TF32X3 at the tf32 rate.  Readings R11, R17, R19, R23 in DESIGN.md. */
 typedef enum {
     PSD_PREC_FP16 = 0,
     PSD_PREC_BF16 = 1,
@@ -122,6 +125,14 @@ psd_status_t psd_filter_set_bound(psd_filter_t h, psd_bound_t bound);
 /* PSD_BOUND_LANCZOS parameters: steps in [1, 64] (default 20; min(steps, n) are
  * run), safety in [1, 2] (default 1.01).  Host only; PSD_EINVAL outside the ranges. */
 psd_status_t psd_filter_set_lanczos(psd_filter_t h, int steps, double safety);
+
+/* Split (*X3) precisions only: accumulate each product's K range in independent runs of
+ * `kchunk` elements (a multiple of 64, at least 64), summed round-to-nearest in fp32 by the
+ * epilogue (reading R23); 0 = one hardware accumulation over the whole K (the
+ * pre-R23 behaviour, error ~4e-9 * n).  The 1-CTA product kernel (few-tile problems) splits K
+ * into at most 512 / tile-width runs of equal length instead.  Default 512.  Host only;
+ * PSD_EINVAL for other values. */
+psd_status_t psd_filter_set_accum_chunk(psd_filter_t h, int64_t kchunk);
 
 /* Number of tensor-core products one matrix costs: sum_t (d_t+1)/2 over stages with
  * d_t > 1, plus 1 if `for_project` (the reconstruction of P:L757).  Host only.

@@ -61,7 +61,8 @@ class Filter:
               (pass lambda_in).
     """
 
-    def __init__(self, stages, eps=1e-3, precision="fp16", bound="frobenius", lanczos_steps=20, lanczos_safety=1.01):
+    def __init__(self, stages, eps=1e-3, precision="fp16", bound="frobenius", lanczos_steps=20, lanczos_safety=1.01,
+                 accum_chunk=None):
         self._lib = load()
         self.stages = [tuple(float(v) for v in c) for c in stages]
         degrees, coeffs = filters.flatten(self.stages)
@@ -76,6 +77,12 @@ class Filter:
         check(self._lib.psd_filter_set_precision(self._h, PRECISIONS[precision]), "psd_filter_set_precision")
         check(self._lib.psd_filter_set_bound(self._h, BOUNDS[bound]), "psd_filter_set_bound")
         check(self._lib.psd_filter_set_lanczos(self._h, int(lanczos_steps), float(lanczos_safety)), "psd_filter_set_lanczos")
+        if accum_chunk is not None:
+            self.set_accum_chunk(accum_chunk)
+
+    def set_accum_chunk(self, kchunk):
+        """Split (x3) precisions: K elements per independent accumulation run (0 = one run)."""
+        check(self._lib.psd_filter_set_accum_chunk(self._h, int(kchunk)), "psd_filter_set_accum_chunk")
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -98,6 +105,10 @@ class Filter:
         if outb.shape != Xb.shape:
             raise ValueError("out shape mismatch")
         B, n = Xb.shape[0], Xb.shape[-1]
+        for name, lam in (("lambda_in", lambda_in), ("lambda_out", lambda_out)):
+            if lam is not None and not (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64
+                                        and lam.is_contiguous() and lam.numel() == B):
+                raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of batch elements")
         li = ctypes.c_void_p(lambda_in.data_ptr()) if lambda_in is not None else None
         lo = ctypes.c_void_p(lambda_out.data_ptr()) if lambda_out is not None else None
         check(self._lib.psd_project_ex(self._h, ctypes.c_void_p(Xb.data_ptr()), n, B,

@@ -8,7 +8,10 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libpsdfilter.so")
+# PSD_LIB_VARIANT=debug selects libpsdfilter_dbg.so (build(debug=True)): the same sources with
+# -DPSD_DEBUG, i.e. the experiment switches and kernel phase stamps; never used by tests or bench
+LIB_PATH = os.path.join(_PKG, "lib", "libpsdfilter_dbg.so" if os.environ.get("PSD_LIB_VARIANT") == "debug"
+                        else "libpsdfilter.so")
 
 PSD_OK, PSD_EINVAL, PSD_ENOMEM, PSD_ECUDA, PSD_ENCCL, PSD_ENONFINITE, PSD_EUNSUPPORTED = range(7)
 STATUS_NAMES = {0: "PSD_OK", 1: "PSD_EINVAL", 2: "PSD_ENOMEM", 3: "PSD_ECUDA", 4: "PSD_ENCCL",
@@ -26,6 +29,7 @@ SIGNATURES = [
     ("psd_filter_set_precision", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_filter_set_bound", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_filter_set_lanczos", _c.c_int, [_c.c_void_p, _c.c_int, _c.c_double]),
+    ("psd_filter_set_accum_chunk", _c.c_int, [_c.c_void_p, _c.c_int64]),
     ("psd_filter_gemm_count", _c.c_int, [_c.c_void_p, _c.c_int]),
     ("psd_project", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
     ("psd_sign", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libpsdfilter.so")
-SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "chain.cu", "bound_scale.cu", "small_batch.cu", "rowpanel.cu", "certificate.cu"]
+SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "bound_scale.cu", "small_batch.cu", "rowpanel.cu", "certificate.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
@@ -29,30 +29,34 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False):
-    os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
+def build(verbose=False, force=False, debug=False):
+    """libpsdfilter.so; with debug=True libpsdfilter_dbg.so (-DPSD_DEBUG: the experiment switches
+    and kernel phase stamps of DESIGN.md section 7, selected by PSD_LIB_VARIANT=debug)."""
+    objdir = os.path.join(LIBDIR, "obj_dbg" if debug else "obj")
+    lib = os.path.join(LIBDIR, "libpsdfilter_dbg.so") if debug else LIB
+    os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "psd_filter.h"))
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(LIBDIR, "obj", src.replace(".cu", ".o"))
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC] + ARCH + FLAGS + ["-c", s, "-o", o]
+            cmd = [NVCC] + ARCH + FLAGS + (["-DPSD_DEBUG"] if debug else []) + ["-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or r.returncode != 0:
                 sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed for " + src)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    print(build(verbose=True, force="--force" in sys.argv, debug="--debug" in sys.argv))

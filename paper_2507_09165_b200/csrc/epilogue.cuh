@@ -397,7 +397,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
         }
     }
     if (diag32) symmetrize_block(v, wsmem);
-    if (e.dbg_nostore) {                             // debug experiment only: keep v live, store nothing
+    if (kDebug && e.dbg_nostore) {                             // debug experiment only: keep v live, store nothing
         float acc = 0.0f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc += v[i];

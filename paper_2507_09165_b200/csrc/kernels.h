@@ -2,11 +2,23 @@
 // sm_100a kernels.  Not part of the public ABI (include/psd_filter.h is).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <vector>
 
 namespace psd {
+
+// Experiment / A-B switches and phase stamps exist only in the debug build (-DPSD_DEBUG,
+// libpsdfilter_dbg.so): the production library never reads the environment and its kernels
+// carry no stamp code (every `if (kDebug && ...)` folds away).
+#ifdef PSD_DEBUG
+constexpr bool kDebug = true;
+inline const char* debug_env(const char* name) { return std::getenv(name); }
+#else
+constexpr bool kDebug = false;
+inline const char* debug_env(const char*) { return nullptr; }
+#endif
 
 enum class OpType : int { F16 = 0, BF16 = 1, TF32 = 2 };
 
@@ -80,6 +92,11 @@ struct GemmShape {
     // (MN-major) from the stored upper tile, and the epilogue skips the mirrored stores of
     // off-diagonal tiles (half the operand stores and DRAM writes)
     int upper_only;
+    // K-chunked accumulation (split / FP32-class precisions): the tensor cores' fp32 accumulator
+    // loses ~2^-24 relative per accumulating MMA (error linear in K, profiles/r1s3_accumulation_error.txt),
+    // so each run of `kchunk` K elements is accumulated from zero and the runs are summed with
+    // round-to-nearest fp32 adds in the epilogue warps.  0: one accumulation over the whole K.
+    int kchunk;
 };
 
 // Visiting order of the upper 256-tiles of one matrix (host side), by name:
@@ -111,31 +128,6 @@ cudaError_t launch_sym_gemm_2cta(OpType t, bool split, const OperandMaps& m, con
 // Whether (n, batch) runs on the CTA-pair kernel, and the padded size it needs.
 bool use_pair_kernel(int64_t n, int64_t batch);
 int64_t padded_n(int64_t n, int64_t batch);
-
-// Persistent chain kernel (chain.cu): every product of one projection in ONE launch for the
-// few-tile regime (n < 1024 or few 256-tiles).  A cluster of CS CTAs owns a 128 x 128 upper tile,
-// CTA r computing its columns [r*BN, (r+1)*BN), BN = 128 / CS, with the A row panel split in CS
-// slices multicast to the whole cluster (each CTA reads 1/CS of A from L2); a grid barrier
-// separates consecutive products.
-constexpr int kChainMaxSteps = 48;
-constexpr int kChainMaps = 12;            // [0, 6): high parts of the operand buffers, [6, 12): low parts
-struct ChainStep {
-    int a, b;                 // operand buffer ids (map index; + 6 for the low part)
-    EpiParams ep;
-};
-struct ChainParams {
-    CUtensorMap map[kChainMaps];    // box rows 128 / CS = BN: the multicast A slices and the B rows
-    int npad, batch, nsteps;
-    unsigned* barrier;              // zeroed grid-barrier counter
-    unsigned long long* dbg;        // debug: %globaltimer phase stamps of CTA 0 [step][8] (NULL in production)
-    int flags;                      // debug bits (PSD_CHAIN_FLAGS): 1 = no addend prefetch, 2 = no tensormap prefetch,
-                                    //   4 = split A_lo loaded per CTA (no multicast)
-    int upper_only;                 // CS = 2, 16-bit single pass: upper-only operand storage (see GemmShape)
-    ChainStep steps[kChainMaxSteps];
-};
-// Cluster size for (npad, batch): 4 or 2, or 0 when the chain kernel cannot run it.
-int chain_cluster_size(OpType t, bool split, int npad, int batch);
-cudaError_t launch_chain(OpType t, bool split, int cs, const ChainParams& p, cudaStream_t stream);
 
 // Batched small-n path (n <= 64), the whole chain in one kernel (small_batch.cu).
 struct SmallStep {

@@ -54,8 +54,7 @@ struct Workspace {
     double* lambda = nullptr;
     unsigned* status = nullptr;
     CUtensorMap tmap[2 * B_COUNT];
-    CUtensorMap tmap64[2 * B_COUNT];        // 64-row boxes: B operand of the 128 x 64 tiles, chain kernel CS = 2
-    CUtensorMap tmap32[2 * B_COUNT];        // 32-row boxes: chain kernel CS = 4
+    CUtensorMap tmap64[2 * B_COUNT];        // 64-row boxes: B operand of the 128 x 64 tiles, transposed loads
     int nblk = 0;
     uint32_t* tiles = nullptr;     // CTA-pair tile visiting order (device)
     int tiles_per_matrix = 0;
@@ -124,10 +123,10 @@ struct psd_filter_s {
     };
     std::vector<GraphEntry> graphs;
     uint64_t graph_clock = 0;
-    bool use_graphs = std::getenv("PSD_NO_GRAPH") == nullptr;
-    // persistent chain kernel (few-tile regime): opt-in (PSD_CHAIN=1) -- measured no faster than
-    // one launch per product at c3 (grid barrier + pipeline refill per product)
-    bool use_chain = std::getenv("PSD_CHAIN") != nullptr && std::getenv("PSD_NO_CHAIN") == nullptr;
+    bool use_graphs = debug_env("PSD_NO_GRAPH") == nullptr;
+    // K-chunked accumulation of the split (FP32-class) precisions, K elements per chunk
+    // (psd_filter_set_accum_chunk; 0 = one accumulation over the whole K)
+    int kchunk = 512;
     cudaStream_t capture_stream = nullptr;
     bool capturing = false;
     // pipelined host-buffer projection (psd_project_host)
@@ -240,6 +239,7 @@ psd_status_t ensure_lz(psd_filter_s* h, int npad, int batch) {
     if (h->capturing) return fail(PSD_ECUDA, "Lanczos scratch must exist before capture");
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    free_graphs(h);          // captured Lanczos launches point into the old scratch
     if (ws.lz_scratch) cudaFree(ws.lz_scratch);
     ws.lz_scratch = nullptr;
     ws.lz_bytes = 0;
@@ -279,8 +279,7 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) cudaMemset(ws.op_buf[i], 0, mat * op_bytes(op));
     for (int i = 0; i < (split ? 2 : 1) * B_COUNT; ++i) {
         if (!make_operand_tmap(&ws.tmap[i], ws.op_buf[i], op, npad, batch) ||
-            !make_operand_tmap(&ws.tmap64[i], ws.op_buf[i], op, npad, batch, 64) ||
-            !make_operand_tmap(&ws.tmap32[i], ws.op_buf[i], op, npad, batch, 32)) {
+            !make_operand_tmap(&ws.tmap64[i], ws.op_buf[i], op, npad, batch, 64)) {
             free_ws(ws);
             return fail(PSD_ECUDA, "cuTensorMapEncodeTiled failed");
         }
@@ -293,7 +292,7 @@ psd_status_t ensure_ws(psd_filter_s* h, int npad, int batch) {
             // visiting order of the upper 256-tiles: row-major up to 16 tile rows (n <= 4096: the
             // panels in flight fit L2 either way), 8 x 8 super-tiles beyond (n = 16384: 79-82 vs
             // 91-97 ms per projection, tools/gemm_probe.py); PSD_TILE_ORDER overrides
-            const char* env_order = std::getenv("PSD_TILE_ORDER");
+            const char* env_order = debug_env("PSD_TILE_ORDER");
             make_tile_order(nt, env_order ? env_order : (nt > 16 ? "grouped8" : "row"), order.data());
             if (cudaMalloc(&ws.tiles, order.size() * 4) != cudaSuccess) {
                 free_ws(ws);
@@ -392,7 +391,7 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
 // GemmShape::upper_only): 16-bit operands, on the CTA-pair kernel or on the 1-CTA kernel without
 // split-K.
 bool upper_only_mode(const psd_filter_s* h, int n, int batch, int npad) {
-    if (op_of(h->prec) == OpType::TF32 || std::getenv("PSD_NO_UPPER_ONLY")) return false;
+    if (op_of(h->prec) == OpType::TF32 || debug_env("PSD_NO_UPPER_ONLY")) return false;
     if (npad % 256 == 0 && use_pair_kernel(n, batch)) return true;
     return sym_gemm_split_k(npad, batch, op_of(h->prec)) == 1;
 }
@@ -457,8 +456,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             sp_plan.sigma2 = admm->sigma;
         }
         sp_plan.s_x0 = static_cast<float>(sz);
-        sp_plan.nofold = std::getenv("PSD_SMALL_NOFOLD") != nullptr ? 1 : 0;
-        sp_plan.mirror_scalar = std::getenv("PSD_SMALL_MIRROR_SCALAR") != nullptr ? 1 : 0;
+        sp_plan.nofold = debug_env("PSD_SMALL_NOFOLD") != nullptr ? 1 : 0;
+        sp_plan.mirror_scalar = debug_env("PSD_SMALL_MIRROR_SCALAR") != nullptr ? 1 : 0;
         for (size_t i = 0; i < steps.size(); ++i) {
             const Step& s = steps[i];
             SmallStep& q = sp_plan.steps[i];
@@ -496,7 +495,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             evs = {take_event(h), take_event(h)};
             cudaEventRecord(evs.first, st);
         }
-        const bool dbg = !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        const bool dbg = !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
             sp_plan.dbg = reinterpret_cast<unsigned long long*>(ws.partial);
             cudaMemsetAsync(ws.partial, 0, 64, st);
@@ -582,20 +581,16 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     e = cudaMemsetAsync(ws.counters, 0, steps.size() * sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
+    shape.kchunk = split ? h->kchunk : 0;
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
     if (h->profiling && !h->capturing && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
     }
     const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
-    const int chain_cs = (!pair && h->use_chain && !steps.empty() && steps.size() <= static_cast<size_t>(kChainMaxSteps))
-                             ? chain_cluster_size(ws.op, split, npad, batch)
-                             : 0;
-    // the chain's operand copies hold only their upper tiles (16-bit operands; CTA-pair kernel,
-    // 1-CTA kernel without split-K, chain kernel with 2-CTA clusters)
-    const bool upper_only = chain_cs ? (chain_cs == 2 && !split && ws.op != OpType::TF32 &&
-                                        std::getenv("PSD_NO_UPPER_ONLY") == nullptr)
-                                     : upper_only_mode(h, n, batch, npad);
+    // the chain's operand copies hold only their upper tiles (16-bit operands; CTA-pair kernel or
+    // 1-CTA kernel without split-K)
+    const bool upper_only = upper_only_mode(h, n, batch, npad);
     shape.upper_only = upper_only ? 1 : 0;
     auto make_ep = [&](const Step& s) {
         EpiParams ep{};
@@ -627,84 +622,16 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             ep.strideF = static_cast<int64_t>(n) * n;
             ep.nF = n;
         }
-        ep.dbg_nostore = std::getenv("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug experiment
+        ep.dbg_nostore = debug_env("PSD_DEBUG_NOSTORE") != nullptr ? 1 : 0;   // debug build only
         ep.upper_only = upper_only ? 1 : 0;
         return ep;
     };
-    if (chain_cs) {
-        // (a3-a6) every product in one persistent launch (chain.cu)
-        std::unique_ptr<ChainParams> cp(new ChainParams());
-        const CUtensorMap* src = chain_cs == 4 ? ws.tmap32 : ws.tmap64;
-        for (int i = 0; i < B_COUNT; ++i) {
-            cp->map[i] = src[i];
-            cp->map[i + kChainMaps / 2] = src[split ? i + B_COUNT : i];
-        }
-        cp->npad = npad;
-        cp->batch = batch;
-        cp->nsteps = static_cast<int>(steps.size());
-        cp->flags = std::getenv("PSD_CHAIN_FLAGS") ? std::atoi(std::getenv("PSD_CHAIN_FLAGS")) : 0;
-        cp->upper_only = upper_only ? 1 : 0;
-        cp->barrier = reinterpret_cast<unsigned*>(ws.counters + (kMaxSteps - 1));
-        for (size_t si = 0; si < steps.size(); ++si) {
-            cp->steps[si].a = steps[si].A;
-            cp->steps[si].b = steps[si].B;
-            cp->steps[si].ep = make_ep(steps[si]);
-        }
-        e = cudaMemsetAsync(cp->barrier, 0, sizeof(unsigned), st);
-        if (e != cudaSuccess) return cuda_fail(e, "chain barrier reset");
-        const bool dbg = !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
-        unsigned long long* dbg_buf = nullptr;
-        unsigned long long* dbg_host = nullptr;
-        if (dbg && cudaHostAlloc(&dbg_host, (512 + 4 * 512) * 8, cudaHostAllocMapped) == cudaSuccess) {
-            std::memset(dbg_host, 0, (512 + 4 * 512) * 8);
-            cudaHostGetDevicePointer(&dbg_buf, dbg_host, 0);
-            cp->dbg = dbg_buf;
-        }
-        h->last_products = 1;
-        e = launch_chain(ws.op, split, chain_cs, *cp, st);
-        if (e != cudaSuccess) return cuda_fail(e, "chain kernel");
-        if (dbg_buf) {       // debug only: per-step phase stamps of CTA 0 (us since the step start)
-            std::vector<unsigned long long> t(kChainMaxSteps * 8);
-            cudaError_t se = cudaStreamSynchronize(st);
-            std::memcpy(t.data(), dbg_host, t.size() * 8);
-            {   // per-CTA progress words (host-mapped: readable after a fault)
-                int ctas = 0;
-                for (int c = 0; c < 512; ++c)
-                    if (dbg_host[512 + 4 * c] || dbg_host[512 + 4 * c + 1] || dbg_host[512 + 4 * c + 2] || dbg_host[512 + 4 * c + 3]) ctas = c + 1;
-                std::fprintf(stderr, "chain progress (sync: %s), %d CTAs:\n", cudaGetErrorString(se), ctas);
-                for (int c = 0; c < ctas; ++c) {
-                    std::fprintf(stderr, "  cta %3d:", c);
-                    const char* nm[4] = {"prod", "mma", "epi", "bar"};
-                    for (int r = 0; r < 4; ++r) {
-                        const unsigned long long w = dbg_host[512 + 4 * c + r];
-                        std::fprintf(stderr, " %s s%llu kb%llu x%llu", nm[r], (w >> 40) & 0xFFFFF, (w >> 20) & 0xFFFFF, w & 0xFFFFF);
-                    }
-                    std::fprintf(stderr, "\n");
-                }
-            }
-            for (size_t si = 0; si < steps.size(); ++si) {
-                const unsigned long long* q = &t[si * 8];
-                auto d = [&](int k) { return q[k] ? (double(q[k]) - double(q[0])) * 1e-3 : -1.0; };
-                const double nxt = si + 1 < steps.size() ? (double(t[(si + 1) * 8]) - double(q[0])) * 1e-3 : -1.0;
-                std::fprintf(stderr, "chain step %2zu (cs %d): first TMA %.2f, first full %.2f, last MMA %.2f, acc ready %.2f, "
-                             "epilogue done %.2f, barrier arrive %.2f, next step %.2f us\n", si, chain_cs, d(1), d(2), d(3), d(4),
-                             d(5), d(6), nxt);
-            }
-        }
-        h->kernel_launches += 1;
-        if (evp.first) {
-            cudaEventRecord(evp.second, st);
-            h->ev_pairs.push_back(evp);
-            h->product_launches_profiled += 1;      // one launch carries every product
-        }
-        return PSD_OK;
-    }
     h->last_products = static_cast<int64_t>(steps.size());
     for (size_t si = 0; si < steps.size(); ++si) {
         const Step& s = steps[si];
         shape.counter = ws.counters + si;
         EpiParams ep = make_ep(s);
-        const bool dbg = pair && !h->capturing && std::getenv("PSD_DEBUG_STAMPS") != nullptr;
+        const bool dbg = pair && !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
             ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial + batch * 128);
             cudaMemsetAsync(ep.dbg, 0, 128, st);
@@ -763,11 +690,6 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         if (h->bound == PSD_BOUND_LANCZOS) {
             rc = ensure_lz(h, static_cast<int>(padded_n(n64, batch64)), static_cast<int>(batch64));
             if (rc != PSD_OK) return rc;
-        }
-        {   // kernel attributes / occupancy queries of the chain kernel happen outside the capture
-            const int npad = static_cast<int>(padded_n(n64, batch64));
-            if (n64 > 64 && !(npad % 256 == 0 && use_pair_kernel(n64, batch64)))
-                chain_cluster_size(op_of(h->prec), split_of(h->prec), npad, static_cast<int>(batch64));
         }
         if (!h->capture_stream) {
             cudaError_t e = cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking);
@@ -1001,7 +923,7 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
         m.b_t = m.b_lo_t = ws.tmap64[s.B];
         // upper-only operand storage (16-bit): the unpack writes each gathered tile without its
         // mirror and the loader reads the left part of a panel transposed
-        const bool upper_only = ws.op != OpType::TF32 && std::getenv("PSD_NO_UPPER_ONLY") == nullptr;
+        const bool upper_only = ws.op != OpType::TF32 && debug_env("PSD_NO_UPPER_ONLY") == nullptr;
         const int r0 = comm ? rank : 0, r1 = comm ? rank + 1 : nranks;
         for (int vr = r0; vr < r1; ++vr) {
             const size_t slot0 = static_cast<size_t>(vr) * rp.per * tile_elems;
@@ -1307,6 +1229,14 @@ psd_status_t psd_filter_set_lanczos(psd_filter_t h, int steps, double safety) {
     return PSD_OK;
 }
 
+psd_status_t psd_filter_set_accum_chunk(psd_filter_t h, int64_t kchunk) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (kchunk < 0 || kchunk % 64 || kchunk > (1 << 20)) return fail(PSD_EINVAL, "kchunk must be 0 or a positive multiple of 64");
+    if (h->kchunk != static_cast<int>(kchunk)) free_graphs(h);   // captured launches carry the old value
+    h->kchunk = static_cast<int>(kchunk);
+    return PSD_OK;
+}
+
 int psd_filter_gemm_count(psd_filter_t h, int for_project) {
     if (!h) return -1;
     int g = 0;
@@ -1413,7 +1343,7 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
     // chunk buffers: enough that the host-to-device copies never wait for a device-to-host copy to
     // free a slot (both copy directions are the bound at c4, profiles/r1s3_e2e_bound.md)
     int slots = std::min<int>(6, chunks + 1);
-    if (const char* v = std::getenv("PSD_HOST_SLOTS")) slots = std::atoi(v);   // A/B only
+    if (const char* v = debug_env("PSD_HOST_SLOTS")) slots = std::atoi(v);   // A/B only
     slots = std::max(1, std::min(slots, psd_filter_s::HostPipe::kMaxSlots));
     if (hp.chunk_bytes < per * mat || hp.nslots != slots) {
         free_hostpipe(h);
@@ -1444,10 +1374,11 @@ psd_status_t psd_project_host(psd_filter_t h, const float* X_host, int64_t n, in
         int64_t b0 = 0;
         const int64_t edge = (chunks >= 4 && per >= 2) ? per / 2 : per;
         while (b0 < batch) {
-            const bool first = parts.empty();
-            int64_t nb = first ? edge : per;
-            if (batch - b0 - nb > 0 && batch - b0 - nb < per) nb = batch - b0 - edge;   // leave a half-size tail
-            if (nb <= 0 || nb > batch - b0) nb = batch - b0;
+            const int64_t rem = batch - b0;
+            int64_t nb = parts.empty() ? edge : per;
+            // leave a half-size tail; never more than `per` matrices (the slot buffers' size)
+            if (rem - nb > 0 && rem - nb < per) nb = std::max<int64_t>(1, std::min(per, rem - edge));
+            nb = std::min(nb, rem);
             parts.emplace_back(b0, nb);
             b0 += nb;
         }
@@ -1613,10 +1544,11 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     ep.ldF = n;
     ep.strideF = static_cast<int64_t>(n) * n;
     ep.nF = n;
-    if (std::getenv("PSD_DEBUG_STAMPS")) ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial);  // debug only
+    if (debug_env("PSD_DEBUG_STAMPS")) ep.dbg = reinterpret_cast<unsigned long long*>(ws.partial);  // debug only
     e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
-    const GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
+    GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
+    shape.kchunk = split ? h->kchunk : 0;
     const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
     const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     OperandMaps m;

@@ -63,7 +63,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define DBG_STAMP(i) do { if (e.dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) e.dbg[i] = gtimer(); } while (0)
+#define DBG_STAMP(i) do { if (kDebug && e.dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) e.dbg[i] = gtimer(); } while (0)
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -92,6 +92,10 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     constexpr int kBK = kBlockKBytes / Tr::kBytes;     // K elements per block (64 f16 / 32 tf32)
     constexpr int kUmmaK = 32 / Tr::kBytes;            // K per tcgen05.mma (16 f16 / 8 tf32)
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, BN);
+    // split precisions (KS = 1): the K range is cut into up to 512 / BN runs, each accumulated from
+    // zero in its own TMEM columns and summed round-to-nearest in the epilogue (GemmShape::kchunk)
+    constexpr bool kRuns = kSplit && KS == 1;
+    constexpr uint32_t kCols = kRuns ? 512 : BN;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
@@ -123,7 +127,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         }
         __syncwarp();
     } else if (warp == 1) {
-        ptx::tmem_alloc<BN>(tmem_slot);
+        ptx::tmem_alloc<kCols>(tmem_slot);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -137,6 +141,10 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     const int kb0 = krank * num_kb;
     const int rowA = b * s.npad + I * kTile;
     const int rowB = b * s.npad + J * BN;
+    int nruns = 1;
+    if (kRuns && s.kchunk > 0) nruns = min(static_cast<int>(kCols / BN), (s.npad + s.kchunk - 1) / s.kchunk);
+    const int run_kb = (num_kb + nruns - 1) / nruns;    // K blocks per accumulation run
+    nruns = (num_kb + run_kb - 1) / run_kb;
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -190,20 +198,22 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 const uint64_t bdesc = desc(sa + kTileBytes, b_mn);
                 const uint32_t idesc = kIdesc | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
                 const uint64_t astep = a_mn ? (2048 >> 4) : (32 >> 4), bstep = b_mn ? (2048 >> 4) : (32 >> 4);
-                auto mma = [&](uint64_t a, uint64_t bb, uint32_t accumulate) {
+                auto mma = [&](uint32_t d, uint64_t a, uint64_t bb, uint32_t accumulate) {
                     if constexpr (T == OpType::TF32)
-                        ptx::mma_tf32(tmem_base, a, bb, kIdesc, accumulate);
+                        ptx::mma_tf32(d, a, bb, kIdesc, accumulate);
                     else
-                        ptx::mma_f16(tmem_base, a, bb, idesc, accumulate);
+                        ptx::mma_f16(d, a, bb, idesc, accumulate);
                 };
+                const int kr = kb % run_kb;                   // position in its accumulation run
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>((kb / run_kb) * BN);
 #pragma unroll
                 for (int k = 0; k < kBK / kUmmaK; ++k) {
-                    mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
+                    mma(d_tmem, adesc + k * astep, bdesc + k * bstep, (kr | k) != 0);
                     if constexpr (kSplit) {
                         const uint64_t alo = desc(sa + kTileBytes + kBBytes, a_mn);
                         const uint64_t blo = desc(sa + 2 * kTileBytes + kBBytes, b_mn);
-                        mma(adesc + k * astep, blo + k * bstep, 1u);            // A_hi B_lo
-                        mma(alo + k * astep, bdesc + k * bstep, 1u);            // A_lo B_hi
+                        mma(d_tmem, adesc + k * astep, blo + k * bstep, 1u);    // A_hi B_lo
+                        mma(d_tmem, alo + k * astep, bdesc + k * bstep, 1u);    // A_lo B_hi
                     }
                 }
                 ptx::mma_commit(&empty[st]);
@@ -231,8 +241,20 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
             const int gj0 = J * BN + c0;
             if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
             uint32_t raw[32];
-            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
+            const uint32_t tl = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0;
+            ptx::tmem_ld_32x32b_x32(tl, raw);
             ptx::tmem_ld_wait();
+            if constexpr (kRuns) {
+                // the K runs in order, round-to-nearest fp32 adds
+                for (int r = 1; r < nruns; ++r) {
+                    uint32_t part[32];
+                    ptx::tmem_ld_32x32b_x32(tl + static_cast<uint32_t>(r * BN), part);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        raw[i] = __float_as_uint(__fadd_rn(__uint_as_float(raw[i]), __uint_as_float(part[i])));
+                }
+            }
             epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
         }
     } else {
@@ -290,7 +312,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<BN>(tmem_base);
+        ptx::tmem_dealloc<kCols>(tmem_base);
     }
     DBG_STAMP(5);
 }
@@ -313,7 +335,7 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
     int na = 0;
-    static const bool pdl = !std::getenv("PSD_NO_PDL");
+    static const bool pdl = !debug_env("PSD_NO_PDL");
     if (pdl) {
         attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[na].val.programmaticStreamSerializationAllowed = 1;
@@ -349,7 +371,7 @@ int sym_gemm_split_k(int npad, int batch, OpType t) {
     // measured (tools/latency_probe.py, n = 1024, 19 products): KS = 1 211 us, 2 229 us, 4 386 us --
     // the cluster barriers / DSMEM reduction cost more than the extra SMs gain once the epilogue
     // is vectorised, so split-K is off unless forced (PSD_SPLITK = 2 | 4)
-    static const int forced = std::getenv("PSD_SPLITK") ? std::atoi(std::getenv("PSD_SPLITK")) : 1;
+    static const int forced = debug_env("PSD_SPLITK") ? std::atoi(debug_env("PSD_SPLITK")) : 1;
     if (forced == 1 || forced == 2 || forced == 4) return forced;
     const int nt = npad / kTile;
     const int tiles = nt * (nt + 1) / 2 * batch;
@@ -361,7 +383,7 @@ int sym_gemm_split_k(int npad, int batch, OpType t) {
 
 // 128 x 64 tiles for few-tile problems: twice the CTAs, half the MMA and epilogue per CTA.
 int sym_gemm_bn(int npad, int batch) {
-    static const int forced = std::getenv("PSD_BN") ? std::atoi(std::getenv("PSD_BN")) : 0;
+    static const int forced = debug_env("PSD_BN") ? std::atoi(debug_env("PSD_BN")) : 0;
     if (forced == 64 || forced == 128) return forced;
     const int nt = npad / kTile;
     return (nt * (nt + 1) / 2 * batch < 100) ? 64 : 128;

@@ -12,7 +12,9 @@
 //   * warp roles: w0 TMA producer, w1 MMA issuer (leader CTA only), w2 TMEM allocator,
 //     w4..w7 epilogue (one TMEM lane quadrant each);
 //   * TMEM holds two 256-column fp32 accumulators (all 512 columns), so the epilogue of
-//     tile i overlaps the mainloop of tile i+1;
+//     tile i overlaps the mainloop of tile i+1; split precisions instead use columns [0, 256) for
+//     K-chunk runs (accumulated from zero every GemmShape::kchunk K elements) and [256, 512) for
+//     their round-to-nearest sum, folded by the epilogue warps while the next run accumulates;
 //   * kStages-deep smem ring, 32 KB per stage per CTA (A 16 KB + B 16 KB, SW128);
 //   * dynamic tile scheduler: the leader's producer takes tile ids from a global counter and
 //     broadcasts them to both CTAs through an mbarrier-guarded smem ring;
@@ -84,6 +86,9 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
     const bool leader = (rank == 0);
     const int total_tiles = s.tiles_per_matrix * s.batch;
     const int num_kb = s.npad / kBK;
+    // K blocks per accumulation run: split precisions restart the accumulator every s.kchunk K
+    // elements (GemmShape::kchunk); otherwise one run per tile
+    const int chunk_kb = (kSplit && s.kchunk >= kBK) ? s.kchunk / kBK : num_kb;
 
     if (warp == 0 && ptx::elect_one()) {
         ptx::tma_prefetch_desc(&tm.a);
@@ -187,28 +192,38 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             int st = 0;
             uint32_t ph = 0;
             int it = 0;
-            // debug phase counters (e.dbg): cycles waiting for a tile id, a free accumulator,
-            // operand stages; total cycles in the loop
-            unsigned long long w_tile = 0, w_tmem = 0, w_full = 0;
-            const unsigned long long t_start = clock64();
-            unsigned long long g_start = 0;
-            if (e.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+            int cc = 0;                  // accumulation runs issued (one per tile, or per K chunk)
+            // debug build only: cycles waiting for a tile id, a free accumulator, operand stages;
+            // total cycles in the loop
+            unsigned long long w_tile = 0, w_tmem = 0, w_full = 0, t_start = 0, g_start = 0;
+            if (kDebug && e.dbg) {
+                t_start = clock64();
+                g_start = ptx::globaltimer();
+            }
             for (;; ++it) {
-                unsigned long long c0 = e.dbg ? clock64() : 0;
+                unsigned long long c0 = (kDebug && e.dbg) ? clock64() : 0;
                 const int t = next_tile(it);
                 release_tile(it);
-                if (e.dbg) { const unsigned long long c1 = clock64(); w_tile += c1 - c0; c0 = c1; }
+                if (kDebug && e.dbg) { const unsigned long long c1 = clock64(); w_tile += c1 - c0; c0 = c1; }
                 if (t >= total_tiles) break;
                 int tb, tI, tJ;
                 decode_tile(t, s, tb, tI, tJ);
-                const int acc = it & 1;
-                const uint32_t acc_ph = (it >> 1) & 1;
-                ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
-                if (e.dbg) { const unsigned long long c1 = clock64(); w_tmem += c1 - c0; }
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * kT2;
+                int acc = 0;
+                uint32_t d_tmem = tmem_base;
                 for (int kb = 0; kb < num_kb; ++kb) {
-                    if (e.dbg) {
+                    const int kc = kb % chunk_kb;          // position in the accumulation run
+                    if (kc == 0) {
+                        // a run starts from zero in a free accumulator: the split path's single chunk
+                        // buffer (the epilogue folds every run into its sum), else the tile ping-pong
+                        acc = kSplit ? 0 : (cc & 1);
+                        const uint32_t acc_ph = kSplit ? (cc & 1) : ((cc >> 1) & 1);
+                        if (kDebug && e.dbg) c0 = clock64();
+                        ptx::mbar_wait(&tmem_empty[acc], acc_ph ^ 1);
+                        if (kDebug && e.dbg) w_tmem += clock64() - c0;
+                        ptx::tc_fence_after();
+                        d_tmem = tmem_base + acc * kT2;
+                    }
+                    if (kDebug && e.dbg) {
                         const unsigned long long c2 = clock64();
                         ptx::mbar_wait(&full[st], ph);
                         w_full += clock64() - c2;
@@ -236,7 +251,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     };
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k) {
-                        mma(adesc + k * astep, bdesc + k * bstep, (kb | k) != 0);
+                        mma(adesc + k * astep, bdesc + k * bstep, (kc | k) != 0);
                         if constexpr (kSplit) {
                             const uint64_t alo = a_mn ? ptx::smem_desc_sw128_mnmajor(sa + 2 * kTileBytes1, kTileBytes1 / 2, 1024)
                                                       : ptx::smem_desc_sw128_kmajor(sa + 2 * kTileBytes1);
@@ -247,18 +262,20 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                         }
                     }
                     ptx::mma_commit_pair(&empty[st], 0x3);
-                    if (kb == num_kb - 1) ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                    if (kc == chunk_kb - 1 || kb == num_kb - 1) {
+                        ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                        ++cc;
+                    }
                     if (++st == kStages2) { st = 0; ph ^= 1; }
                 }
             }
-            if (e.dbg) {
+            if (kDebug && e.dbg) {
                 atomicAdd(e.dbg + 0, w_tile);
                 atomicAdd(e.dbg + 1, w_tmem);
                 atomicAdd(e.dbg + 2, w_full);
                 atomicAdd(e.dbg + 3, clock64() - t_start);
                 atomicAdd(e.dbg + 4, static_cast<unsigned long long>(it));
-                unsigned long long g_end;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+                const unsigned long long g_end = ptx::globaltimer();
                 atomicAdd(e.dbg + 7, 1ull);                                   // clusters
                 atomicMin(e.dbg + 8, g_start);                                // first start
                 atomicMax(e.dbg + 9, g_start);                                // last start
@@ -267,8 +284,12 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                 atomicMax(e.dbg + 12, static_cast<unsigned long long>(it));   // most tiles
             }
             // drain: the last accumulators must be read out before the pair tears down
-            for (int last = it - 2; last < it; ++last)
-                if (last >= 0) ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
+            if constexpr (kSplit) {
+                if (cc > 0) ptx::mbar_wait(&tmem_empty[0], (cc - 1) & 1);
+            } else {
+                for (int last = cc - 2; last < cc; ++last)
+                    if (last >= 0) ptx::mbar_wait(&tmem_empty[last & 1], (last >> 1) & 1);
+            }
         }
         __syncwarp();
     } else if (warp >= 4) {
@@ -277,6 +298,9 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
         uint8_t* wsmem = epi_smem + q * kEpiWarpSmemBytes;
         const uint32_t tmem_empty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[0]), 0);
         const uint32_t tmem_empty_leader1 = ptx::mapa_shared(ptx::smem_u32(&tmem_empty[1]), 0);
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const int nchunks = (num_kb + chunk_kb - 1) / chunk_kb;
+        int cc = 0;                                    // accumulation runs consumed
         for (int it = 0;; ++it) {
             const int t = next_tile(it);
             __syncwarp();
@@ -285,7 +309,6 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             if (t >= total_tiles) break;
             int b, I, J;
             decode_tile(t, s, b, I, J);
-            const int acc = it & 1;
             {
                 // addend rows of this thread (row gi0 + lane) for the whole tile into L2 while the
                 // tile's MMAs run (first column at or right of the diagonal on a diagonal tile)
@@ -293,32 +316,64 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                 const int c_lo = (I == J) ? ((gi - J * kT2) & ~31) : 0;
                 prefetch_addend_l2<T>(e, b, s.npad, gi, J * kT2 + c_lo, kT2 - c_lo);
             }
-            const unsigned long long e0 = (e.dbg && q == 0 && ptx::elect_one()) ? clock64() : 0;
-            ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
-            const unsigned long long e1 = e0 ? clock64() : 0;
-            ptx::tc_fence_after();
             const int gi0 = I * kT2 + static_cast<int>(rank) * kRowsPerCta + q * 32;
             const bool diag = (I == J);
+            const unsigned long long e0 = (kDebug && e.dbg && q == 0 && ptx::elect_one()) ? clock64() : 0;
+            uint32_t tsum;                             // TMEM columns the stores read the tile from
+            if constexpr (kSplit) {
+                // every K chunk's run lands in the chunk buffer (columns [0, 256)); fold it into the
+                // running sum (columns [256, 512)) with round-to-nearest fp32 adds and hand the
+                // buffer back, so the next run starts while this warp keeps folding / storing
+                const uint32_t tC = tmem_base + lane_off, tS = tmem_base + kT2 + lane_off;
+                for (int ch = 0; ch < nchunks; ++ch, ++cc) {
+                    ptx::mbar_wait(&tmem_full[0], cc & 1);
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int c0 = 0; c0 < kT2; c0 += 32) {
+                        if (diag && J * kT2 + c0 + 31 < gi0) continue;   // never stored
+                        uint32_t a[32], sum[32];
+                        ptx::tmem_ld_32x32b_x32(tC + c0, a);
+                        if (ch) ptx::tmem_ld_32x32b_x32(tS + c0, sum);
+                        ptx::tmem_ld_wait();
+                        if (ch) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) a[i] = __float_as_uint(__fadd_rn(__uint_as_float(sum[i]), __uint_as_float(a[i])));
+                        }
+                        ptx::tmem_st_32x32b_x32(tS + c0, a);
+                    }
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive_remote(tmem_empty_leader0);
+                }
+                tsum = tS;
+            } else {
+                const int acc = it & 1;
+                ptx::mbar_wait(&tmem_full[acc], (it >> 1) & 1);
+                ptx::tc_fence_after();
+                tsum = tmem_base + acc * kT2 + lane_off;
+            }
+            const unsigned long long e1 = e0 ? clock64() : 0;
             float alpha = e.alpha;
             if (e.alpha_dev) alpha *= static_cast<float>(e.alpha_dev[b]);
-            const uint32_t tbase = tmem_base + acc * kT2 + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
             for (int c0 = 0; c0 < kT2; c0 += 32) {
                 const int gj0 = J * kT2 + c0;
                 if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
                 uint32_t raw[32];
-                ptx::tmem_ld_32x32b_x32(tbase + c0, raw);
+                ptx::tmem_ld_32x32b_x32(tsum + c0, raw);
                 ptx::tmem_ld_wait();
                 const int64_t pk = e.packed ? static_cast<int64_t>(t) * (kT2 * kT2) +
                                               static_cast<int64_t>(gi0 - I * kT2) * kT2 + c0
                                             : -1;
                 epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem, pk);
             }
-            ptx::tc_fence_before();
-            ptx::mbar_arrive_remote(acc ? tmem_empty_leader1 : tmem_empty_leader0);
-            if (e0) {
-                atomicAdd(e.dbg + 5, e1 - e0);                 // epilogue warp 4 waiting for an accumulator
-                atomicAdd(e.dbg + 6, clock64() - e1);          // its epilogue work per tile
+            if constexpr (!kSplit) {
+                ptx::tc_fence_before();
+                ptx::mbar_arrive_remote((it & 1) ? tmem_empty_leader1 : tmem_empty_leader0);
+            }
+            if (kDebug && e0) {
+                atomicAdd(e.dbg + 5, e1 - e0);                 // epilogue warp 4 waiting for / folding accumulators
+                atomicAdd(e.dbg + 6, clock64() - e1);          // its store work per tile
             }
         }
     }

@@ -318,17 +318,18 @@ def test_project_host_pipeline(pkg):
     assert torch.equal(Xh2, ref)
 
 
-@pytest.mark.parametrize("slots", [1, 2, 8])
-def test_project_host_slot_reuse(pkg, monkeypatch, slots):
-    """Fewer chunk buffers than chunks: a chunk's host-to-device copy waits for the device-to-host
-    copy of the chunk that last used its buffer (the `freed` events) -- results bitwise equal."""
-    X = synth.batch("goe", 256, 7, 37)
+@pytest.mark.parametrize("n,batch,chunks", [(256, 7, 7), (128, 9, 4), (128, 13, 5), (96, 30, 7)])
+def test_project_host_chunking(pkg, n, batch, chunks):
+    """Chunk plans of psd_project_host (half-size first / last chunks, more chunks than the 6 chunk
+    buffers: a chunk's host-to-device copy waits for the device-to-host copy of the chunk that last
+    used its buffer) -- results bitwise equal to psd_project.  (9, 4) and (13, 5) are chunk plans
+    whose tail fix-up once produced a chunk larger than the buffers."""
+    X = synth.batch("goe", n, batch, 37 + batch)
     f = pkg.Filter(pkg.filters.half_filter())
     Xh = torch.tensor(X, dtype=torch.float32).pin_memory()
     ref = f.project(Xh.cuda()).cpu()
-    monkeypatch.setenv("PSD_HOST_SLOTS", str(slots))
     for _ in range(2):
-        out = f.project_host(Xh, chunks=7)
+        out = f.project_host(Xh, chunks=chunks)
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
 
@@ -400,50 +401,6 @@ def test_lanczos_bound_edge_cases(pkg):
     assert lam[0] == 0 and not P[0].any()
     assert lam[1] == pytest.approx(np.linalg.norm(X[1], 2), rel=1e-5)
     assert abs(lam[2] - 1.0) <= 2.0 ** -11
-
-
-def _with_env(var, value, fn):
-    import os
-    old = os.environ.get(var)
-    if value is None:
-        os.environ.pop(var, None)
-    else:
-        os.environ[var] = value
-    try:
-        return fn()
-    finally:
-        if old is None:
-            os.environ.pop(var, None)
-        else:
-            os.environ[var] = old
-
-
-@pytest.mark.parametrize("n,batch,which,prec,cs", [
-    (1024, 1, "c3", "fp16", None),            # config c3: the chain kernel's one-wave case
-    (1024, 1, "c3", "fp16", "2"),             # same with 2-CTA clusters (64-column CTAs)
-    (384, 24, "half", "fp16", None),          # 144 tiles: several tiles per cluster (double-buffered TMEM)
-    (640, 3, "single", "tf32", None),         # tf32 operands, ragged tile count
-])
-def test_chain_kernel_parity(pkg, n, batch, which, prec, cs):
-    """Persistent chain kernel (every product in one launch, grid barrier between products,
-    multicast A slices; opt-in, PSD_CHAIN=1) vs the oracle, and vs the per-product launches of the
-    same plan."""
-    X = synth.batch("goe", n, batch, synth.SEED_BASE + 13 * n)
-    run = lambda: _with_env("PSD_CHAIN", "1", lambda: _gpu(pkg, _product_filter(which, pkg), X, prec))
-    P, lam, f = _with_env("PSD_CHAIN_CS", cs, run)
-    assert f.status() == "PSD_OK"
-    st, kap = _oracle_filter(which)
-    bar = TOL_X3.get(prec) or tol(prec, n, which)
-    for b in sorted({0, batch // 2, batch - 1}):
-        ref, _ = chain.project(X[b], st, kap, lam=_lam(X[b], lam[b]))
-        assert _rel(P[b], ref) <= bar, (b, _rel(P[b], ref))
-    for b in range(batch):
-        assert np.array_equal(P[b], P[b].T)
-    # the same plan as one launch per product (the default): same operands, same K order per element
-    P2, lam2, _ = _gpu(pkg, _product_filter(which, pkg), X, prec)
-    assert np.array_equal(lam, lam2)
-    for b in range(batch):
-        assert _rel(P[b], P2[b]) <= 1e-6, (b, _rel(P[b], P2[b]))
 
 
 @pytest.fixture(scope="module")
@@ -519,36 +476,82 @@ def test_boundary_sizes(pkg, n):
             assert abs(P[b][0, 0] - max(X[b][0, 0], 0.0)) <= 1e-2 * abs(X[b][0, 0])
 
 
-@pytest.mark.parametrize("prec", ["fp16", "fp16x3"])
-def test_small_scale_fold_bitwise(pkg, monkeypatch, prec):
-    """The small-n kernel folds each operand scale (a power of two) into alpha and beta; the
-    unfolded order (PSD_SMALL_NOFOLD) must give bitwise the same projection."""
-    X = torch.tensor(synth.batch("goe", 64, 9, 41), dtype=torch.float32).cuda()
-    folded = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
-    monkeypatch.setenv("PSD_SMALL_NOFOLD", "1")
-    unfolded = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
+# FP32-class bar at the north-star sizes.  The tensor cores' fp32 accumulator loses ~2^-24 relative
+# per accumulating MMA (one n = 4096 product: 1.7e-5, profiles/r1s3_accumulation_error.txt); the
+# split path accumulates K in independent runs of 512 summed round-to-nearest (reading R23).
+@pytest.mark.parametrize("n,batch,family,prec", [
+    (2048, 1, "dominant", "fp16x3"),   # 1-CTA kernel (36 tiles): 4 K runs in separate TMEM columns
+    (2048, 1, "goe", "tf32x3"),
+    (2048, 3, "dominant", "fp16x3"),   # CTA-pair kernel (108 tiles): K chunks folded by the epilogue
+    (2048, 3, "goe", "tf32x3"),
+    (2560, 2, "sdp_shaped", "fp16x3"), # ragged for 256-tiles? (2560 = 10 x 256), pair kernel
+])
+def test_split_fp32_bar_large_n(pkg, n, batch, family, prec):
+    """The north-star FP32 bar (1e-5) at n >= 2048, incl. the paper's failure family."""
+    X = synth.batch(family, n, batch, 2948 + n)
+    P, lam, f = _gpu(pkg, pkg.filters.single_filter(), X, prec)
+    assert f.status() == "PSD_OK"
+    for b in sorted({0, batch - 1}):
+        ref, _ = chain.project(X[b], tables.F_SINGLE_REFINED, tables.single_kappas(10), lam=_lam(X[b], lam[b]))
+        assert _rel(P[b], ref) <= TOL_X3[prec], (b, _rel(P[b], ref))
+        assert np.array_equal(P[b], P[b].T)
+
+
+@pytest.mark.parametrize("n,batch", [(2048, 1), (4096, 1)])
+def test_split_accumulation_runs(pkg, n, batch):
+    """One split product C = X X with fp16-exact symmetric X (operand conversion exact, so only the
+    accumulation errs): K runs of 512 bring the relative error under 3e-6 on both product kernels
+    (n = 2048 batch 1: 1-CTA kernel; n = 4096: CTA-pair kernel), while one hardware accumulation over
+    K = n (kchunk 0) is ~4e-9 n (reading R23)."""
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((n, n))
+    X = ((G + G.T) / 2).astype(np.float16).astype(np.float64)
+    ref = X @ X
+    iu = np.triu_indices(n)
+    t = torch.tensor(X[None], dtype=torch.float32, device="cuda")
+    errs = {}
+    for kc in (0, 512):
+        f = pkg.Filter(pkg.filters.half_filter(), precision="fp16x3", accum_chunk=kc)
+        C = f.sym_product(t, t).double().cpu().numpy()[0]
+        errs[kc] = np.linalg.norm((C - ref)[iu]) / np.linalg.norm(ref[iu])
+        assert np.array_equal(C, C.T)
+    assert errs[512] <= 3e-6, errs
+    assert errs[0] >= 2e-9 * n, errs        # the hardware effect the runs remove (documents R23)
+
+
+@pytest.mark.parametrize("prec", ["fp16x3", "tf32x3"])
+def test_c4_full_size_structured_fp32(pkg, prec):
+    """Config c4 on the FP32-class path in bench.py's launch configuration: batch 32 x n = 4096,
+    f~*_single + kappa (T = 10, 31 products), sampled outputs vs the exact structured oracle at the
+    north-star 1e-5 bar; every output exactly symmetric."""
+    n, batch = 4096, 32
+    mats, blocks = [], []
+    for b in range(batch):
+        Xb, bl = synth.structured(n, synth.SEED_BASE + 19 * b, block=64,
+                                  family=("goe", "sdp_shaped", "dominant")[b % 3])
+        mats.append(Xb)
+        blocks.append(bl)
+    X = np.stack(mats)
+    P, lam, f = _gpu(pkg, _product_filter("single", pkg), X, prec)
+    assert f.status() == "PSD_OK"
+    for b in range(batch):
+        assert np.array_equal(P[b], P[b].T)
+    for b in [0, 1, 2, 17, 31]:
+        ref = spectral.structured_project(blocks[b], *SINGLE, _lam(X[b], lam[b]))
+        assert _rel(P[b], ref) <= TOL_X3[prec], (b, _rel(P[b], ref))
+
+
+def test_c5_full_size_structured_fp32(pkg, c5_input):
+    """Config c5 (one n = 16384) on the FP32-class path (fp16x3, f~*_single + kappa): sampled rows
+    vs the exact structured oracle at the 1e-5 bar."""
+    Xd, blocks, lam = c5_input
+    f = pkg.Filter(_product_filter("single", pkg), precision="fp16x3")
+    lam_d = torch.zeros(1, dtype=torch.float64, device="cuda")
+    P = f.project(Xd[None], lambda_out=lam_d)[0]
     torch.cuda.synchronize()
-    assert torch.equal(folded, unfolded)
-
-
-@pytest.mark.parametrize("prec", ["fp16", "fp16x3"])
-def test_small_mirror_ldmatrix_bitwise(pkg, monkeypatch, prec):
-    """The stage-output mirror of the small-n kernel (one warp per 8x8 block, ldmatrix.trans /
-    stmatrix) moves the same bits as the per-thread block mirror (PSD_SMALL_MIRROR_SCALAR)."""
-    X = torch.tensor(synth.batch("goe", 61, 11, 43), dtype=torch.float32).cuda()
-    warp = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
-    monkeypatch.setenv("PSD_SMALL_MIRROR_SCALAR", "1")
-    scalar = pkg.Filter(pkg.filters.c2_filter(), precision=prec).project(X)
-    torch.cuda.synchronize()
-    assert torch.equal(warp, scalar)
-    assert torch.equal(warp, warp.transpose(1, 2))
-
-
-@pytest.mark.xfail(strict=False, reason="FP32-class split path misses the 1e-5 bar at n >= 2048: tensor-core "
-                   "fp32 accumulation error grows ~n (DESIGN.md section 5, profiles/r1s3_split_precision_vs_n.txt)")
-def test_split_fp32_bar_large_n(pkg):
-    """The north-star FP32 bar (1e-5) at n = 2048 on the paper's failure family."""
-    X = synth.batch("dominant", 2048, 1, 2948)
-    P, lam, _ = _gpu(pkg, pkg.filters.single_filter(), X, "fp16x3")
-    ref, _ = chain.project(X[0], tables.F_SINGLE_REFINED, tables.single_kappas(10), lam=_lam(X[0], lam[0]))
-    assert _rel(P[0], ref) <= TOL_X3["fp16x3"], _rel(P[0], ref)
+    assert f.status() == "PSD_OK"
+    assert abs(float(lam_d[0]) - lam) <= 1e-9 * lam
+    rows = [0, 1, 2047, 2048, 5000, 8191, 12345, 16383]
+    Pr = P[rows].double().cpu().numpy()
+    ref = spectral.structured_project_rows(blocks, *SINGLE, lam, rows)
+    assert _rel(Pr, ref) <= TOL_X3["fp16x3"], _rel(Pr, ref)
