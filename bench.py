@@ -43,6 +43,55 @@ CONFIGS = {
 }
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def filter_name(cfg, precision):
+    """The paper's pairing: the split (FP32-class) precisions run
+    f~*_single (T = 10, 31 products), the 16-bit ones f~*_half (T = 7, 22 products)."""
+    if cfg["filter"] == "half" and precision.endswith("x3"):
+        return "single"
+    return cfg["filter"]
+
+
+def config_dict(cfg, args, world, count):
+    """The line's `config` -- identical in both arms (same workload, filter, products)."""
+    fname = filter_name(cfg, args.precision)
+    G = {"half": 22, "single": 31}.get(fname)
+    n = cfg["n"]
+    d = {"workload": cfg["workload"], "n": n, "global_batch": cfg["batch"], "per_gpu_batch": count,
+         "family": cfg["family"], "filter": fname, "precision": args.precision,
+         "parallelism": f"batch-sharded dp{world}" if cfg["batch"] > 1 else f"row-panel tp{world}",
+         "l2": "inputs > 126 MB L2 (no flush needed)" if n * n * 4 * count > 126e6 else "inputs smaller than L2"}
+    if G:
+        d["products_per_matrix"] = G
+    return d
+
+
+def maybe_spawn(args):
+    """`--gpus N` (N > 1) without a torchrun environment: re-run this command under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous) and return its exit code;
+    None when this process already is a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -239,9 +288,10 @@ def oracle_filter(name):
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    st, kap = oracle_filter(cfg["filter"])
+    st, kap = oracle_filter(filter_name(cfg, args.precision))
     per_step = max(5.0, 100.0 / max(args.steps + args.warmup, 1))
     vals = []
     threads, sample = 1, ""
@@ -254,10 +304,9 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "n": cfg["n"], "global_batch": cfg["batch"],
-                   "family": cfg["family"]},
+        "config": config_dict(cfg, args, world, cfg["batch"] // world if cfg["batch"] > 1 else 1),
         "cpu_baseline": {"value": value, "unit": "matrices/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "matrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -282,7 +331,7 @@ def run_ours(args, cfg):
         return run_rowpanel(args, cfg, world, rank, dev)
     first, count = pdist.shard_range(gb, world, rank)
 
-    stages = product_filter(cfg["filter"])
+    stages = product_filter(filter_name(cfg, args.precision))
     f = Filter(stages, precision=args.precision)
     G = f.gemm_count(True)
 
@@ -321,7 +370,7 @@ def run_ours(args, cfg):
     e2e_ms = None
     host_out = torch.empty_like(host_in, pin_memory=True)
     if not args.no_e2e:
-        e2e_steps = max(1, min(args.steps, 5))
+        e2e_steps = args.steps
         # 32 chunks (one matrix each at c4): the host path is PCIe-duplex-bound and the
         # pipeline's fill/drain shrinks with the chunk (tools/e2e_probe.py: 4 chunks 511, 8 570,
         # 16 625 matrices/s; tools/ab_host_slots.py: 32 vs 16 chunks 49.2 vs 50.0 ms median)
@@ -369,14 +418,14 @@ def run_ours(args, cfg):
             peak = peak_bf16 / 2.0 / passes
             peak_note = f"{peak_src} bf16 sustained x 1/2 (tf32 nominal ratio)" + (" / 3 passes" if passes == 3 else "")
         traffic, traffic_src = load_traffic(cfg)
+        # step-level fraction beside the kernel-level one: the method's flops of a whole step (this
+        # rank's shard) over the step time
+        step_achieved = alg_flops_product * G * count / (ms_step / 1000.0) / 1e12
         line = {
             "metric": "psd_projections_per_sec", "value": value, "unit": "matrices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": cfg["workload"], "n": n, "global_batch": gb, "per_gpu_batch": count,
-                       "family": cfg["family"], "filter": cfg["filter"], "products_per_matrix": G,
-                       "parallelism": f"batch-sharded dp{world}", "l2": "inputs 2.1 GB > 126 MB L2, no flush"
-                       if n * n * 4 * count > 126e6 else "inputs smaller than L2"},
+            "config": config_dict(cfg, args, world, count),
             "tflops_dense_equivalent": dense_flops_matrix * gb * args.steps / (ms / 1000.0) / 1e12,
             "tflops_algorithmic": alg_flops_product * G * gb * args.steps / (ms / 1000.0) / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -388,6 +437,10 @@ def run_ours(args, cfg):
                                                                        "product, fused epilogue)")),
                          "per_launch_flops": per_launch, "mma_passes": passes,
                          "avg_launch_ms": launch_ms, "peak_source": peak_note,
+                         "launch_timing": "CUDA events recorded by the graph's own event nodes around the "
+                                          "product run of every step (bound / scale excluded), summed over "
+                                          "the timed steps / product launches",
+                         "step_achieved": step_achieved, "step_frac": step_achieved / peak,
                          # context: the same achieved rate against the measured BURST bf16 figure
                          # (a kernel timed alone) and the executed flops (diagonal 256-tiles are
                          # computed whole: 136/128 of the triangle at n = 4096)
@@ -408,10 +461,10 @@ def run_ours(args, cfg):
                            "h2d_bytes_per_step": int(host_in.numel() * 4 * world),
                            "d2h_bytes_per_step": int(host_out.numel() * 4 * world)}
         if world == 1 and not args.no_cpu_baseline:
-            st, kap = oracle_filter(cfg["filter"])
+            st, kap = oracle_filter(filter_name(cfg, args.precision))
             v, threads, sample = cpu_oracle_sample(cfg, st, kap, seconds_cap=args.cpu_seconds)
             line["cpu_baseline"] = {"value": v, "unit": "matrices/s", "cores": threads, "kind": "oracle",
-                                    "sample": sample}
+                                    "cpu_model": cpu_model(), "sample": sample}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -426,7 +479,7 @@ def run_rowpanel(args, cfg, world, rank, dev):
     import synth
     from paper_2507_09165_b200 import Filter, dist as pdist
     n = cfg["n"]
-    f = Filter(product_filter(cfg["filter"]), precision=args.precision)
+    f = Filter(product_filter(filter_name(cfg, args.precision)), precision=args.precision)
     # p2p (default): each product kernel stores its tiles into every rank's region over NVLink
     # (no collective); nccl: packed tiles all-gathered with NCCL after each product
     rp = pdist.PeerRowPanelProjector(f, n) if args.rowpanel == "p2p" else pdist.RowPanelProjector(f, n)
@@ -490,6 +543,11 @@ def main():
     cfg = CONFIGS[args.config]
     if args.precision is None:
         args.precision = cfg.get("precision", "fp16")
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -120,6 +120,12 @@ struct psd_filter_s {
         cudaGraphExec_t exec;
         int64_t kernels, products;
         uint64_t last_use;
+        // the captured graph (kept: its event-record nodes bracket the product run, so profiling
+        // times the product kernels alone, not the whole sequence) and the nodes' own events
+        cudaGraph_t graph;
+        cudaGraphNode_t ev_node[2];
+        cudaEvent_t own[2];
+        bool borrowed;             // the nodes currently record profiling events from the pool
     };
     std::vector<GraphEntry> graphs;
     uint64_t graph_clock = 0;
@@ -129,6 +135,7 @@ struct psd_filter_s {
     int kchunk = 512;
     cudaStream_t capture_stream = nullptr;
     bool capturing = false;
+    cudaEvent_t cap_ev[2] = {nullptr, nullptr};   // during capture: record nodes around the product run
     // pipelined host-buffer projection (psd_project_host)
     struct HostPipe {
         cudaStream_t s[3] = {nullptr, nullptr, nullptr};   // h2d, compute, d2h
@@ -494,6 +501,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         if (h->profiling && !h->capturing) {
             evs = {take_event(h), take_event(h)};
             cudaEventRecord(evs.first, st);
+        } else if (h->capturing && h->cap_ev[0]) {
+            cudaEventRecordWithFlags(h->cap_ev[0], st, cudaEventRecordExternal);
         }
         const bool dbg = !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
@@ -515,6 +524,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             cudaEventRecord(evs.second, st);
             h->ev_pairs.push_back(evs);
             h->product_launches_profiled += 1;     // one launch carries the whole chain
+        } else if (h->capturing && h->cap_ev[1]) {
+            cudaEventRecordWithFlags(h->cap_ev[1], st, cudaEventRecordExternal);
         }
         return PSD_OK;
     }
@@ -586,6 +597,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     if (h->profiling && !h->capturing && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
         cudaEventRecord(evp.first, st);
+    } else if (h->capturing && h->cap_ev[0] && !steps.empty()) {
+        cudaEventRecordWithFlags(h->cap_ev[0], st, cudaEventRecordExternal);
     }
     const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
     // the chain's operand copies hold only their upper tiles (16-bit operands; CTA-pair kernel or
@@ -658,12 +671,21 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         cudaEventRecord(evp.second, st);
         h->ev_pairs.push_back(evp);
         h->product_launches_profiled += static_cast<int64_t>(steps.size());
+    } else if (h->capturing && h->cap_ev[1] && !steps.empty()) {
+        cudaEventRecordWithFlags(h->cap_ev[1], st, cudaEventRecordExternal);
     }
     return PSD_OK;
 }
 
+void free_graph_entry(psd_filter_s::GraphEntry& g) {
+    cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    for (auto e : g.own)
+        if (e) cudaEventDestroy(e);
+}
+
 void free_graphs(psd_filter_s* h) {
-    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : h->graphs) free_graph_entry(g);
     h->graphs.clear();
 }
 
@@ -696,31 +718,67 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
         }
         const int64_t k0 = h->kernel_launches, p0 = h->product_launches_profiled;
+        cudaEvent_t own[2] = {nullptr, nullptr};
+        if (cudaEventCreate(&own[0]) != cudaSuccess || cudaEventCreate(&own[1]) != cudaSuccess) {
+            for (auto x : own)
+                if (x) cudaEventDestroy(x);
+            return fail(PSD_ECUDA, "cudaEventCreate");
+        }
         cudaError_t e = cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
         h->capturing = true;
+        h->cap_ev[0] = own[0];
+        h->cap_ev[1] = own[1];
         rc = run_body(h, X, n64, batch64, out, lambda_in, lambda_out, want_sign, h->capture_stream);
         h->capturing = false;
+        h->cap_ev[0] = h->cap_ev[1] = nullptr;
         cudaGraph_t graph = nullptr;
         e = cudaStreamEndCapture(h->capture_stream, &graph);
-        if (rc != PSD_OK) {
+        auto drop = [&]() {
             if (graph) cudaGraphDestroy(graph);
+            for (auto x : own) cudaEventDestroy(x);
+        };
+        if (rc != PSD_OK) {
+            drop();
             return rc;
         }
-        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        if (e != cudaSuccess) {
+            drop();
+            return cuda_fail(e, "cudaStreamEndCapture");
+        }
+        // the event-record nodes bracketing the product run (absent for a product-free chain)
+        cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
+        {
+            size_t count = 0;
+            cudaGraphGetNodes(graph, nullptr, &count);
+            std::vector<cudaGraphNode_t> nodes(count);
+            if (count) cudaGraphGetNodes(graph, nodes.data(), &count);
+            for (auto nd : nodes) {
+                cudaGraphNodeType ty;
+                if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t ev = nullptr;
+                cudaGraphEventRecordNodeGetEvent(nd, &ev);
+                for (int i = 0; i < 2; ++i)
+                    if (ev == own[i]) ev_node[i] = nd;
+            }
+        }
         cudaGraphExec_t exec = nullptr;
         e = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+        if (e != cudaSuccess) {
+            drop();
+            return cuda_fail(e, "cudaGraphInstantiate");
+        }
         if (h->graphs.size() >= 8) {       // evict the least recently used
             size_t lru = 0;
             for (size_t i = 1; i < h->graphs.size(); ++i)
                 if (h->graphs[i].last_use < h->graphs[lru].last_use) lru = i;
-            cudaGraphExecDestroy(h->graphs[lru].exec);
+            free_graph_entry(h->graphs[lru]);
             h->graphs.erase(h->graphs.begin() + lru);
         }
         psd_filter_s::GraphEntry g{X, out, lambda_in, lambda_out, n64, batch64, static_cast<int>(want_sign), static_cast<int>(key_prec),
-                     static_cast<int>(key_bound), exec, h->kernel_launches - k0, 0, 0};
+                     static_cast<int>(key_bound), exec, h->kernel_launches - k0, 0, 0, graph,
+                     {ev_node[0], ev_node[1]}, {own[0], own[1]}, false};
+        if (!(ev_node[0] && ev_node[1])) g.ev_node[0] = g.ev_node[1] = nullptr;
         // the product count of the sequence (for profiling) = its number of product kernels
         g.products = h->last_products;
         h->kernel_launches = k0;
@@ -729,16 +787,28 @@ psd_status_t run(psd_filter_t h, const float* X, int64_t n64, int64_t batch64, f
         hit = &h->graphs.back();
     }
     hit->last_use = ++h->graph_clock;
+    // profiling: the graph's own record nodes around the product run are pointed at a fresh event
+    // pair for this launch, so the interval is the product kernels only (bound, scale, counter
+    // reset excluded)
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
-    if (h->profiling) {
+    cudaError_t e;
+    if (h->profiling && hit->ev_node[0]) {
         evp = {take_event(h), take_event(h)};
-        cudaEventRecord(evp.first, st);
+        if ((e = cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[0], evp.first)) != cudaSuccess ||
+            (e = cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[1], evp.second)) != cudaSuccess)
+            return cuda_fail(e, "cudaGraphExecEventRecordNodeSetEvent");
+        hit->borrowed = true;
+    } else if (hit->borrowed) {
+        // back to the graph's own events (the pool's may be reused elsewhere)
+        if ((e = cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[0], hit->own[0])) != cudaSuccess ||
+            (e = cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[1], hit->own[1])) != cudaSuccess)
+            return cuda_fail(e, "cudaGraphExecEventRecordNodeSetEvent");
+        hit->borrowed = false;
     }
-    cudaError_t e = cudaGraphLaunch(hit->exec, st);
+    e = cudaGraphLaunch(hit->exec, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
     h->kernel_launches += hit->kernels;
     if (evp.first) {
-        cudaEventRecord(evp.second, st);
         h->ev_pairs.push_back(evp);
         h->product_launches_profiled += hit->products;
     }

@@ -262,3 +262,25 @@ def test_rowpanel_p2p_world1():
         assert np.array_equal(out, out2)
     finally:
         tdist.destroy_process_group()
+
+
+def test_bench_spawns_ranks_cpu():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself under
+    torch.distributed.run with 2 local ranks (127.0.0.1 rendezvous); rank 0 alone prints the one JSON
+    line (here the reference arm, which needs no GPU) with n_gpus = 2 and the same config dict the
+    GPU arm prints."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "c3", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["filter"] == "c3" and d["config"]["n"] == 1024
+    assert d["cpu_baseline"]["cpu_model"] and d["cpu_baseline"]["cores"] >= 1

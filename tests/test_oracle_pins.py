@@ -246,3 +246,94 @@ def test_bound_is_upper_bound():
         assert np.abs(np.linalg.eigvalsh(X)).max() <= chain.frobenius_bound(X)
     A = synth.rng(1).standard_normal((6, 6))
     assert chain.frobenius_bound(A) == chain.frobenius_bound(np.triu(A) + np.triu(A, 1).T)
+
+
+# ------------------------------------------------------- pins added in round 2
+
+def _c2_stages():
+    """Config c2's T = 4, d = 7 Remez chain (data/remez_filters.json, written by tools/make_coeffs.py
+    from oracle/remez.py only)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data", "remez_filters.json")
+    with open(path) as f:
+        return [tuple(c) for c in json.load(f)["c2_T4_d7_eps1e-3"]["stages"]]
+
+
+@pytest.mark.parametrize("which,eps,rtol,chk10", [
+    ("c1", 1e-3, 1e-6, 0.860),      # f*_half stages 1-3 (config c1)
+    ("c2", 1e-3, 1e-9, 0.137),      # config c2 (T = 4, d = 7)
+    ("c3", 1e-3, 1e-4, 9.16e-4),    # f*_half stages 1-6 (config c3)
+    ("half", 1e-3, 2e-3, 5.8e-10),  # f*_half (Table 2, T = 7)
+])
+def test_sign_err_closed_form(which, eps, rtol, chk10):
+    """certify.sign_err (max over float32 x in [eps, 1] of |s(x) - 1|) equals the draft Theorem's
+    closed form 1 - a_{T+1} with a_1 = eps, a_{t+1} = f_t(a_t) (eq:10-11): for a
+    sequential-Remez chain (Algorithm 1) each stage maps [a_t, 2 - a_t] onto
+    [a_{t+1}, 2 - a_{t+1}], so the worst sign error sits at the interval ends.  SURVEY [chk-10]
+    values to 3 digits.  rtol follows the printed 10-digit coefficients (the T = 6, 7 chains are
+    flat to 1e-4 / 1e-9 and inherit the coefficient rounding)."""
+    st = {"c1": tables.F_HALF[:3], "c2": _c2_stages(), "c3": tables.F_HALF[:6], "half": tables.F_HALF}[which]
+    a = eps
+    for c in st:                           # a_{t+1} = f_t(a_t), the odd monomial sum written out
+        a = sum(cj * a ** (2 * j + 1) for j, cj in enumerate(c))
+    closed = 1.0 - a
+    e, am = certify.sign_err(st, eps)
+    assert abs(e - closed) <= rtol * closed, (e, closed)
+    assert abs(closed - chk10) <= 5e-3 * chk10 + 1e-12
+    assert eps <= am <= 1.0
+    assert e >= abs(float(chain.scalar_chain(np.float32(0.5), st)) - 1.0)   # a maximum over [eps, 1]
+
+
+def test_sign_err_window():
+    """sign_err only looks at [eps, 1]: below eps s(x) -> 0 (s is odd, s(0) = 0), so a window that
+    started at 0 would report ~1; a larger eps can only shrink the maximum (nested windows)."""
+    st = tables.F_HALF
+    e3, _ = certify.sign_err(st, 1e-3)
+    e2, _ = certify.sign_err(st, 1e-2)
+    e_tiny, am = certify.sign_err(st, 1e-6)
+    assert e2 <= e3 < 1e-8
+    assert e_tiny > 0.99 and am < 1e-3
+
+
+@pytest.mark.parametrize("X,expected", [
+    ([[3.0, 0.0], [0.0, 4.0]], 5.0),                          # diag(3, 4): the 3-4-5 triangle
+    ([[1.0, 2.0], [2.0, 1.0]], np.sqrt(10.0)),               # off-diagonal counted twice
+    ([[1.0, 2.0], [99.0, 1.0]], np.sqrt(10.0)),              # lower triangle never read (R10)
+    ([[2.0, 1.0, 2.0], [0.0, 2.0, 1.0], [0.0, 0.0, 2.0]], np.sqrt(24.0)),
+    ([[0.0]], 0.0),
+])
+def test_frobenius_bound_exact(X, expected):
+    """lambda~ = ||X||_F = sqrt(sum_ij x_ij^2) of the upper-triangle symmetric X (R10),
+    exact small-integer cases: a missing sqrt, an upper-triangle-only sum or a read of the lower
+    triangle each fails one of them."""
+    assert chain.frobenius_bound(np.array(X)) == expected
+
+
+@pytest.mark.parametrize("family,which", [("goe", "half"), ("haar", "half"), ("sdp_shaped", "single"),
+                                          ("goe", "c1"), ("dominant", "half")])
+def test_idempotence_bound(family, which):
+    """Idempotence error bound (BASELINE north star): with e = relu_err (Eq. comp:error-approx,
+    P:L583-590), P(X) = Q g(L) Q^T and g(l) >= -lam~ e, and P(P(X)) = Q g'(g(L)) Q^T with
+    |g'(m) - relu(m)| <= lam~' e (lam~' = ||P(X)||_F bounds its spectrum), so eigenvalue-wise
+    |g'(g(l)) - g(l)| <= lam~' e + lam~ e:
+        ||P(P(X)) - P(X)||_2 <= (lam~ + lam~') e,   ||.||_F <= sqrt(n) (lam~ + lam~') e.
+    (SURVEY.md's 2 sqrt(n) lam~' e assumes lam~ <= lam~'; the bound above needs no assumption.)
+    The exact projection is idempotent; a dropped 1/2 in the return line (P = 2 relu, P(P) = 4 relu)
+    or the stabilisation applied after the last stage too (s -> 1/1.01) breaks the bound.  (A
+    flipped reconstruction sign, min(X, 0), is idempotent as well: the spectral-operator pins above
+    catch that one.)"""
+    st, k = {"half": (tables.F_HALF_REFINED, tables.half_kappas()), "single": (tables.F_SINGLE_REFINED,
+             tables.single_kappas(10)), "c1": (tables.F_HALF[:3], None)}[which]
+    e, _, _ = certify.relu_err(st, k)
+    n = 72
+    X = synth.make(family, n, synth.SEED_BASE + 71)
+    P, lam = chain.project(X, st, k)
+    PP, lam2 = chain.project(P, st, k)
+    assert lam2 == chain.frobenius_bound(P)
+    D = PP - P
+    assert np.linalg.norm(D, 2) <= 1.01 * (lam + lam2) * e
+    assert np.linalg.norm(D) <= 1.01 * np.sqrt(n) * (lam + lam2) * e
+    # and the method really is (nearly) idempotent at the paper's filter accuracy
+    if which != "c1":
+        assert np.linalg.norm(D) <= 1e-3 * np.linalg.norm(P)
