@@ -80,6 +80,12 @@ class Filter:
         if accum_chunk is not None:
             self.set_accum_chunk(accum_chunk)
 
+    @classmethod
+    def from_file(cls, path, **kw):
+        """A filter from a coefficient file (``filters.load_coefficient_file``: SPEC S:L213 JSON)."""
+        stages, eps, _ = filters.load_coefficient_file(path)
+        return cls(stages, eps=kw.pop("eps", eps), **kw)
+
     def set_accum_chunk(self, kchunk):
         """Split (x3) precisions: K elements per independent accumulation run (0 = one run)."""
         check(self._lib.psd_filter_set_accum_chunk(self._h, int(kchunk)), "psd_filter_set_accum_chunk")

@@ -62,6 +62,46 @@ def fold_stabilization(stages, kappa, n_scaled):
     return [tuple(c) for c in out]
 
 
+def fold_kappas(stages, kappas):
+    """Per-stage stabilisation factors kappa_t (X <- kappa_t X after stage t) folded into
+    the coefficients: kappa_t for t < T into stage t + 1 (as ``fold_stabilization``); a kappa after
+    the last stage, if not 1, stays a trailing degree-1 stage (reading R7: a scalar, 0 products)."""
+    out = [list(c) for c in stages]
+    T = len(out)
+    if len(kappas) != T:
+        raise ValueError("one kappa per stage")
+    for t in range(T - 1):
+        k = float(kappas[t])
+        if k != 1.0:
+            out[t + 1] = [v * k ** (2 * j + 1) for j, v in enumerate(out[t + 1])]
+    stages = [tuple(c) for c in out]
+    if float(kappas[-1]) != 1.0:
+        stages.append((float(kappas[-1]),))
+    return stages
+
+
+def load_coefficient_file(path):
+    """A coefficient file (the JSON layout of SPEC S:L213: {"epsilon", "T", "degrees", "stages":
+    [[c_1, c_3, c_5, ...], ...], "provenance"}, optional "kappas": one stabilisation factor per
+    stage, folded offline by ``fold_kappas``).  Third-party sets (e.g. Polar Express)
+    are ingested this way.  Returns (stages, eps, provenance); raises ValueError on an
+    inconsistent file."""
+    with open(path) as f:
+        d = json.load(f)
+    stages = [tuple(float(v) for v in c) for c in d["stages"]]
+    T = int(d.get("T", len(stages)))
+    degrees = [int(x) for x in d.get("degrees", [2 * len(c) - 1 for c in stages])]
+    if T != len(stages) or len(degrees) != T:
+        raise ValueError(f"{path}: T, degrees and stages disagree")
+    for t, (deg, c) in enumerate(zip(degrees, stages)):
+        if deg % 2 == 0 or deg < 1 or len(c) != (deg + 1) // 2:
+            raise ValueError(f"{path}: stage {t}: degree {deg} with {len(c)} coefficients")
+    eps = float(d.get("epsilon", d.get("eps", 1e-3)))
+    if "kappas" in d:
+        stages = fold_kappas(stages, d["kappas"])
+    return stages, eps, d.get("provenance", "")
+
+
 def half_filter():
     """f~*_half with 1/1.01 after stages 1..6 (the 16-bit path)."""
     return fold_stabilization(HALF_REFINED, 1.0 / 1.01, 6)

@@ -555,3 +555,74 @@ def test_c5_full_size_structured_fp32(pkg, c5_input):
     Pr = P[rows].double().cpu().numpy()
     ref = spectral.structured_project_rows(blocks, *SINGLE, lam, rows)
     assert _rel(Pr, ref) <= TOL_X3["fp16x3"], _rel(Pr, ref)
+
+
+# Baseline filters through the same path: Newton-Schulz g(x) = 1/2 x (3 - x^2)
+# (10 / 15 iterations = 21 / 31 GEMMs) -- degree-3 stages take the p = 1
+# plan branch (Z' = c_0 Z + c_1 Z Y, two products per stage) -- and chains with degree-1 stages
+# (reading R7: a scalar, folded into the neighbouring products).
+NS = (1.5, -0.5)
+DEG1_CHAIN = [(2.0,), NS, NS, (0.9,), NS, NS, NS, (1.1,)]      # leading, inner and trailing degree-1 stages
+
+
+@pytest.mark.parametrize("n,batch,iters,prec", [
+    (64, 40, 10, "fp16"),        # small-n kernel
+    (64, 40, 15, "fp16x3"),
+    (256, 2, 10, "fp16"),        # 1-CTA kernel
+    (256, 2, 15, "fp16x3"),
+    (1024, 8, 10, "fp16"),       # CTA-pair kernel
+    (1024, 8, 15, "fp16x3"),
+    (640, 3, 10, "tf32"),
+])
+def test_newton_schulz_parity(pkg, n, batch, iters, prec):
+    X = synth.batch("goe", n, batch, synth.SEED_BASE + 23 * n + iters)
+    f = pkg.Filter(pkg.filters.newton_schulz(iters), precision=prec)
+    assert f.gemm_count(True) == 2 * iters + 1                   # 21 / 31
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    lam = torch.zeros(batch, dtype=torch.float64, device="cuda")
+    P = f.project(Xd, lambda_out=lam).double().cpu().numpy()
+    S = f.sign(Xd).double().cpu().numpy()
+    assert f.status() == "PSD_OK"
+    bar = TOL_X3.get(prec) or tol(prec, n)
+    for b in sorted({0, batch - 1}):
+        lo = _lam(X[b], float(lam[b]))
+        ref, _ = chain.project(X[b], [tables.NEWTON_SCHULZ_STAGE] * iters, lam=lo)
+        assert _rel(P[b], ref) <= bar, (b, _rel(P[b], ref))
+        refS, _ = chain.sign(X[b], [tables.NEWTON_SCHULZ_STAGE] * iters, lam=lo)
+        assert _rel(S[b], refS) <= bar, (b, _rel(S[b], refS))
+        assert np.array_equal(P[b], P[b].T)
+
+
+@pytest.mark.parametrize("n,batch,prec", [(48, 9, "fp16x3"), (300, 2, "fp16"), (1024, 8, "fp16x3"), (256, 1, "tf32")])
+def test_degree1_stages_parity(pkg, n, batch, prec):
+    """Degree-1 stages (scalars, 0 products) before, between and after degree-3 stages."""
+    X = synth.batch("haar", n, batch, synth.SEED_BASE + 29 * n)
+    f = pkg.Filter(DEG1_CHAIN, precision=prec)
+    assert f.gemm_count(True) == 2 * 5 + 1
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    lam = torch.zeros(batch, dtype=torch.float64, device="cuda")
+    P = f.project(Xd, lambda_out=lam).double().cpu().numpy()
+    S = f.sign(Xd).double().cpu().numpy()
+    bar = TOL_X3.get(prec) or tol(prec, n)
+    for b in sorted({0, batch - 1}):
+        lo = _lam(X[b], float(lam[b]))
+        ref, _ = chain.project(X[b], DEG1_CHAIN, lam=lo)
+        assert _rel(P[b], ref) <= bar, (b, _rel(P[b], ref))
+        refS, _ = chain.sign(X[b], DEG1_CHAIN, lam=lo)
+        assert _rel(S[b], refS) <= bar, (b, _rel(S[b], refS))
+
+
+def test_coefficient_file_roundtrip(pkg, tmp_path):
+    """A coefficient file (SPEC S:L213 JSON: epsilon, T, degrees, stages, provenance; optional
+    stabilisation kappas folded offline, reading R1) gives the same projection as the coefficient
+    tuples it holds."""
+    import json
+    path = tmp_path / "half.json"
+    json.dump({"epsilon": 1e-3, "T": 7, "degrees": [5] * 7, "stages": [list(c) for c in pkg.filters.HALF_REFINED],
+               "kappas": [1 / 1.01] * 6 + [1.0], "provenance": "Table 2 right column (P:L671-677)"},
+              open(path, "w"))
+    X = torch.tensor(synth.batch("goe", 300, 2, 5), dtype=torch.float32, device="cuda")
+    a = pkg.Filter.from_file(str(path)).project(X)
+    b = pkg.Filter(pkg.filters.half_filter()).project(X)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

@@ -163,3 +163,41 @@ def test_admm_and_peer_arguments_rejected_before_any_device_work(lib):
     assert lib.psd_rowpanel_p2p_region(h, 1024, 2, 0, hb) == 6                 # split: unsupported
     lib.psd_rowpanel_p2p_release(h)
     lib.psd_filter_destroy(h)
+
+
+def test_coefficient_file_loader(tmp_path):
+    """filters.load_coefficient_file (SPEC S:L213 layout): kappas folded offline equal the literal
+    stabilisation of the oracle's scalar chain (reading R1/R7: a kappa after the last stage becomes a
+    trailing degree-1 stage); inconsistent files are rejected."""
+    import json
+    import numpy as np
+    from oracle import chain, tables
+    from paper_2507_09165_b200 import filters
+    kap = [1 / 1.01] * 6 + [0.99]
+    path = tmp_path / "f.json"
+    json.dump({"epsilon": 1e-3, "T": 7, "degrees": [5] * 7, "stages": [list(c) for c in tables.F_HALF_REFINED],
+               "kappas": kap, "provenance": "test"}, open(path, "w"))
+    stages, eps, prov = filters.load_coefficient_file(str(path))
+    assert eps == 1e-3 and prov == "test" and len(stages) == 8 and stages[-1] == (0.99,)
+    x = np.linspace(-1, 1, 10001)
+    s_fold = chain.scalar_chain(x, stages)
+    s_lit = chain.scalar_chain(x, tables.F_HALF_REFINED, kap)
+    assert np.max(np.abs(s_fold - s_lit)) < 1e-13
+    for bad in [{"T": 6}, {"degrees": [5] * 6 + [4]}, {"degrees": [3] * 7}]:
+        d = {"epsilon": 1e-3, "T": 7, "degrees": [5] * 7, "stages": [list(c) for c in tables.F_HALF_REFINED]}
+        d.update(bad)
+        json.dump(d, open(path, "w"))
+        with pytest.raises(ValueError):
+            filters.load_coefficient_file(str(path))
+
+
+@pytest.mark.parametrize("name", ["f_half_refined", "f_single_refined", "newton_schulz_10"])
+def test_shipped_coefficient_files(name):
+    """data/filters/*.json load to the filters the product path uses."""
+    import os
+    from paper_2507_09165_b200 import filters
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    stages, eps, _ = filters.load_coefficient_file(os.path.join(root, "data", "filters", name + ".json"))
+    want = {"f_half_refined": filters.half_filter(), "f_single_refined": filters.single_filter(),
+            "newton_schulz_10": filters.newton_schulz(10)}[name]
+    assert stages == [tuple(c) for c in want]
