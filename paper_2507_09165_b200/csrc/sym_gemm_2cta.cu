@@ -103,7 +103,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tmem_full[i], 1);     // one multicast MMA commit
-            ptx::mbar_init(&tmem_empty[i], 2 * 128);   // every epilogue thread of both CTAs
+            ptx::mbar_init(&tmem_empty[i], 2 * 4);     // every epilogue warp of both CTAs
         }
         for (int i = 0; i < kRing; ++i) {
             ptx::mbar_init(&tile_full[i], 1);     // the fetcher's (local or remote) arrive
@@ -328,22 +328,34 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                 for (int ch = 0; ch < nchunks; ++ch, ++cc) {
                     ptx::mbar_wait(&tmem_full[0], cc & 1);
                     ptx::tc_fence_after();
+                    // 64 columns per TMEM round trip (four loads in flight per wait); blocks wholly
+                    // below the diagonal of a diagonal tile are never stored, so never folded
+                    const int c_first = diag ? max(0, (gi0 - J * kT2) & ~31) : 0;
 #pragma unroll 1
-                    for (int c0 = 0; c0 < kT2; c0 += 32) {
-                        if (diag && J * kT2 + c0 + 31 < gi0) continue;   // never stored
-                        uint32_t a[32], sum[32];
-                        ptx::tmem_ld_32x32b_x32(tC + c0, a);
-                        if (ch) ptx::tmem_ld_32x32b_x32(tS + c0, sum);
+                    for (int c0 = c_first & ~63; c0 < kT2; c0 += 64) {
+                        const bool lo_live = c0 >= c_first;            // block c0 (block c0 + 32 always is)
+                        uint32_t a0[32], a1[32], s0[32], s1[32];
+                        if (lo_live) ptx::tmem_ld_32x32b_x32(tC + c0, a0);
+                        ptx::tmem_ld_32x32b_x32(tC + c0 + 32, a1);
+                        if (ch) {
+                            if (lo_live) ptx::tmem_ld_32x32b_x32(tS + c0, s0);
+                            ptx::tmem_ld_32x32b_x32(tS + c0 + 32, s1);
+                        }
                         ptx::tmem_ld_wait();
                         if (ch) {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) a[i] = __float_as_uint(__fadd_rn(__uint_as_float(sum[i]), __uint_as_float(a[i])));
+                            for (int i = 0; i < 32; ++i) {
+                                a0[i] = __float_as_uint(__fadd_rn(__uint_as_float(s0[i]), __uint_as_float(a0[i])));
+                                a1[i] = __float_as_uint(__fadd_rn(__uint_as_float(s1[i]), __uint_as_float(a1[i])));
+                            }
                         }
-                        ptx::tmem_st_32x32b_x32(tS + c0, a);
+                        if (lo_live) ptx::tmem_st_32x32b_x32(tS + c0, a0);
+                        ptx::tmem_st_32x32b_x32(tS + c0 + 32, a1);
                     }
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive_remote(tmem_empty_leader0);
+                    __syncwarp();
+                    if (ptx::elect_one()) ptx::mbar_arrive_remote(tmem_empty_leader0);
                 }
                 tsum = tS;
             } else {
@@ -369,7 +381,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
             }
             if constexpr (!kSplit) {
                 ptx::tc_fence_before();
-                ptx::mbar_arrive_remote((it & 1) ? tmem_empty_leader1 : tmem_empty_leader0);
+                __syncwarp();
+                if (ptx::elect_one()) ptx::mbar_arrive_remote((it & 1) ? tmem_empty_leader1 : tmem_empty_leader0);
             }
             if (kDebug && e0) {
                 atomicAdd(e.dbg + 5, e1 - e0);                 // epilogue warp 4 waiting for / folding accumulators
