@@ -52,7 +52,8 @@ typedef enum {
     PSD_ECUDA = 3,         /* a CUDA runtime/driver call failed */
     PSD_ENCCL = 4,         /* reserved for the row-panel multi-GPU path */
     PSD_ENONFINITE = 5,    /* device found a non-finite input (output is NaN) */
-    PSD_EUNSUPPORTED = 6   /* configuration not supported by this build / device */
+    PSD_EUNSUPPORTED = 6,  /* configuration not supported by this build / device */
+    PSD_ETIMEOUT = 7       /* peer row panels: a peer never reached a barrier (result invalid) */
 } psd_status_t;
 
 /* Operand precision of the tensor-core products; accumulation is always fp32.
@@ -268,7 +269,11 @@ psd_status_t psd_project_rowpanel_virtual(psd_filter_t h, const float* X, int64_
  *       order; opens the peers' regions (cudaIpcOpenMemHandle, lazy peer access).
  * Run: psd_project_rowpanel_p2p(h, X_rows, n, rank, nranks, out_rows, want_sign, stream): X_rows,
  *   out_rows = this rank's rows [rank*n/nranks, +n/nranks) x n fp32 (device).  Every rank must
- *   call it (collective); a rank that never arrives makes the others trap after 10 s.
+ *   call it (collective) and the ranks should pass a host barrier between attach and the first
+ *   call (dist.PeerRowPanelProjector does); a rank that never arrives makes the others give up
+ *   after the timeout (default 10 s): psd_status then returns PSD_ETIMEOUT and out_rows is invalid
+ *   -- the context is never trapped or hung.
+ * psd_rowpanel_p2p_timeout(h, seconds): that barrier timeout, (0, 3600] s.
  * psd_project_rowpanel_p2p_virtual(h, X, n, nranks, out, want_sign, stream): all nranks regions
  *   local to this device and every rank's kernels run here (tests of the per-rank code on one
  *   GPU); X, out full n x n.
@@ -279,6 +284,7 @@ psd_status_t psd_project_rowpanel_p2p(psd_filter_t h, const float* X_rows, int64
                                       float* out_rows, int want_sign, void* stream);
 psd_status_t psd_project_rowpanel_p2p_virtual(psd_filter_t h, const float* X, int64_t n, int nranks, float* out,
                                               int want_sign, void* stream);
+psd_status_t psd_rowpanel_p2p_timeout(psd_filter_t h, double seconds);
 void psd_rowpanel_p2p_release(psd_filter_t h);
 
 /* Host helper: the upper 256-tiles rank `rank` computes, as (I << 16) | J codes in its packed

@@ -168,7 +168,7 @@ class Filter:
         """Synchronise and return 'PSD_OK' or 'PSD_ENONFINITE' (device numeric status)."""
         from ._lib import STATUS_NAMES
         code = self._lib.psd_status(self._h, _stream_ptr(stream))
-        if code not in (0, 5):
+        if code not in (0, 5, 7):
             check(code, "psd_status")
         return STATUS_NAMES[code]
 

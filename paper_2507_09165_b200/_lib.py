@@ -13,9 +13,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libpsdfilter_dbg.so" if os.environ.get("PSD_LIB_VARIANT") == "debug"
                         else "libpsdfilter.so")
 
-PSD_OK, PSD_EINVAL, PSD_ENOMEM, PSD_ECUDA, PSD_ENCCL, PSD_ENONFINITE, PSD_EUNSUPPORTED = range(7)
+PSD_OK, PSD_EINVAL, PSD_ENOMEM, PSD_ECUDA, PSD_ENCCL, PSD_ENONFINITE, PSD_EUNSUPPORTED, PSD_ETIMEOUT = range(8)
 STATUS_NAMES = {0: "PSD_OK", 1: "PSD_EINVAL", 2: "PSD_ENOMEM", 3: "PSD_ECUDA", 4: "PSD_ENCCL",
-                5: "PSD_ENONFINITE", 6: "PSD_EUNSUPPORTED"}
+                5: "PSD_ENONFINITE", 6: "PSD_EUNSUPPORTED", 7: "PSD_ETIMEOUT"}
 PRECISIONS = {"fp16": 0, "bf16": 1, "tf32": 2, "tf32x3": 3, "fp16x3": 4, "bf16x3": 5}
 BOUNDS = {"frobenius": 0, "user": 1, "lanczos": 2}
 
@@ -59,6 +59,7 @@ SIGNATURES = [
                                             _c.c_int, _c.c_void_p]),
     ("psd_project_rowpanel_p2p_virtual", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_void_p,
                                                     _c.c_int, _c.c_void_p]),
+    ("psd_rowpanel_p2p_timeout", _c.c_int, [_c.c_void_p, _c.c_double]),
     ("psd_rowpanel_p2p_release", None, [_c.c_void_p]),
     ("psd_rowpanel_tiles", _c.c_int, [_c.c_int64, _c.c_int, _c.c_int, _c.c_void_p, _c.c_int]),
     ("psd_sym_product", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_double, _c.c_double,

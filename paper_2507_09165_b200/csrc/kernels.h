@@ -165,11 +165,12 @@ cudaError_t launch_unpack_tiles(int elem_bytes, const void* packed, const uint32
 int rowpanel_tiles(int nt, int nranks, int rank, uint32_t* codes, int cap);
 // Cross-rank epoch barrier of the peer-memory path: signal stores `epoch` into slot `rank` of every
 // rank's flag array (system-scope release after a system fence); wait spins until every slot of
-// this rank's flags reaches `epoch` (system-scope acquire; traps after 10 s instead of hanging).
+// this rank's flags reaches `epoch` (system-scope acquire); after timeout_ns it sets bit 1 of
+// *status (psd_status: PSD_ETIMEOUT) and returns instead of hanging.
 cudaError_t launch_peer_signal(unsigned long long* const* flags_dev, int nranks, int rank, unsigned long long epoch,
                                cudaStream_t stream);
 cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, unsigned long long epoch,
-                             cudaStream_t stream);
+                             unsigned long long timeout_ns, unsigned* status, cudaStream_t stream);
 
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.

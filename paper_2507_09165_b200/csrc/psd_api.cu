@@ -109,6 +109,7 @@ struct psd_filter_s {
         std::vector<int> counts;
         int per = 0;
     } pp;
+    unsigned long long peer_timeout_ns = 10000000000ull;   // peer barrier wait (psd_rowpanel_p2p_timeout)
     // CUDA-graph cache of whole psd_project sequences (host launch overhead dominates small n)
     struct GraphEntry {
         const void* X;
@@ -1128,7 +1129,8 @@ psd_status_t run_rowpanel_p2p(psd_filter_s* h, const float* X, float* out, bool 
         }
         for (int r = r_lo; r < r_hi; ++r) {
             const auto* fl = reinterpret_cast<const unsigned long long*>(pp.base[r] + pp.flags_off);
-            if ((e = launch_peer_wait(fl, P, pp.epoch, st)) != cudaSuccess) return cuda_fail(e, "peer wait");
+            if ((e = launch_peer_wait(fl, P, pp.epoch, h->peer_timeout_ns, ws.status, st)) != cudaSuccess)
+                return cuda_fail(e, "peer wait");
         }
         h->kernel_launches += 2 * (r_hi - r_lo);
         return PSD_OK;
@@ -1369,6 +1371,7 @@ psd_status_t psd_status(psd_filter_t h, void* stream) {
     e = cudaMemcpy(&v, h->ws.status, sizeof(unsigned), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "status readback");
     cudaMemset(h->ws.status, 0, sizeof(unsigned));
+    if (v & 2u) return fail(PSD_ETIMEOUT, "peer row panels: a peer did not reach the barrier in time");
     return v ? PSD_ENONFINITE : PSD_OK;
 }
 
@@ -1570,6 +1573,14 @@ psd_status_t psd_project_rowpanel_p2p_virtual(psd_filter_t h, const float* X, in
         if ((rc = peer_finish(h)) != PSD_OK) return rc;
     }
     return run_rowpanel_p2p(h, X, out, want_sign != 0, static_cast<cudaStream_t>(stream));
+}
+
+psd_status_t psd_rowpanel_p2p_timeout(psd_filter_t h, double seconds) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (!(seconds > 0.0) || !(seconds <= 3600.0)) return fail(PSD_EINVAL, "timeout must be in (0, 3600] s");
+    const unsigned long long ns = static_cast<unsigned long long>(seconds * 1e9);
+    h->peer_timeout_ns = ns;
+    return PSD_OK;
 }
 
 void psd_rowpanel_p2p_release(psd_filter_t h) {

@@ -80,7 +80,8 @@ __global__ void peer_signal_kernel(unsigned long long* const* __restrict__ flags
         asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(flags[p] + rank), "l"(epoch) : "memory");
 }
 
-__global__ void peer_wait_kernel(const unsigned long long* __restrict__ my_flags, int nranks, unsigned long long epoch) {
+__global__ void peer_wait_kernel(const unsigned long long* __restrict__ my_flags, int nranks, unsigned long long epoch,
+                                 unsigned long long timeout_ns, unsigned* __restrict__ status) {
     const int p = threadIdx.x;
     if (p < nranks) {
         unsigned long long t0, t, v;
@@ -89,7 +90,13 @@ __global__ void peer_wait_kernel(const unsigned long long* __restrict__ my_flags
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + p) : "memory");
             if (v >= epoch) break;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 10000000000ull) __trap();      // a peer never arrived: fail, never hang the GPU
+            if (t - t0 > timeout_ns) {
+                // a peer never arrived: record it (psd_status -> PSD_ETIMEOUT) and let the stream
+                // go on (the result is invalid), never hang or trap the context
+                atomicOr(status, 2u);
+                break;
+            }
+            __nanosleep(256);
         }
     }
     __syncthreads();
@@ -106,8 +113,8 @@ cudaError_t launch_peer_signal(unsigned long long* const* flags_dev, int nranks,
 }
 
 cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, unsigned long long epoch,
-                             cudaStream_t stream) {
-    peer_wait_kernel<<<1, 32, 0, stream>>>(my_flags, nranks, epoch);
+                             unsigned long long timeout_ns, unsigned* status, cudaStream_t stream) {
+    peer_wait_kernel<<<1, 32, 0, stream>>>(my_flags, nranks, epoch, timeout_ns, status);
     return cudaGetLastError();
 }
 

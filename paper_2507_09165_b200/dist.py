@@ -112,6 +112,9 @@ class PeerRowPanelProjector:
         check(self._lib.psd_rowpanel_p2p_region(self.f._h, self.n, self.world, self.rank, h), "psd_rowpanel_p2p_region")
         handles = exchange_ipc_handles(h.raw, group)
         check(self._lib.psd_rowpanel_p2p_attach(self.f._h, b"".join(handles)), "psd_rowpanel_p2p_attach")
+        # every rank's region is mapped before anyone's first peer epoch: the device barrier's
+        # timeout then only has to cover kernel skew, not host-side setup
+        dist.barrier(group)
 
     def row_range(self):
         return self.rank * self.rows, self.rows
