@@ -1,6 +1,6 @@
 """Summarise an ncu session (tools/gpu_session.sh output dir) into profiles/.
 
-    python tools/summarize_ncu.py gpurun_out/<tag> <round-name>
+    python tools/summarize_ncu.py gpurun_out/<tag> <round-name> [launches.csv] [prof.ncu-rep] [latest.json]
 
 Writes profiles/<round-name>_summary.md (launch-list shares + the top kernel's full-set
 metrics) and profiles/ncu_latest.json ({kernel, dram bytes per launch, ...}) which
@@ -53,15 +53,18 @@ def full_metrics(rep):
 
 def main():
     d, name = sys.argv[1], sys.argv[2]
+    lfile = sys.argv[3] if len(sys.argv) > 3 else "launches.csv"
+    rfile = sys.argv[4] if len(sys.argv) > 4 else "prof_gemm.ncu-rep"
+    latest = sys.argv[5] if len(sys.argv) > 5 else "ncu_latest.json"
     lines = [f"# ncu summary: {name}", "", f"Source: `{d}` (tools/gpu_session.sh), B200, `--clock-control none`.", ""]
-    lp = os.path.join(d, "launches.csv")
+    lp = os.path.join(d, lfile)
     if os.path.exists(lp):
         lines += ["## Launch list (`--metrics gpu__time_duration.sum`, cold-cache, serialised)", "",
                   "| kernel | launches | avg time | share of step |", "|---|---|---|---|"]
         for k, cnt, avg, share in launch_shares(lp):
             lines.append(f"| `{k[:90]}` | {cnt} | {avg * 1e6:.1f} us | {share:.3f} |")
         lines.append("")
-    rep = os.path.join(d, "prof_gemm.ncu-rep")
+    rep = os.path.join(d, rfile)
     js = {}
     if os.path.exists(rep):
         m = full_metrics(rep)
@@ -79,7 +82,7 @@ def main():
     with open(os.path.join(ROOT, "profiles", f"{name}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if js:
-        with open(os.path.join(ROOT, "profiles", "ncu_latest.json"), "w") as f:
+        with open(os.path.join(ROOT, "profiles", latest), "w") as f:
             json.dump(js, f, indent=1)
     print("\n".join(lines))
 
