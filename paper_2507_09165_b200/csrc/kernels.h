@@ -146,8 +146,6 @@ struct SmallPlan {
     float* out2;              // ADMM: X_next = sigma2 (P - M), stored like out
     float sigma2;
     unsigned long long* dbg;  // debug: per-phase clock totals of CTA 0 (NULL in production)
-    int nofold;               // A/B only (PSD_SMALL_NOFOLD): apply the operand scale after the addend
-    int mirror_scalar;        // A/B only (PSD_SMALL_MIRROR_SCALAR): per-thread 8x8 block mirror
     SmallStep steps[40];
 };
 int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U

@@ -464,8 +464,6 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             sp_plan.sigma2 = admm->sigma;
         }
         sp_plan.s_x0 = static_cast<float>(sz);
-        sp_plan.nofold = debug_env("PSD_SMALL_NOFOLD") != nullptr ? 1 : 0;
-        sp_plan.mirror_scalar = debug_env("PSD_SMALL_MIRROR_SCALAR") != nullptr ? 1 : 0;
         for (size_t i = 0; i < steps.size(); ++i) {
             const Step& s = steps[i];
             SmallStep& q = sp_plan.steps[i];
@@ -508,17 +506,20 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         const bool dbg = !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
             sp_plan.dbg = reinterpret_cast<unsigned long long*>(ws.partial);
-            cudaMemsetAsync(ws.partial, 0, 64, st);
+            cudaMemsetAsync(ws.partial, 0, 128, st);   // 16 counters
         }
         h->last_products = 1;
         e = launch_small_batch(sp, X, out, n, batch, lambda_out, ws.status, sp_plan, st);
         if (e != cudaSuccess) return cuda_fail(e, "small_batch");
         if (dbg) {
-            unsigned long long t[4] = {};
+            unsigned long long t[16] = {};
             cudaStreamSynchronize(st);
             cudaMemcpy(t, sp_plan.dbg, sizeof(t), cudaMemcpyDeviceToHost);
-            if (t[3]) std::fprintf(stderr, "psd small stamps (cycles/step, CTA 0, %llu steps): mma %.0f, tmem-ld %.0f, epilogue+sync %.0f\n",
-                                   t[3], double(t[0]) / t[3], double(t[1]) / t[3], double(t[2]) / t[3]);
+            if (t[3]) std::fprintf(stderr, "psd small stamps (cycles/step, CTA 0, %llu steps): mma issue %.0f, mma wait + barrier %.0f, epilogue %.0f, fences + barrier %.0f\n",
+                                   t[3], double(t[0]) / t[3], double(t[1]) / t[3], double(t[2]) / t[3], double(t[4]) / t[3]);
+            if (t[7]) std::fprintf(stderr, "psd small stamps (cycles/pair, CTA 0, %llu pairs): load + bound + X_0 %.0f (loads %.0f, bound %.0f, X_0 %.0f), final product %.0f\n",
+                                   t[7], double(t[5]) / t[7], double(t[8]) / t[7], double(t[9]) / t[7], double(t[10]) / t[7], double(t[6]) / t[7]);
+            std::fprintf(stderr, "psd small stamps: first pair loads %llu cycles\n", t[11]);
         }
         h->kernel_launches += 1;
         if (evs.first) {

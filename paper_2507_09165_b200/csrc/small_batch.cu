@@ -1,18 +1,25 @@
 // small_batch.cu -- batched small-n path (n <= 64): the whole of Algorithm 2 for a
-// pair of matrices per CTA iteration, on-chip, HBM touched once for X and once for P.
+// pair of matrices per CTA iteration, on-chip; HBM is touched once for X (upper triangle only,
+// reading R10) and once for P.
 //
-//   * bound + scale in-kernel: a CTA stages the two 64x64 fp32 inputs
-//     in smem, reduces ||X||_F per matrix in fp64 (deterministic fixed order) and writes X_0 in
-//     the operand format (SW128 K-major fp16, hi/lo for the split path);
+//   * bound + scale in-kernel: each thread loads the upper part of its
+//     own row straight into registers, the CTA reduces ||X||_F per matrix in fp64 (fixed order,
+//     deterministic) and writes X_0 in the operand format (SW128 K-major fp16, hi/lo for the split
+//     path); the lower triangle is then filled from the upper one in shared memory (R20);
 //   * every product of the chain is tcgen05.mma.cta_group::1 M=64 N=64 K=16 from smem
 //     descriptors into TMEM; the two matrices of the pair use the two half-subpartition
 //     interleaves of one 64-column accumulator (lanes 32w+[0,16) and 32w+[16,32)), so one
 //     tcgen05.ld 32x32b gives each thread one row of one matrix;
-//   * epilogue: alpha*acc + beta*D (D = the rounded operand copy in smem, reading R18), written
-//     back in place into the operand slot (the MMA has completed), fence.proxy.async, barrier;
-//   * reconstruction P = 1/2 X + 1/2 lambda~ X_0 S: X_0 is re-staged from X, and the
-//     result is symmetrised through smem (exact symmetry) and stored to HBM.
-// Two CTAs per SM (96 KB smem each) so one CTA's epilogue overlaps the other's MMAs.
+//   * epilogue (one row of 64 columns per thread): alpha*acc + beta*D with packed f32x2 FMAs
+//     (D = the rounded operand copy in smem, reading R18), written back in place into the
+//     operand slot (the MMA has completed), fence.proxy.async, barrier;
+//   * reconstruction P = 1/2 X + 1/2 lambda~ X_0 S: X is reloaded (L2) into registers,
+//     X_0 restaged for the last product, the result symmetrised through smem (exact symmetry) and
+//     stored to HBM.
+// 4 CTAs of 4 warps per SM on the 16-bit path (2 on the split path): while one CTA waits for its
+// MMAs, the others run their epilogues.  Only the issuing thread waits on the MMA barrier; the
+// other warps sleep in bar.sync (a 256-thread spin on the mbarrier took ~15% of the issue slots
+// in the first version, profiles/r2_c2_small_v2.md).
 #include <cuda_fp16.h>
 
 #include "kernels.h"
@@ -24,119 +31,109 @@ namespace {
 
 constexpr int kN = 64;                  // padded matrix edge
 constexpr int kSlotBytes = kN * 128;    // 64 rows x 128 B (fp16), one SW128 atom wide
-constexpr int kThreadsS = 256;        // 8 warps: TMEM quadrant = warp & 3, column half = warp >> 2
+constexpr int kThreadsS = 128;          // 4 warps: warp = TMEM lane quadrant, lane >> 4 = matrix
 
-// byte offset of element (row, col) in a SW128 K-major 64x64 fp16 slot
+// byte offset of the 16-byte chunk `chunk` (8 fp16 columns) of row `row` in a SW128 K-major slot
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
     return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
 template <bool kSplit>
 struct SmallLayout {
-    // per matrix: Z slot, Y slot (hi [+ lo]), U slot (always 16 KB: hi + lo, or fp32 staging)
+    // per matrix: Z slot, Y slot, U slot (hi [+ lo] each); the fp32 staging of the final product
+    // reuses the first 16 KB of the matrix region (its operands are consumed by then)
     static constexpr int kParts = kSplit ? 2 : 1;
     static constexpr int kZ = 0;
     static constexpr int kY = kParts * kSlotBytes;
     static constexpr int kU = 2 * kParts * kSlotBytes;
-    static constexpr int kPerMatrix = kU + 2 * kSlotBytes;
-    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 256;   // + align slack, barrier, tmem slot, 2x8 partial sums
+    static constexpr int kPerMatrix = 3 * kParts * kSlotBytes;
+    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 128;   // + align slack, barrier, tmem slot, partial sums
 };
+// resident CTAs per SM: 4 x 49 KB (16-bit), 2 x 97 KB (split)
+template <bool kSplit> constexpr int kSmallCtasPerSm = kSplit ? 2 : 4;
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <bool kSplit, bool kScale = true>
-__device__ __forceinline__ void store_row(uint8_t* slot, int row, int half, const float (&v)[32], float s) {
-    // hi = rn(v s) [, lo = rn(v s - hi)] into the swizzled slot row, columns [32 half, 32 half + 32)
-    // (kScale false: s is already folded into v)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-        const int c = 4 * half + cc;
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const float a = kScale ? v[8 * cc + 2 * h] * s : v[8 * cc + 2 * h];
-            const float b = kScale ? v[8 * cc + 2 * h + 1] * s : v[8 * cc + 2 * h + 1];
-            const __half2 hh = __floats2half2_rn(a, b);
-            hi[h] = *reinterpret_cast<const uint32_t*>(&hh);
-            if constexpr (kSplit) {
-                const float2 hf = __half22float2(hh);
-                const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
-                lo[h] = *reinterpret_cast<const uint32_t*>(&ll);
-            }
-        }
-        *reinterpret_cast<uint4*>(slot + swz(row, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        if constexpr (kSplit)
-            *reinterpret_cast<uint4*>(slot + kSlotBytes + swz(row, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    }
+// ---- packed fp32 pairs (FFMA2 / FMUL2 on sm_100)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// float(h) + c for the two halves of a packed fp16 pair (FHADD: one instruction per element)
+__device__ __forceinline__ float2 add_h2(uint32_t h, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+        "add.rn.f32.f16 %0, lo, %3;\n\tadd.rn.f32.f16 %1, hi, %4;\n\t}"
+        : "=f"(d.x), "=f"(d.y) : "r"(h), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Exact symmetry of a stored operand: row `row` takes its lower part (col < row) from the
-// upper part of the rows above it (reads touch only the upper triangle, writes only the lower).
-// Without it the rounding-level antisymmetric part of the products grows like prod_t c_{t,0}
-// along the chain (it is not damped by the sign dynamics).
+// The rounded operand value(s) of 8 consecutive columns: hi [+ lo] (the same copy the tensor
+// cores multiply, reading R18)
 template <bool kSplit>
-__device__ __forceinline__ void mirror_lower(uint8_t* slot, int row) {
-    for (int c = 0; c < row; ++c) {
-        const uint32_t src = static_cast<uint32_t>(c * 128 + ((((row >> 3) ^ (c & 7))) << 4) + (row & 7) * 2);
-        const uint32_t dst = static_cast<uint32_t>(row * 128 + ((((c >> 3) ^ (row & 7))) << 4) + (c & 7) * 2);
-        *reinterpret_cast<uint16_t*>(slot + dst) = *reinterpret_cast<const uint16_t*>(slot + src);
-        if constexpr (kSplit)
-            *reinterpret_cast<uint16_t*>(slot + kSlotBytes + dst) = *reinterpret_cast<const uint16_t*>(slot + kSlotBytes + src);
-    }
-}
-
-// Block version: the 64x64 fp16 part(s) of a slot as 8x8 blocks of 8x8 elements; block (bi, bj),
-// bi > bj, becomes the transpose of block (bj, bi); a diagonal block takes its lower triangle from
-// its upper triangle.  36 block tasks per matrix part, one per thread (16-byte smem accesses).
-__device__ __forceinline__ void mirror_block_task(uint8_t* part, int task) {
-    // task -> (bi >= bj): row-major over the lower triangle of the 8 x 8 block grid
-    int bi = 0, rem = task;
-    while (rem > bi) { rem -= bi + 1; ++bi; }
-    const int bj = rem;
-    uint16_t blk[8][8];
+__device__ __forceinline__ void load_operand8(const uint8_t* part, uint32_t off, float2 (&d)[4]) {
+    const uint4 h = *reinterpret_cast<const uint4*>(part + off);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+    if constexpr (kSplit) {
+        const uint4 l = *reinterpret_cast<const uint4*>(part + kSlotBytes + off);
+        const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int row = 8 * bj + r;                    // source: block (bj, bi) (upper)
-        const uint4 q = *reinterpret_cast<const uint4*>(part + swz(row, bi));
-        const uint16_t* h = reinterpret_cast<const uint16_t*>(&q);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) blk[r][c] = h[c];
-    }
-    if (bi != bj) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            __align__(16) uint16_t o[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) o[c] = blk[c][r];   // transpose
-            *reinterpret_cast<uint4*>(part + swz(8 * bi + r, bj)) = *reinterpret_cast<const uint4*>(o);
-        }
+        for (int q = 0; q < 4; ++q) d[q] = add_h2(lw[q], __half22float2(*reinterpret_cast<const __half2*>(&hw[q])));
     } else {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            __align__(16) uint16_t o[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) o[c] = (c >= r) ? blk[r][c] : blk[c][r];
-            *reinterpret_cast<uint4*>(part + swz(8 * bi + r, bj)) = *reinterpret_cast<const uint4*>(o);
-        }
+        for (int q = 0; q < 4; ++q) d[q] = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
     }
 }
 
-// The same mirror, four 8x8 blocks per warp instruction: ldmatrix.x4.trans reads upper blocks
-// (bj, bi) transposed and stmatrix.x4 writes them as blocks (bi, bj); lanes 8q..8q+7 address the
-// rows of block q.  Group g of a 64x64 part: g < 7 the off-diagonal blocks 4g..4g+3 (row-major over
-// the strict lower block triangle), g = 7, 8 the diagonal blocks 4(g-7)..+3, which merge their
-// plain and transposed loads (upper part kept).  The 8 row addresses of a block hit 8 distinct
-// 16-byte chunks of the SW128 rows: conflict-free.  Fragment of lane t: row t/4, columns 2(t%4)+{0,1}.
+// hi = rn(v) [, lo = rn(v - hi)] of 8 consecutive columns into the slot
+template <bool kSplit>
+__device__ __forceinline__ void store_operand8(uint8_t* part, uint32_t off, const float2 (&v)[4]) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        hi[q] = pack_h2(v[q].x, v[q].y);
+        if constexpr (kSplit) {
+            const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[q]));
+            lo[q] = pack_h2(v[q].x - hf.x, v[q].y - hf.y);
+        }
+    }
+    *reinterpret_cast<uint4*>(part + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if constexpr (kSplit)
+        *reinterpret_cast<uint4*>(part + kSlotBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+// Exact symmetry of a stored operand (reading R20), four 8x8 blocks per warp instruction:
+// ldmatrix.x4.trans reads upper blocks (bj, bi) transposed and stmatrix.x4 writes them as blocks
+// (bi, bj); lanes 8q..8q+7 address the rows of block q.  Group g of a 64x64 part: g < 7 the
+// strictly-lower blocks 4g..4g+3 (row-major), g = 7, 8 the diagonal blocks 4(g-7)..+3, which merge
+// their plain and transposed loads (upper part kept).  The 8 row addresses of a block hit 8
+// distinct 16-byte chunks of the SW128 rows: conflict-free.  Fragment of lane t: row t/4, columns
+// 2(t%4)+{0,1}.
 constexpr int kMirrorGroups = 9;
 __device__ __forceinline__ void mirror_group_warp(uint8_t* part, int g, int lane) {
     const int q = lane >> 3, rr = lane & 7;
     int bi, bj;
     if (g < 7) {
-        const int k = 4 * g + q;                       // 0..27
-        bi = 1;
-        while (k >= bi * (bi + 1) / 2) ++bi;
+        const int k = 4 * g + q;                       // 0..27 over the strict lower block triangle
+        bi = 1 + (k >= 1) + (k >= 3) + (k >= 6) + (k >= 10) + (k >= 15) + (k >= 21);
         bj = k - bi * (bi - 1) / 2;
     } else {
         bi = bj = 4 * (g - 7) + q;
@@ -159,175 +156,412 @@ __device__ __forceinline__ void mirror_group_warp(uint8_t* part, int g, int lane
                  :: "r"(dst), "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]) : "memory");
 }
 
+// mirror the slot at `slot_off` of both matrices (all parts); caller synchronises before/after
 template <bool kSplit>
-__device__ __forceinline__ void add_row(const uint8_t* slot, int row, int half, float beta, float (&v)[32]) {
-    // v += beta * (hi [+ lo]) of the slot row, columns [32 half, 32 half + 32)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-        const int c = 4 * half + cc;
-        const uint4 h = *reinterpret_cast<const uint4*>(slot + swz(row, c));
-        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-        float2 lf[4];
-        if constexpr (kSplit) {
-            const uint4 l = *reinterpret_cast<const uint4*>(slot + kSlotBytes + swz(row, c));
-            const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) lf[q] = __half22float2(*reinterpret_cast<const __half2*>(&lw[q]));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
-            if constexpr (kSplit) {
-                f.x += lf[q].x;
-                f.y += lf[q].y;
-            }
-            v[8 * cc + 2 * q] += beta * f.x;
-            v[8 * cc + 2 * q + 1] += beta * f.y;
-        }
+__device__ __forceinline__ void mirror_slot(uint8_t* smem, int slot_off, int warp, int lane) {
+    using L = SmallLayout<kSplit>;
+    constexpr int kTasks = 2 * L::kParts * kMirrorGroups;
+#pragma unroll 1
+    for (int task = warp; task < kTasks; task += kThreadsS / 32) {
+        const int mm = task / (L::kParts * kMirrorGroups);
+        const int part = (task / kMirrorGroups) % L::kParts;
+        mirror_group_warp(smem + mm * L::kPerMatrix + slot_off + part * kSlotBytes, task % kMirrorGroups, lane);
     }
 }
 
-__device__ __forceinline__ float4 load_row4(const float* base, int64_t roff, int n, int q) {
-    // columns 4q..4q+3 of a row (zero past n)
-    const float* xr = base + roff;
-    if (n == kN) return __ldg(reinterpret_cast<const float4*>(xr) + q);
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int c = 4 * q;
-    if (c + 0 < n) x.x = __ldg(xr + c + 0);
-    if (c + 1 < n) x.y = __ldg(xr + c + 1);
-    if (c + 2 < n) x.z = __ldg(xr + c + 2);
-    if (c + 3 < n) x.w = __ldg(xr + c + 3);
-    return x;
+// 16 bytes of a row when `p` holds (else zeros), as one predicated load: the 16 loads of a row group
+// are issued back to back (a branch around each made the compiler wait for every load in turn)
+__device__ __forceinline__ float4 ldg4_pred(const float* ptr, bool p) {
+    float4 v;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                 "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+                 "@q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "r"(static_cast<int>(p)));
+    return v;
+}
+// the same for rows whose length is not a multiple of 4 (4-byte aligned): up to `rem` elements
+__device__ __forceinline__ float4 ldg4_tail(const float* ptr, bool p, int rem) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p) {
+        v.x = __ldg(ptr);
+        if (rem > 1) v.y = __ldg(ptr + 1);
+        if (rem > 2) v.z = __ldg(ptr + 2);
+        if (rem > 3) v.w = __ldg(ptr + 3);
+    }
+    return v;
 }
 
-// resident CTAs per SM (8 warps each): 3 for the single-pass layout (80 registers, a 136-byte spill:
-// measured 0.289 -> 0.271 ms at c2 vs 2 CTAs), 2 for the split one (smem)
-template <bool kSplit> constexpr int kSmallCtasPerSm = kSplit ? 2 : 3;
+// ---- fragment-layout epilogue of the chain products
+// tcgen05.ld 16x256b: 16 TMEM lanes x 8 fp32 columns per repetition; thread t gets lane t/4 cols
+// 2(t%4)+{0,1} (regs 0,1) and lane t/4+8, same cols (regs 2,3) -- the 8x8-block fragment layout
+// of ldmatrix / stmatrix / movmatrix, so the epilogue reads the addend, writes the output and its
+// transpose (the mirror, R20) with one warp instruction per 8x8 block group.
+__device__ __forceinline__ void tmem_ld_16x256b_x1(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&d)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&d)[2]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(d[0]), "=r"(d[1]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void stsm_x4(uint32_t addr, const uint32_t (&d)[4]) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};"
+                 :: "r"(addr), "r"(d[0]), "r"(d[1]), "r"(d[2]), "r"(d[3]) : "memory");
+}
+__device__ __forceinline__ void stsm_x2(uint32_t addr, uint32_t d0, uint32_t d1) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x2.shared.b16 [%0], {%1, %2};" :: "r"(addr), "r"(d0), "r"(d1) : "memory");
+}
+__device__ __forceinline__ void stsm_x2_trans(uint32_t addr, uint32_t d0, uint32_t d1) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x2.trans.shared.b16 [%0], {%1, %2};" :: "r"(addr), "r"(d0), "r"(d1) : "memory");
+}
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
+}
+
+// One 8x8 output block in fragment form: hi [, lo] of alpha acc + beta D (D = hi [+ lo] of the
+// addend's fragment, R18); the operand scale is folded into alpha and beta by the caller.
+template <bool kSplit>
+struct Frag {
+    uint32_t hi, lo;
+};
+template <bool kSplit>
+__device__ __forceinline__ Frag<kSplit> combine(uint32_t a0, uint32_t a1, bool has_d, uint32_t dh, uint32_t dl,
+                                                float2 alpha, float2 beta) {
+    float2 v = make_float2(__uint_as_float(a0), __uint_as_float(a1));
+    if (has_d) {
+        float2 d = __half22float2(*reinterpret_cast<const __half2*>(&dh));
+        if constexpr (kSplit) d = add_h2(dl, d);
+        v = fma2(alpha, v, mul2(beta, d));
+    } else {
+        v = mul2(alpha, v);
+    }
+    Frag<kSplit> f;
+    f.hi = pack_h2(v.x, v.y);
+    f.lo = 0;
+    if constexpr (kSplit) {
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&f.hi));
+        f.lo = pack_h2(v.x - hf.x, v.y - hf.y);
+    }
+    return f;
+}
+// a diagonal block made exactly symmetric from its upper triangle (fragment of lane t: row t/4,
+// columns 2(t%4)+{0,1})
+__device__ __forceinline__ uint32_t diag_upper(uint32_t f, uint32_t mask) {
+    const uint32_t t = movmatrix_trans(f);
+    return (f & mask) | (t & ~mask);
+}
+
+// The chain-product epilogue of warp W (TMEM lane quadrant W = rows 16W..16W+15 of both matrices),
+// every block index a compile-time constant.  Only the upper 8x8 blocks are computed; each writes
+// itself and its transpose (every product is exactly symmetric, R20).  Warp W owns the 9 unordered
+// block pairs {P, Q} with P in its row blocks {2W, 2W+1}: the three inside them, and for every
+// other warp b the two (2W, 2b), (2W, 2b+1) if b > W, else (2W, 2b+1), (2W+1, 2b+1) -- the same
+// count for every quadrant (SMSP), and every pair exactly once.  In place is safe: a warp reads
+// the addend only at the positions it writes.
+template <int W, int K> struct Region {
+    static constexpr int bq = K + (K >= W ? 1 : 0);   // the other warp
+    static constexpr bool kRight = bq > W;           // (R0, 2bq), (R0, 2bq+1)  else  (R0, 2bq+1), (R1, 2bq+1)
+};
+template <int W, int K>
+__device__ __forceinline__ void region_load(uint32_t tb, uint32_t (&a)[8]) {
+    using Rg = Region<W, K>;
+    if constexpr (Rg::kRight) tmem_ld_16x256b_x2(tb + 16 * Rg::bq, a);
+    else tmem_ld_16x256b_x1(tb + 16 * Rg::bq + 8, *reinterpret_cast<uint32_t(*)[4]>(a));
+}
+template <bool kSplit, int W, int K>
+__device__ __forceinline__ void region_store(const uint32_t (&a)[8], uint32_t pd, uint32_t po, bool has_d,
+                                             float2 alpha, float2 beta, uint32_t lrow128, uint32_t lrow, uint32_t lq1) {
+    using Rg = Region<W, K>;
+    constexpr int R0 = 2 * W, bq = Rg::bq;
+    uint32_t on, ot, a0, a1, a2, a3;
+    if constexpr (Rg::kRight) {
+        on = (8 * R0) * 128 + lrow128 + (((2 * bq + lq1) ^ lrow) << 4);
+        ot = (8 * 2 * bq) * 128 + lq1 * 1024 + lrow128 + ((R0 ^ lrow) << 4);
+        a0 = a[0]; a1 = a[1]; a2 = a[4]; a3 = a[5];
+    } else {
+        on = (8 * R0) * 128 + lq1 * 1024 + lrow128 + (((2 * bq + 1) ^ lrow) << 4);
+        ot = (8 * (2 * bq + 1)) * 128 + lrow128 + (((R0 + lq1) ^ lrow) << 4);
+        a0 = a[0]; a1 = a[1]; a2 = a[2]; a3 = a[3];
+    }
+    uint32_t dh[2] = {0, 0}, dl[2] = {0, 0};
+    if (has_d) {
+        ldsm_x2(pd + on, dh);
+        if constexpr (kSplit) ldsm_x2(pd + kSlotBytes + on, dl);
+    }
+    const Frag<kSplit> g0 = combine<kSplit>(a0, a1, has_d, dh[0], dl[0], alpha, beta);
+    const Frag<kSplit> g1 = combine<kSplit>(a2, a3, has_d, dh[1], dl[1], alpha, beta);
+    stsm_x2(po + on, g0.hi, g1.hi);
+    stsm_x2_trans(po + ot, g0.hi, g1.hi);
+    if constexpr (kSplit) {
+        stsm_x2(po + kSlotBytes + on, g0.lo, g1.lo);
+        stsm_x2_trans(po + kSlotBytes + ot, g0.lo, g1.lo);
+    }
+}
+template <bool kSplit, int W>
+__device__ __forceinline__ void chain_epilogue(uint32_t tmem, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
+                                               bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
+    constexpr int R0 = 2 * W;
+    const uint32_t lrow = lane & 7, lq = lane >> 3, lq1 = lq & 1;
+    const uint32_t lrow128 = lrow * 128;
+    // blocks inside the warp's rows, lane group q: [(R0,R0), (R1,R0), (R0,R1), (R1,R1)]
+    const uint32_t offW = (8 * R0) * 128 + (lq & 1) * 1024 + lrow128 + (((R0 + (lq >> 1)) ^ lrow) << 4);
+    // both matrices' accumulator fragments in flight before the first wait
+    uint32_t aWs[2][8], a0s[2][8], a1s[2][8], a2s[2][8];
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+        const uint32_t tb = tmem + (static_cast<uint32_t>(32 * W + 16 * mm) << 16);
+        tmem_ld_16x256b_x2(tb + 16 * W, aWs[mm]);
+        region_load<W, 0>(tb, a0s[mm]);
+        region_load<W, 1>(tb, a1s[mm]);
+        region_load<W, 2>(tb, a2s[mm]);
+    }
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+        const uint32_t (&aW)[8] = aWs[mm];
+        const uint32_t (&a0)[8] = a0s[mm];
+        const uint32_t (&a1)[8] = a1s[mm];
+        const uint32_t (&a2)[8] = a2s[mm];
+        const uint32_t pd = pd0 + mm * mat_bytes, po = po0 + mm * mat_bytes;
+        {
+            uint32_t dh[4] = {0, 0, 0, 0}, dl[4] = {0, 0, 0, 0};
+            if (has_d) {
+                ldsm_x4(pd + offW, dh);
+                if constexpr (kSplit) ldsm_x4(pd + kSlotBytes + offW, dl);
+            }
+            const Frag<kSplit> f0 = combine<kSplit>(aW[0], aW[1], has_d, dh[0], dl[0], alpha, beta);
+            const Frag<kSplit> f2 = combine<kSplit>(aW[4], aW[5], has_d, dh[2], dl[2], alpha, beta);
+            const Frag<kSplit> f3 = combine<kSplit>(aW[6], aW[7], has_d, dh[3], dl[3], alpha, beta);
+            const uint32_t h[4] = {diag_upper(f0.hi, diag_mask), movmatrix_trans(f2.hi), f2.hi, diag_upper(f3.hi, diag_mask)};
+            stsm_x4(po + offW, h);
+            if constexpr (kSplit) {
+                const uint32_t l[4] = {diag_upper(f0.lo, diag_mask), movmatrix_trans(f2.lo), f2.lo, diag_upper(f3.lo, diag_mask)};
+                stsm_x4(po + kSlotBytes + offW, l);
+            }
+        }
+        region_store<kSplit, W, 0>(a0, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+        region_store<kSplit, W, 1>(a1, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+        region_store<kSplit, W, 2>(a2, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+    }
+}
 
 template <bool kSplit>
 __global__ void __launch_bounds__(kThreadsS, kSmallCtasPerSm<kSplit>)
 small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
-                   double* __restrict__ lambda_out, unsigned* __restrict__ status, const SmallPlan plan) {
+                   double* __restrict__ lambda_out, unsigned* __restrict__ status,
+                   const __grid_constant__ SmallPlan plan) {
     using L = SmallLayout<kSplit>;
-    constexpr int kWarps = kThreadsS / 32;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
-    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][8 warps]
+    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][4 warps]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int quad = warp & 3;                   // TMEM lane quadrant: rows 16 quad .. 16 quad + 15
-    const int half = warp >> 2;                  // column half: [32 half, 32 half + 32)
-    const int m = lane >> 4;                     // matrix of the pair this thread serves
-    const int row = 16 * quad + (lane & 15);     // its row
-    const int c0 = 32 * half;                    // its first column
+    const int m = lane >> 4;                     // row-per-thread phases: matrix of the pair
+    const int row = 16 * warp + (lane & 15);     // its row (TMEM lane 32 warp + lane)
+    const int rx = row & 7;                      // its SW128 chunk swizzle
+    const uint32_t rbase = static_cast<uint32_t>(row * 128);
     uint8_t* mat = smem + m * L::kPerMatrix;
+    const bool vec = (n & 3) == 0;               // float4 rows (X is 16-byte aligned)
+    const uint32_t smem_base = ptx::smem_u32(smem);
+    // fragment phases: lane t addresses row t & 7 of block t >> 3 in ldmatrix / stmatrix; its
+    // fragment is row t/4, cols 2(t%4)+{0,1}
+    const uint32_t diag_mask = ((2 * (lane & 3) >= (lane >> 2)) ? 0xFFFFu : 0u) |
+                               ((2 * (lane & 3) + 1 >= (lane >> 2)) ? 0xFFFF0000u : 0u);
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(mma_bar, 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 0) ptx::tmem_alloc<64>(tmem_slot);
+    if (warp == 0) ptx::tmem_alloc<128>(tmem_slot);   // cols [0,64): accumulator, [64,128): the input rows
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_row = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    const uint32_t tmem_x = tmem_row + 64;
     constexpr uint32_t kIdesc = ptx::make_idesc(0, 64, 64);   // f16 x f16 -> f32, M=64, N=64
     uint32_t mma_phase = 0;
 
     const int pairs = (batch + 1) / 2;
     for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        const long long t_pair = kDebug ? clock64() : 0;
         const int b = 2 * pr + m;
         const bool valid = b < batch;
-        float* stage = reinterpret_cast<float*>(mat + L::kU);   // 64 x 64 fp32 staging (16 KB)
 
-        // ---- stage X (zero padded) for both matrices of the pair into the U slots: coalesced loads
-        auto stage_X = [&]() {
-            const int64_t base = static_cast<int64_t>(2 * pr) * n * n;
-            const int nvalid = min(2, batch - 2 * pr);
-            for (int e = threadIdx.x; e < 2 * kN * kN / 4; e += kThreadsS) {
-                const int mm = e / (kN * kN / 4);
-                const int rem = e - mm * (kN * kN / 4);
-                const int r = rem >> 4, q = rem & 15;
-                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (mm < nvalid && r < n) {
-                    const int64_t roff = base + static_cast<int64_t>(mm) * n * n + static_cast<int64_t>(r) * n;
-                    x = load_row4(X, roff, n, q);
-                    if (plan.form.Xk) {           // ADMM: M = C - X_k / sigma - Diag(y) (R22)
-                        const float4 k = load_row4(plan.form.Xk, roff, n, q);
+        // X_0 = sym_upper(X) / lambda~ into a slot: this row's upper part (column chunks left of the
+        // warp's first row are below the diagonal for every lane: skipped), then the mirror
+        // X_0 in fp32: x * fl(1 / lambda~), the operand scale (a power of two) applied exactly
+        auto store_x0 = [&](const float (&xr)[kN], double inv, int slot_off) {
+            const float is = static_cast<float>(inv) * plan.s_x0;
+            const float2 invs = make_float2(is, is);
+#pragma unroll
+            for (int j = 0; j < kN / 8; ++j) {
+                if (j < 2 * warp) continue;
+                float2 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = mul2(make_float2(xr[8 * j + 2 * q], xr[8 * j + 2 * q + 1]), invs);
+                store_operand8<kSplit>(mat + slot_off, rbase + ((j ^ rx) << 4), v);
+            }
+            __syncthreads();
+            mirror_slot<kSplit>(smem, slot_off, warp, lane);
+            fence_proxy_async_smem();
+            __syncthreads();
+        };
+        // the input rows kept in TMEM columns [64, 128) from the first read on (X is read once)
+        auto x_from_tmem = [&](float (&xr)[kN]) {
+            ptx::tmem_ld_32x32b_x32(tmem_x, *reinterpret_cast<uint32_t(*)[32]>(xr));
+            ptx::tmem_ld_32x32b_x32(tmem_x + 32, *reinterpret_cast<uint32_t(*)[32]>(xr + 32));
+            ptx::tmem_ld_wait();
+        };
+
+        // ---- bound: lambda~ = ||X||_F over the upper triangle, fp64, fixed reduction order
+        double lam, inv;
+        {
+            float xr[kN];
+            // the upper part (c >= r; whole 4-column groups that reach the diagonal) of the input
+            // rows -- X, or the ADMM argument M = X - X_k / sigma - Diag(y) (R22); the lower
+            // triangle is never read (R10).  Coalesced: per instruction, lanes 0-15 read one row of
+            // matrix 0 and lanes 16-31 the same row of matrix 1 (2 x 256 B); the rows are handed to
+            // the row-per-thread layout through fp32 staging in the (still free) Y and U slots.
+            {
+                float4* xs = reinterpret_cast<float4*>(mat + L::kY);     // 64 x 16 float4, swizzled
+                const int cl = lane & 15;
+                const int c4 = 4 * cl;
+                // all 16 loads in flight before the first use (predicated, no branches between them)
+                float4 xv[16];
+                const int64_t base = static_cast<int64_t>(b) * n * n + c4;
+                auto pred = [&](int i) { const int r = 16 * warp + i; return valid && r < n && c4 < n && c4 + 3 >= r; };
+                if (vec) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        xv[i] = ldg4_pred(X + base + static_cast<int64_t>(16 * warp + i) * n, pred(i));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) xv[i] = ldg4_tail(X + base + static_cast<int64_t>(16 * warp + i) * n, pred(i), n - c4);
+                }
+                if (plan.form.Xk) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = 16 * warp + i;
+                        const float* kp = plan.form.Xk + base + static_cast<int64_t>(r) * n;
+                        const float4 k = vec ? ldg4_pred(kp, pred(i)) : ldg4_tail(kp, pred(i), n - c4);
+                        float4& x = xv[i];
                         x.x = __fsub_rn(x.x, __fmul_rn(k.x, plan.form.inv_sigma));
                         x.y = __fsub_rn(x.y, __fmul_rn(k.y, plan.form.inv_sigma));
                         x.z = __fsub_rn(x.z, __fmul_rn(k.z, plan.form.inv_sigma));
                         x.w = __fsub_rn(x.w, __fmul_rn(k.w, plan.form.inv_sigma));
-                        if (plan.form.y && (r >> 2) == q) {
-                            const float yv = plan.form.y[static_cast<int64_t>(2 * pr + mm) * n + r];
-                            const int d = r & 3;
-                            if (d == 0) x.x = __fsub_rn(x.x, yv);
-                            if (d == 1) x.y = __fsub_rn(x.y, yv);
-                            if (d == 2) x.z = __fsub_rn(x.z, yv);
-                            if (d == 3) x.w = __fsub_rn(x.w, yv);
+                        if (plan.form.y && pred(i) && r >= c4 && r < c4 + 4) {
+                            const float yv = plan.form.y[static_cast<int64_t>(b) * n + r];
+                            if (r == c4 + 0) x.x = __fsub_rn(x.x, yv);
+                            if (r == c4 + 1) x.y = __fsub_rn(x.y, yv);
+                            if (r == c4 + 2) x.z = __fsub_rn(x.z, yv);
+                            if (r == c4 + 3) x.w = __fsub_rn(x.w, yv);
                         }
                     }
                 }
-                // XOR-swizzle float4 columns by row to keep the transposed reads conflict-light
-                reinterpret_cast<float4*>(smem + mm * L::kPerMatrix + L::kU)[r * 16 + (q ^ (r & 15))] = x;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int r = 16 * warp + i;
+                    xs[r * 16 + (cl ^ (r & 15))] = xv[i];
+                }
+                __syncwarp();                    // the warp reads back only the rows it wrote
+#pragma unroll
+                for (int q = 0; q < kN / 4; ++q) {
+                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (q >= 4 * warp) x = xs[row * 16 + (q ^ (row & 15))];   // left of the warp's rows: lower
+                    xr[4 * q + 0] = x.x;
+                    xr[4 * q + 1] = x.y;
+                    xr[4 * q + 2] = x.z;
+                    xr[4 * q + 3] = x.w;
+                }
             }
+            const long long t_ld = kDebug ? clock64() : 0;
+            // the next pair's matrices into L2 while this pair's chain runs (bulk prefetch: one
+            // instruction per contiguous matrix when its start is 16-byte aligned)
+            if (pr + static_cast<int>(gridDim.x) < pairs && (lane & 15) == 0 && warp == 0) {
+                const int bn = 2 * (pr + gridDim.x) + m;
+                if (bn < batch) {
+                    const float* nx = X + static_cast<int64_t>(bn) * n * n;
+                    if (((n * n) & 3) == 0) {
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nx), "r"(n * n * 4) : "memory");
+                        if (plan.form.Xk)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                         :: "l"(plan.form.Xk + static_cast<int64_t>(bn) * n * n), "r"(n * n * 4) : "memory");
+                    } else {
+                        for (int o = 0; o < n * n; o += 32) asm volatile("prefetch.global.L2 [%0];" :: "l"(nx + o));
+                    }
+                }
+            }
+            ptx::tmem_st_32x32b_x32(tmem_x, *reinterpret_cast<const uint32_t(*)[32]>(xr));
+            ptx::tmem_st_32x32b_x32(tmem_x + 32, *reinterpret_cast<const uint32_t(*)[32]>(xr + 32));
+            // sum of x^2 over c > row (counted twice) and the diagonal; four independent fp64
+            // accumulators (fixed combination order: deterministic)
+            double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+            double dg = 0.0;
+#pragma unroll
+            for (int g = 0; g < kN / 16; ++g) {
+                if (g < warp) continue;                          // left of the warp's first row
+#pragma unroll
+                for (int c = 16 * g; c < 16 * g + 16; ++c) {
+                    const double x = xr[c];
+                    if (c > row) acc4[c & 3] = fma(x, x, acc4[c & 3]);
+                    if (c == row) dg = x * x;
+                }
+            }
+            double ss = fma(2.0, (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]), dg);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);   // within 16 lanes
+            if ((lane & 15) == 0) red[m * 4 + warp] = ss;
+            ptx::tmem_st_wait();
             __syncthreads();
-        };
-        auto stage_at = [&](int r, int c) -> float {      // swizzled staging read
-            return stage[r * kN + (((c >> 2) ^ (r & 15)) << 2) + (c & 3)];
-        };
-        stage_X();
-        double ss = 0.0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int c = c0 + i;
-            if (c >= row) {
-                const double x = stage_at(row, c);                         // upper triangle (R10)
-                ss += (c == row ? 1.0 : 2.0) * x * x;
+            const double lsum = ((red[m * 4 + 0] + red[m * 4 + 1]) + red[m * 4 + 2]) + red[m * 4 + 3];
+            lam = sqrt(lsum);
+            if (!isfinite(lam)) {
+                if (lane == 0 && warp == 0 && valid) atomicOr(status, 1u);
+                if (lane == 16 && warp == 0 && valid) atomicOr(status, 1u);
+                lam = __longlong_as_double(0x7ff8000000000000LL);
+            }
+            if (valid && warp == 0 && (lane & 15) == 0 && lambda_out) lambda_out[b] = lam;
+            inv = lam > 0.0 ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);
+            const long long t_lam = kDebug ? clock64() : 0;
+            store_x0(xr, inv, L::kZ);
+            if (kDebug && plan.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+                atomicAdd(plan.dbg + 8, static_cast<unsigned long long>(t_ld - t_pair));    // loads
+                if (pr == static_cast<int>(blockIdx.x)) atomicAdd(plan.dbg + 11, static_cast<unsigned long long>(t_ld - t_pair));
+                atomicAdd(plan.dbg + 9, static_cast<unsigned long long>(t_lam - t_ld));    // bound
+                atomicAdd(plan.dbg + 10, static_cast<unsigned long long>(clock64() - t_lam));   // X_0 + mirror
             }
         }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);   // within 16 lanes
-        if ((lane & 15) == 0) red[m * kWarps + warp] = ss;
-        __syncthreads();
-        double lsum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) lsum += red[m * kWarps + w];             // fixed order
-        double lam = sqrt(lsum);
-        if (!isfinite(lam)) {
-            if ((lane & 15) == 0 && warp == 0 && valid) atomicOr(status, 1u);
-            lam = __longlong_as_double(0x7ff8000000000000LL);
-        }
-        if (valid && warp == 0 && (lane & 15) == 0 && lambda_out) lambda_out[b] = lam;
-        const double inv = lam > 0.0 ? 1.0 / lam : (lam == 0.0 ? 0.0 : lam);
-        auto store_x0 = [&](int slot_off) {               // X_0 = sym_upper(X) / lambda~ from staging
-            float x0[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int c = c0 + i;
-                const float x = (c >= row) ? stage_at(row, c) : stage_at(c, row);
-                x0[i] = static_cast<float>(static_cast<double>(x) * inv);
-            }
-            store_row<kSplit>(mat + slot_off, row, half, x0, plan.s_x0);
-        };
-        store_x0(L::kZ);
-        fence_proxy_async_smem();
-        __syncthreads();
 
+        if (kDebug && plan.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+            atomicAdd(plan.dbg + 5, static_cast<unsigned long long>(clock64() - t_pair));   // load, bound, X_0
+            atomicAdd(plan.dbg + 7, 1ull);
+        }
         // ---- the chain of products
+#pragma unroll 1
         for (int si = 0; si < plan.nsteps; ++si) {
-            const SmallStep st = plan.steps[si];
+            const SmallStep& st = plan.steps[si];
             if (st.reload_x0) {
-                // X_0 back into the Y slot for the reconstruction product (Z slot holds S; the
-                // U slots are free again and serve as staging)
-                stage_X();
-                store_x0(L::kY);
-                fence_proxy_async_smem();
-                __syncthreads();
+                // X_0 back into the Y slot for the reconstruction product (the Z slot holds S)
+                float xr[kN];
+                x_from_tmem(xr);
+                store_x0(xr, inv, L::kY);
             }
             const long long t_a = kDebug ? clock64() : 0;
+            long long t_i = t_a;
             if (threadIdx.x == 0) {
                 ptx::tc_fence_after();
 #pragma unroll 1
@@ -350,129 +584,149 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     }
                 }
                 ptx::mma_commit(mma_bar);
+                if (kDebug) t_i = clock64();
+                ptx::mbar_wait(mma_bar, mma_phase);    // only the issuer polls; the rest sleep in bar.sync
+                ptx::tc_fence_before();
             }
-            ptx::mbar_wait(mma_bar, mma_phase);
             mma_phase ^= 1;
+            __syncthreads();
             ptx::tc_fence_after();
             const long long t_b = kDebug ? clock64() : 0;
 
-            // a chain product's operand scale (a power of two, compute_scales) is folded into alpha
-            // and beta: (alpha acc + beta D) s == (alpha s) acc + (beta s) D exactly
-            const bool fold = st.final_mode == 0 && !plan.nofold;
-            const float alpha = fold ? st.alpha * st.out_scale : st.alpha;
-            const float beta = fold ? st.beta * st.out_scale : st.beta;
-            float v[32];
-            {
-                uint32_t raw[32];
-                ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * quad) << 16) + c0, raw);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = alpha * __uint_as_float(raw[i]);
-            }
-            ptx::tc_fence_before();
-            const long long t_c = kDebug ? clock64() : 0;
-            if (st.slot_d >= 0) add_row<kSplit>(mat + st.slot_d, row, half, beta, v);
             if (st.final_mode == 0) {
-                // in place: the MMA that read this slot has completed (mma_bar)
-                if (fold)
-                    store_row<kSplit, false>(mat + st.slot_out, row, half, v, 1.0f);
-                else
-                    store_row<kSplit>(mat + st.slot_out, row, half, v, st.out_scale);
-                if (st.mirror) {
-                    // the stage output Z must be exactly symmetric: its antisymmetric part would
-                    // grow like prod c_{t,0} over the stages (R20); Y and U need not be (their
-                    // rounding-level asymmetry is not amplified -- rounding model)
-                    __syncthreads();
-                    constexpr int kParts = kSplit ? 2 : 1;
-                    if (plan.mirror_scalar) {     // A/B baseline (PSD_SMALL_MIRROR_SCALAR)
-                        for (int task = threadIdx.x; task < 2 * kParts * 36; task += kThreadsS) {
-                            const int mm = task / (kParts * 36);
-                            const int part = (task / 36) % kParts;
-                            mirror_block_task(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes, task % 36);
-                        }
-                    } else {
-                        for (int task = warp; task < 2 * kParts * kMirrorGroups; task += kWarps) {
-                            const int mm = task / (kParts * kMirrorGroups);
-                            const int part = (task / kMirrorGroups) % kParts;
-                            mirror_group_warp(smem + mm * L::kPerMatrix + st.slot_out + part * kSlotBytes,
-                                              task % kMirrorGroups, lane);
-                        }
-                    }
+                // chain product: (alpha acc + beta D) s, the operand scale s (a power of two,
+                // compute_scales) folded into alpha and beta exactly; in place (the MMA that read
+                // the slots has completed).  Only the upper 8x8 blocks are computed; each writes
+                // itself and its transpose (every product is exactly symmetric, R20).  Warp w owns
+                // the 9 unordered block pairs {P, Q} with P in its row blocks {2w, 2w+1}: the three
+                // inside them, and for every other warp b the two (2w, 2b), (2w, 2b+1) if b > w,
+                // else (2w, 2b+1), (2w+1, 2b+1) -- the same count for every warp (quadrant), and
+                // every pair exactly once.
+                const float2 alpha = make_float2(st.alpha * st.out_scale, st.alpha * st.out_scale);
+                const float2 beta = make_float2(st.beta * st.out_scale, st.beta * st.out_scale);
+                const bool has_d = st.slot_d >= 0;
+                const uint32_t pd = smem_base + static_cast<uint32_t>(has_d ? st.slot_d : 0);
+                const uint32_t po = smem_base + static_cast<uint32_t>(st.slot_out);
+                switch (warp) {
+                    case 0: chain_epilogue<kSplit, 0>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    case 1: chain_epilogue<kSplit, 1>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    case 2: chain_epilogue<kSplit, 2>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    default: chain_epilogue<kSplit, 3>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
                 }
+                const long long t_c = kDebug ? clock64() : 0;
+                ptx::tc_fence_before();
                 fence_proxy_async_smem();
                 __syncthreads();
                 if (kDebug && plan.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
                     const long long t_d = clock64();
-                    atomicAdd(plan.dbg + 0, static_cast<unsigned long long>(t_b - t_a));   // MMA issue + wait
-                    atomicAdd(plan.dbg + 1, static_cast<unsigned long long>(t_c - t_b));   // TMEM loads
-                    atomicAdd(plan.dbg + 2, static_cast<unsigned long long>(t_d - t_c));   // epilogue + mirror + sync
+                    atomicAdd(plan.dbg + 0, static_cast<unsigned long long>(t_i - t_a));   // MMA issue
+                    atomicAdd(plan.dbg + 1, static_cast<unsigned long long>(t_b - t_i));   // MMA completion wait + barrier
+                    atomicAdd(plan.dbg + 2, static_cast<unsigned long long>(t_c - t_b));   // epilogue (warp 0)
+                    atomicAdd(plan.dbg + 4, static_cast<unsigned long long>(t_d - t_c));   // fences + barrier
                     atomicAdd(plan.dbg + 3, 1ull);
                 }
             } else {
-                // final: 1/2 X + 1/2 lambda~ X0 S  (mode 1)  or  S (mode 2); symmetrise via staging
-                // the input element (row, c), c >= row: X, or the ADMM argument M (R22)
-                const int64_t roff = static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
-                const float yv = (plan.form.Xk && plan.form.y && valid && row < n)
-                                     ? plan.form.y[static_cast<int64_t>(b) * n + row] : 0.0f;
-                auto input_at = [&](int c) -> float {
-                    const bool in = valid && row < n && c < n && c >= row;
-                    float x = in ? __ldg(X + roff + c) : 0.0f;
-                    if (plan.form.Xk) {
-                        const float k = in ? __ldg(plan.form.Xk + roff + c) : 0.0f;
-                        x = __fsub_rn(x, __fmul_rn(k, plan.form.inv_sigma));
-                        if (c == row) x = __fsub_rn(x, yv);
-                    }
-                    return x;
-                };
-                if (st.final_mode == 1) {
-                    // + beta X[row][c] for c >= row (the lower part is replaced by the mirror below)
-                    const float a = static_cast<float>(lam);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = a * v[i] + st.beta * input_at(c0 + i);
-                }
+                const long long t_f = kDebug ? clock64() : 0;
+                // final: P = lambda~ alpha acc + beta X  (mode 1, R5)  or
+                //        S = alpha acc + beta D          (mode 2; the sign output)
+                // computed on this row's upper part (row per thread, 32x32b loads), staged as fp32
+                // in the (consumed) operand region, and stored whole: the lower part is read back
+                // transposed (exact symmetry)
+                float* stage = reinterpret_cast<float*>(mat);          // 64 x 64 fp32, float4-swizzled
                 float4* srow = reinterpret_cast<float4*>(stage + row * kN);
-                // ADMM: X_next = sigma (P - M) is stored first, while the inputs (which the
-                // outputs may overwrite: in place) are still intact; then P
-                const bool two = st.final_mode == 1 && plan.out2;
-                for (int pass = two ? 1 : 0; pass >= 0; --pass) {
-                    if (pass == 1) {
-#pragma unroll
-                        for (int qq = 0; qq < 8; ++qq) {
-                            const int c = c0 + 4 * qq;
-                            srow[(8 * half + qq) ^ (row & 15)] =
-                                make_float4(plan.sigma2 * (v[4 * qq] - input_at(c)),
-                                            plan.sigma2 * (v[4 * qq + 1] - input_at(c + 1)),
-                                            plan.sigma2 * (v[4 * qq + 2] - input_at(c + 2)),
-                                            plan.sigma2 * (v[4 * qq + 3] - input_at(c + 3)));
-                        }
-                    } else {
-#pragma unroll
-                        for (int qq = 0; qq < 8; ++qq)
-                            srow[(8 * half + qq) ^ (row & 15)] =
-                                make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
-                    }
-                    __syncthreads();
-                    float* dst = pass == 0 ? out : plan.out2;
-                    if (valid && row < n) {
-                        float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(row) * n;
-                        if (n == kN) {
-#pragma unroll
-                            for (int qq = 0; qq < 8; ++qq) {
-                                const int c = c0 + 4 * qq;
-                                float4 o;
-                                o.x = (c + 0 >= row) ? stage_at(row, c + 0) : stage_at(c + 0, row);
-                                o.y = (c + 1 >= row) ? stage_at(row, c + 1) : stage_at(c + 1, row);
-                                o.z = (c + 2 >= row) ? stage_at(row, c + 2) : stage_at(c + 2, row);
-                                o.w = (c + 3 >= row) ? stage_at(row, c + 3) : stage_at(c + 3, row);
-                                __stcs(reinterpret_cast<float4*>(orow + c), o);
+                auto stage_at = [&](int r, int c) -> float {
+                    return stage[r * kN + (((c >> 2) ^ (r & 15)) << 2) + (c & 3)];
+                };
+                auto store_staged = [&](float* dst) {                  // after a barrier
+                    // coalesced: per instruction lanes 0-15 write one row of matrix 0, lanes 16-31
+                    // the same row of matrix 1; the lower part is the transpose of the upper
+                    if (!valid) return;
+                    const int cl = lane & 15;
+                    const int c4 = 4 * cl;
+#pragma unroll 4
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = 16 * warp + i;
+                        if (r >= n) break;
+                        float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(r) * n;
+                        if (vec) {
+                            if (c4 < n) {
+                                float4 o = reinterpret_cast<const float4*>(stage)[r * 16 + (cl ^ (r & 15))];
+                                if (c4 + 0 < r) o.x = stage_at(c4 + 0, r);
+                                if (c4 + 1 < r) o.y = stage_at(c4 + 1, r);
+                                if (c4 + 2 < r) o.z = stage_at(c4 + 2, r);
+                                if (c4 + 3 < r) o.w = stage_at(c4 + 3, r);
+                                __stcs(reinterpret_cast<float4*>(orow + c4), o);
                             }
                         } else {
-                            for (int c = c0; c < min(c0 + 32, n); ++c)
-                                orow[c] = (c >= row) ? stage_at(row, c) : stage_at(c, row);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (c4 + e < n) orow[c4 + e] = (c4 + e >= r) ? stage_at(r, c4 + e) : stage_at(c4 + e, r);
                         }
                     }
+                };
+                if (st.final_mode == 1) {
+                    // the epilogue reads no operand slot: staging may start at once (the MMA has
+                    // completed).  ADMM: X_next = sigma (P - M) first, then P; both from
+                    // the accumulator and the input rows kept in TMEM.
+                    const float lamf = static_cast<float>(lam);
+#pragma unroll 1
+                    for (int pass = plan.out2 ? 1 : 0; pass >= 0; --pass) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (32 * h + 31 < 16 * warp) continue;      // below the diagonal for the warp
+                            uint32_t r[32], xh[32];
+                            ptx::tmem_ld_32x32b_x32(tmem_row + 32 * h, r);
+                            ptx::tmem_ld_32x32b_x32(tmem_x + 32 * h, xh);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int qq = 0; qq < kN / 8; ++qq) {
+                                float o[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float x = __uint_as_float(xh[4 * qq + e]);
+                                    const float p = lamf * (st.alpha * __uint_as_float(r[4 * qq + e])) + st.beta * x;
+                                    o[e] = pass == 1 ? plan.sigma2 * (p - x) : p;
+                                }
+                                srow[((kN / 8) * h + qq) ^ (row & 15)] = make_float4(o[0], o[1], o[2], o[3]);
+                            }
+                        }
+                        __syncthreads();
+                        store_staged(pass == 0 ? out : plan.out2);
+                        __syncthreads();
+                    }
+                } else {
+                    float v[kN];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t r[32];
+                        ptx::tmem_ld_32x32b_x32(tmem_row + 32 * h, r);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[32 * h + i] = st.alpha * __uint_as_float(r[i]);
+                    }
+                    if (st.slot_d >= 0) {
+#pragma unroll
+                        for (int j = 0; j < kN / 8; ++j) {
+                            float2 d[4];
+                            load_operand8<kSplit>(mat + st.slot_d, rbase + ((j ^ rx) << 4), d);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                v[8 * j + 2 * q] += st.beta * d[q].x;
+                                v[8 * j + 2 * q + 1] += st.beta * d[q].y;
+                            }
+                        }
+                    }
+                    __syncthreads();             // every operand read is done: staging may overwrite
+#pragma unroll
+                    for (int q = 0; q < kN / 4; ++q)
+                        srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    __syncthreads();
+                    store_staged(out);
                     __syncthreads();
                 }
+                if (kDebug && plan.dbg && blockIdx.x == 0 && threadIdx.x == 0)
+                    atomicAdd(plan.dbg + 6, static_cast<unsigned long long>(clock64() - t_f + (t_b - t_a)));   // final product
+                ptx::tc_fence_before();
             }
         }
     }
@@ -480,7 +734,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
     __syncthreads();
     if (warp == 0) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<64>(tmem);
+        ptx::tmem_dealloc<128>(tmem);
     }
 }
 
