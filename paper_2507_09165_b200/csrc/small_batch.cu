@@ -564,22 +564,23 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             long long t_i = t_a;
             if (threadIdx.x == 0) {
                 ptx::tc_fence_after();
-#pragma unroll 1
-                for (int mm = 0; mm < 2; ++mm) {
-                    uint8_t* mb = smem + mm * L::kPerMatrix;
-                    const uint32_t a = ptx::smem_u32(mb + st.slot_a);
-                    const uint32_t bb = ptx::smem_u32(mb + st.slot_b);
-                    const uint64_t ad = ptx::smem_desc_sw128_kmajor(a), bd = ptx::smem_desc_sw128_kmajor(bb);
-                    const uint32_t d = tmem + (static_cast<uint32_t>(16 * mm) << 16);
+                // the two matrices' K steps interleaved: two independent accumulation chains in
+                // flight (each MMA of a chain waits for the previous one's accumulator)
+                const uint32_t a0 = ptx::smem_u32(smem + st.slot_a), b0 = ptx::smem_u32(smem + st.slot_b);
+                const uint64_t ad0 = ptx::smem_desc_sw128_kmajor(a0), bd0 = ptx::smem_desc_sw128_kmajor(b0);
+                constexpr uint64_t kMatDesc = static_cast<uint64_t>(L::kPerMatrix >> 4);   // next matrix
+                constexpr uint64_t kLoDesc = static_cast<uint64_t>(kSlotBytes >> 4);       // lo part
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
-                        ptx::mma_f16(d, ad + koff, bd + koff, kIdesc, k != 0);
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
+#pragma unroll
+                    for (int mm = 0; mm < 2; ++mm) {
+                        const uint64_t ad = ad0 + mm * kMatDesc + koff, bd = bd0 + mm * kMatDesc + koff;
+                        const uint32_t d = tmem + (static_cast<uint32_t>(16 * mm) << 16);
+                        ptx::mma_f16(d, ad, bd, kIdesc, k != 0);
                         if constexpr (kSplit) {
-                            const uint64_t al = ptx::smem_desc_sw128_kmajor(a + kSlotBytes);
-                            const uint64_t bl = ptx::smem_desc_sw128_kmajor(bb + kSlotBytes);
-                            ptx::mma_f16(d, ad + koff, bl + koff, kIdesc, 1u);
-                            ptx::mma_f16(d, al + koff, bd + koff, kIdesc, 1u);
+                            ptx::mma_f16(d, ad, bd + kLoDesc, kIdesc, 1u);
+                            ptx::mma_f16(d, ad + kLoDesc, bd, kIdesc, 1u);
                         }
                     }
                 }
