@@ -307,7 +307,8 @@ cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int 
 // step (reading R21).  Everything runs on the symmetric operand copy X0 = X / lambda_F (entries
 // |.| <= 1, so fp16 is safe; the chain itself runs on this rounded matrix):
 //   v_0 = h / ||h||  (h: fixed counter-hash start vector, the oracle implements the same hash)
-//   k = 0..m-1:  w = X0 (X0 v_k);  two classical Gram-Schmidt passes against v_0..v_k
+//   k = 0..m-1:  w = X0 (X0 v_k) (two SYMVs over the upper 128-blocks of X0: half the bytes of
+//                a GEMV);  two classical Gram-Schmidt passes against v_0..v_k
 //                (alpha_k = the v_k coefficients); beta_k = ||w||; v_{k+1} = w / beta_k
 //   (theta, y) = largest eigenpair of the tridiagonal T_m (bisection + inverse iteration)
 //   q = V y;  sigma = q^T X0^2 q / q^T q;  r = || X0^2 q / |q| - sigma q / |q| ||
@@ -316,8 +317,6 @@ cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int 
 // ---------------------------------------------------------------------------------------------
 namespace {
 
-constexpr int kGemvRows = 32;        // rows per block
-constexpr int kGemvThreads = 256;    // 8 warps x 4 rows
 constexpr int kLzThreads = 1024;
 constexpr int kMaxLz = 64;
 
@@ -347,66 +346,106 @@ __device__ double block_sum(double v, double* red) {
     return t;
 }
 
-// y[b] = A[b] x[b] / sqrt(xnorm2[b]) (xpart == nullptr: no normalisation); ypart[b][blk] = sum y^2
+// Symmetric matrix-vector product from the upper 128-blocks of X0 only (half the bytes of a
+// full GEMV; every operand layout of the chain -- whole, or upper-only with whole diagonal
+// blocks -- holds them).  Block (I, J), I <= J, contributes X_IJ x_J to y_I and, for I < J,
+// X_IJ^T x_I to y_J; each contribution goes to its own partial slot P[b][row block][col block]
+// and lz_symv_reduce_kernel sums the slots of a row block in block order (deterministic).
+constexpr int kSymvB = 128;          // block edge
+constexpr int kSymvThreads = 256;    // 16 threads per block row (8 elements each), 16 rows per pass
+
+// x scale: 1 / sqrt(sum of xpart[b][0..xparts)) when xpart != nullptr
+__device__ __forceinline__ float symv_xscale(const double* xpart, int xparts, int b) {
+    if (!xpart) return 1.0f;
+    const double nn = sum_partials(xpart + static_cast<int64_t>(b) * xparts, xparts);
+    return static_cast<float>(nn > 0.0 ? 1.0 / sqrt(nn) : 0.0);
+}
+
 template <typename E>
-__global__ void __launch_bounds__(kGemvThreads)
-lz_gemv_kernel(const E* __restrict__ A, int npad, const float* __restrict__ x, int64_t xstride,
-               const double* __restrict__ xpart, int xparts, float* __restrict__ y, double* __restrict__ ypart) {
-    extern __shared__ float xs[];                 // npad floats
-    __shared__ double red[kGemvThreads / 32];
-    const int b = blockIdx.y;
-    double inv = 1.0;
-    if (xpart) {
-        const double nn = sum_partials(xpart + static_cast<int64_t>(b) * xparts, xparts);
-        inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-    }
-    for (int j = threadIdx.x; j < npad; j += kGemvThreads)
-        xs[j] = static_cast<float>(x[static_cast<int64_t>(b) * xstride + j] * inv);
+__global__ void __launch_bounds__(kSymvThreads, 4)
+lz_symv_kernel(const E* __restrict__ A, int npad, int nb, const float* __restrict__ x, int64_t xstride,
+               const double* __restrict__ xpart, int xparts, float* __restrict__ P, int reverse) {
+    // blockIdx.x enumerates the upper blocks row-major: (I, J), I <= J.  Consecutive launches walk
+    // the batch in opposite directions, so a launch starts on the matrices the previous one read
+    // last (still in L2)
+    const int b = reverse ? static_cast<int>(gridDim.y) - 1 - static_cast<int>(blockIdx.y) : static_cast<int>(blockIdx.y);
+    int I = 0, rem = blockIdx.x;
+    while (rem >= nb - I) { rem -= nb - I; ++I; }
+    const int J = I + rem;
+    __shared__ float xI[kSymvB], xJ[kSymvB];
+    __shared__ float colp[kSymvThreads / 16][kSymvB];       // column partials of the 16 row groups
+    const float sc = symv_xscale(xpart, xparts, b);
+    const float* xb = x + static_cast<int64_t>(b) * xstride;
+    if (threadIdx.x < kSymvB) xJ[threadIdx.x] = xb[J * kSymvB + threadIdx.x] * sc;
+    else xI[threadIdx.x - kSymvB] = xb[I * kSymvB + threadIdx.x - kSymvB] * sc;
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double acc2 = 0.0;
-    for (int rr = 0; rr < kGemvRows / 8; ++rr) {
-        const int i = blockIdx.x * kGemvRows + warp * (kGemvRows / 8) + rr;
-        if (i >= npad) break;
-        const E* row = A + (static_cast<int64_t>(b) * npad + i) * npad;
-        float s = 0.0f;
-        constexpr int kEl = 16 / sizeof(E);             // elements per 16-byte load
-        constexpr int kU = 4;                           // independent loads in flight per lane
-        for (int j0 = lane * kEl; j0 < npad; j0 += 32 * kEl * kU) {
-            uint4 raw[kU];
+    const int cq = threadIdx.x & 15;               // 8-column chunk of this thread
+    const int rg = threadIdx.x >> 4;               // row group: rows rg, rg + 16, ...
+    constexpr int kEl = 8;
+    const E* blk = A + (static_cast<int64_t>(b) * npad + static_cast<int64_t>(I) * kSymvB) * npad +
+                   static_cast<int64_t>(J) * kSymvB + cq * kEl;
+    float cs[kEl];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int j = j0 + u * 32 * kEl;
-                raw[u] = j < npad ? __ldcs(reinterpret_cast<const uint4*>(row + j)) : make_uint4(0, 0, 0, 0);
-            }
+    for (int e = 0; e < kEl; ++e) cs[e] = 0.0f;
+    float xj[kEl];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int j = j0 + u * 32 * kEl;
-                if (j < npad) {
-                    const E* e = reinterpret_cast<const E*>(&raw[u]);
+    for (int e = 0; e < kEl; ++e) xj[e] = xJ[cq * kEl + e];
+    float* Pb = P + static_cast<int64_t>(b) * nb * npad;
+    constexpr int kRows = kSymvB / 16;            // 8 rows per thread
+    constexpr int kWords = kEl * sizeof(E) / 16;  // 16-byte loads per row chunk (1 or 2)
+    uint4 raw[kRows][kWords];
 #pragma unroll
-                    for (int k = 0; k < kEl; k += 4) {
-                        const float4 xv = *reinterpret_cast<const float4*>(xs + j + k);   // 16 B smem reads
-                        s += elem_to_float<E>(e[k]) * xv.x + elem_to_float<E>(e[k + 1]) * xv.y +
-                             elem_to_float<E>(e[k + 2]) * xv.z + elem_to_float<E>(e[k + 3]) * xv.w;
-                    }
-                }
-            }
-        }
+    for (int k = 0; k < kRows; ++k) {             // all loads in flight first
+        const uint4* rp = reinterpret_cast<const uint4*>(blk + static_cast<int64_t>(rg + 16 * k) * npad);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-            y[static_cast<int64_t>(b) * npad + i] = s;
-            acc2 += static_cast<double>(s) * s;
-        }
+        for (int w = 0; w < kWords; ++w) raw[k][w] = __ldg(rp + w);
     }
-    if (lane == 0) red[warp] = acc2;
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+        const int i = rg + 16 * k;
+        float rs = 0.0f;
+        const float xi = xI[i];
+        const E* ev = reinterpret_cast<const E*>(raw[k]);
+#pragma unroll
+        for (int e = 0; e < kEl; ++e) {
+            const float a = elem_to_float<E>(ev[e]);
+            rs = fmaf(a, xj[e], rs);
+            cs[e] = fmaf(a, xi, cs[e]);
+        }
+        // row sum over the 16 threads of the row (lanes 16h .. 16h + 15 of the warp), fixed order
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (cq == 0) Pb[static_cast<int64_t>(J) * npad + I * kSymvB + i] = rs;   // slot (row block I, col J)
+    }
+    if (I == J) return;
+#pragma unroll
+    for (int e = 0; e < kEl; ++e) colp[rg][cq * kEl + e] = cs[e];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kGemvThreads / 32; ++w) t += red[w];
-        ypart[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = t;
+    if (threadIdx.x < kSymvB) {
+        float t = 0.0f;
+#pragma unroll
+        for (int g = 0; g < kSymvThreads / 16; ++g) t += colp[g][threadIdx.x];
+        Pb[static_cast<int64_t>(I) * npad + J * kSymvB + threadIdx.x] = t;         // slot (row block J, col I)
     }
+}
+
+// y[b][rows of block I] = sum over column blocks J of P[b][J][rows] (J = 0..nb-1, fixed order);
+// ypart[b][I] = sum of y^2 over the block (fp64)
+__global__ void __launch_bounds__(kSymvB)
+lz_symv_reduce_kernel(const float* __restrict__ P, int npad, int nb, float* __restrict__ y, double* __restrict__ ypart) {
+    __shared__ double red[kSymvB / 32];
+    const int b = blockIdx.y, I = blockIdx.x;
+    const int i = I * kSymvB + threadIdx.x;
+    const float* Pb = P + static_cast<int64_t>(b) * nb * npad;
+    float t = 0.0f;
+    for (int J = 0; J < nb; ++J) t += Pb[static_cast<int64_t>(J) * npad + i];
+    y[static_cast<int64_t>(b) * npad + i] = t;
+    double s2 = static_cast<double>(t) * t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) ypart[static_cast<int64_t>(b) * nb + I] = ((red[0] + red[1]) + red[2]) + red[3];
 }
 
 __device__ __forceinline__ float start_hash(int j) {
@@ -442,31 +481,55 @@ lz_step_kernel(float* __restrict__ V, float* __restrict__ W, int npad, int64_t v
     float* Vb = V + static_cast<int64_t>(b) * vstride;
     float* w = W + static_cast<int64_t>(b) * npad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n4 = npad >> 2;                    // float4 groups (npad is a multiple of 128)
     double alpha = 0.0;
     for (int pass = 0; pass < 2; ++pass) {
+        // c_i = v_i . w: warp i (i, i + 32, ...), float4 loads, lane partials in fp64, fixed order
         for (int i = warp; i <= k; i += kLzThreads / 32) {
-            const float* vi = Vb + static_cast<int64_t>(i) * npad;
+            const float4* vi = reinterpret_cast<const float4*>(Vb + static_cast<int64_t>(i) * npad);
+            const float4* w4 = reinterpret_cast<const float4*>(w);
             double s = 0.0;
-            for (int j = lane; j < npad; j += 32) s += static_cast<double>(vi[j]) * w[j];
+            for (int j = lane; j < n4; j += 32) {
+                const float4 a = vi[j], x = w4[j];
+                s += (static_cast<double>(a.x) * x.x + static_cast<double>(a.y) * x.y) +
+                     (static_cast<double>(a.z) * x.z + static_cast<double>(a.w) * x.w);
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) c[i] = s;
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < npad; j += kLzThreads) {
-            double t = w[j];
-            for (int i = 0; i <= k; ++i) t -= c[i] * Vb[static_cast<int64_t>(i) * npad + j];
-            w[j] = static_cast<float>(t);
+        // w -= sum_i c_i v_i, four consecutive entries per thread
+        for (int j = threadIdx.x; j < n4; j += kLzThreads) {
+            const float4 x = reinterpret_cast<const float4*>(w)[j];
+            double t0 = x.x, t1 = x.y, t2 = x.z, t3 = x.w;
+            for (int i = 0; i <= k; ++i) {
+                const float4 a = reinterpret_cast<const float4*>(Vb + static_cast<int64_t>(i) * npad)[j];
+                t0 -= c[i] * a.x;
+                t1 -= c[i] * a.y;
+                t2 -= c[i] * a.z;
+                t3 -= c[i] * a.w;
+            }
+            reinterpret_cast<float4*>(w)[j] = make_float4(static_cast<float>(t0), static_cast<float>(t1),
+                                                          static_cast<float>(t2), static_cast<float>(t3));
         }
         alpha += c[k];
         __syncthreads();
     }
     double s = 0.0;
-    for (int j = threadIdx.x; j < npad; j += kLzThreads) s += static_cast<double>(w[j]) * w[j];
+    for (int j = threadIdx.x; j < n4; j += kLzThreads) {
+        const float4 x = reinterpret_cast<const float4*>(w)[j];
+        s += (static_cast<double>(x.x) * x.x + static_cast<double>(x.y) * x.y) +
+             (static_cast<double>(x.z) * x.z + static_cast<double>(x.w) * x.w);
+    }
     const double beta = sqrt(block_sum(s, red));
     const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
-    float* vn = Vb + static_cast<int64_t>(k + 1) * npad;
-    for (int j = threadIdx.x; j < npad; j += kLzThreads) vn[j] = static_cast<float>(w[j] * inv);
+    float4* vn = reinterpret_cast<float4*>(Vb + static_cast<int64_t>(k + 1) * npad);
+    for (int j = threadIdx.x; j < n4; j += kLzThreads) {
+        const float4 x = reinterpret_cast<const float4*>(w)[j];
+        vn[j] = make_float4(static_cast<float>(x.x * inv), static_cast<float>(x.y * inv),
+                            static_cast<float>(x.z * inv), static_cast<float>(x.w * inv));
+    }
     if (threadIdx.x == 0) {
         AB[static_cast<int64_t>(b) * 2 * kMaxLz + k] = alpha;
         AB[static_cast<int64_t>(b) * 2 * kMaxLz + kMaxLz + k] = beta;
@@ -597,33 +660,32 @@ __global__ void lz_finalize_kernel(const double* __restrict__ wpart, int parts, 
 }
 
 template <typename E>
-void gemv_launch(const void* A, int npad, int parts, int batch, const float* x, int64_t xstride, const double* xpart,
-                 int xparts, float* y, double* ypart, cudaStream_t stream) {
-    lz_gemv_kernel<E><<<dim3(parts, batch), kGemvThreads, static_cast<size_t>(npad) * 4, stream>>>(
-        static_cast<const E*>(A), npad, x, xstride, xpart, xparts, y, ypart);
+void symv_launch(const void* A, int npad, int batch, const float* x, int64_t xstride, const double* xpart, int xparts,
+                 float* P, float* y, double* ypart, int reverse, cudaStream_t stream) {
+    const int nb = npad / kSymvB;
+    lz_symv_kernel<E><<<dim3(nb * (nb + 1) / 2, batch), kSymvThreads, 0, stream>>>(
+        static_cast<const E*>(A), npad, nb, x, xstride, xpart, xparts, P, reverse);
+    lz_symv_reduce_kernel<<<dim3(nb, batch), kSymvB, 0, stream>>>(P, npad, nb, y, ypart);
 }
 
 }  // namespace
 
-void lanczos_prepare() {
-    cudaFuncSetAttribute(lz_gemv_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lz_gemv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lz_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-}
+void lanczos_prepare() {}
 
-int lanczos_parts(int npad) { return (npad + kGemvRows - 1) / kGemvRows; }
+int lanczos_parts(int npad) { return npad / kSymvB; }
 
-int lanczos_launches(int steps, int n) { return 3 * (steps < n ? steps : n) + 6; }
+int lanczos_launches(int steps, int n) { return 5 * (steps < n ? steps : n) + 8; }
 
 size_t lanczos_scratch_bytes(int npad, int batch, int steps) {
     const size_t parts = static_cast<size_t>(lanczos_parts(npad));
     return static_cast<size_t>(batch) * npad * 4 * (steps + 1 + 4) +           // V, t, w, q, z
+           static_cast<size_t>(batch) * npad * 4 * parts +                    // SYMV partials
            static_cast<size_t>(batch) * 8 * (2 * kMaxLz + 2 * parts + 16 + 1) + 256;
 }
 
 cudaError_t launch_lanczos_bound(OpType t, const void* X0, double s0, int n, int npad, int batch, int steps,
                                  double safety, void* scratch, double* lambda, double* lambda_out, cudaStream_t stream) {
-    if (static_cast<size_t>(npad) * 4 > 200 * 1024 || steps < 1 || steps > kMaxLz) return cudaErrorInvalidValue;
+    if (npad % kSymvB != 0 || steps < 1 || steps > kMaxLz) return cudaErrorInvalidValue;
     const int m = steps < n ? steps : n;
     const int parts = lanczos_parts(npad);
     const int64_t vstride = static_cast<int64_t>(m + 1) * npad;
@@ -632,27 +694,30 @@ cudaError_t launch_lanczos_bound(OpType t, const void* X0, double s0, int n, int
     float* wv = tv + static_cast<int64_t>(batch) * npad;
     float* qv = wv + static_cast<int64_t>(batch) * npad;
     float* zv = qv + static_cast<int64_t>(batch) * npad;
-    double* AB = reinterpret_cast<double*>(zv + static_cast<int64_t>(batch) * npad);
+    float* P = zv + static_cast<int64_t>(batch) * npad;
+    double* AB = reinterpret_cast<double*>(P + static_cast<int64_t>(batch) * npad * parts);
     double* pa = AB + static_cast<int64_t>(batch) * 2 * kMaxLz;
     double* pb = pa + static_cast<int64_t>(batch) * parts;
     double* pr = pb + static_cast<int64_t>(batch) * parts;
     double* qn2 = pr + static_cast<int64_t>(batch) * 16;
-    auto gemv = [&](const float* x, int64_t xs, const double* xp, int xps, float* y, double* yp) {
+    int dir = 0;
+    auto symv = [&](const float* x, int64_t xs, const double* xp, int xps, float* y, double* yp) {
         switch (t) {
-            case OpType::F16: gemv_launch<__half>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
-            case OpType::BF16: gemv_launch<__nv_bfloat16>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
-            case OpType::TF32: gemv_launch<float>(X0, npad, parts, batch, x, xs, xp, xps, y, yp, stream); break;
+            case OpType::F16: symv_launch<__half>(X0, npad, batch, x, xs, xp, xps, P, y, yp, dir, stream); break;
+            case OpType::BF16: symv_launch<__nv_bfloat16>(X0, npad, batch, x, xs, xp, xps, P, y, yp, dir, stream); break;
+            case OpType::TF32: symv_launch<float>(X0, npad, batch, x, xs, xp, xps, P, y, yp, dir, stream); break;
         }
+        dir ^= 1;
     };
     lz_init_kernel<<<batch, kLzThreads, 0, stream>>>(V, n, npad, vstride);
     for (int k = 0; k < m; ++k) {
-        gemv(V + static_cast<int64_t>(k) * npad, vstride, nullptr, 0, tv, pa);   // t = X0 v_k
-        gemv(tv, npad, nullptr, 0, wv, pa);                                      // w = X0 t
+        symv(V + static_cast<int64_t>(k) * npad, vstride, nullptr, 0, tv, pa);   // t = X0 v_k
+        symv(tv, npad, nullptr, 0, wv, pa);                                      // w = X0 t
         lz_step_kernel<<<batch, kLzThreads, 0, stream>>>(V, wv, npad, vstride, k, AB);
     }
     lz_ritz_kernel<<<batch, kLzThreads, 0, stream>>>(V, npad, vstride, m, AB, qv, qn2);
-    gemv(qv, npad, qn2, 1, wv, pa);        // w = X0 q / |q|,  sigma = |w|^2
-    gemv(wv, npad, pa, parts, zv, pb);     // z = X0 w / |w|
+    symv(qv, npad, qn2, 1, wv, pa);        // w = X0 q / |q|,  sigma = |w|^2
+    symv(wv, npad, pa, parts, zv, pb);     // z = X0 w / |w|
     constexpr int kRBlocks = 16;
     lz_residual_kernel<<<dim3(kRBlocks, batch), 256, 0, stream>>>(qv, qn2, zv, pa, parts, npad, pr);
     lz_finalize_kernel<<<batch, 1, 0, stream>>>(pa, parts, pr, kRBlocks, s0, safety, lambda, lambda_out);
