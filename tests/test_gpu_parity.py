@@ -136,13 +136,20 @@ def test_sym_product_parity(pkg):
     assert np.array_equal(C, C.T)
 
 
-def test_batch_position_determinism_and_inplace(pkg):
-    """The same matrix at different batch positions gives bitwise-equal output; out == X works."""
-    x = synth.goe(192, 11)
-    X = np.stack([x, synth.goe(192, 12), x])
-    P, _, _ = _gpu(pkg, _product_filter("half", pkg), X, "fp16")
-    assert np.array_equal(P[0], P[2])
-    Pi, _, _ = _gpu(pkg, _product_filter("half", pkg), X, "fp16", inplace=True)
+@pytest.mark.parametrize("n,prec,which", [
+    (192, "fp16", "half"),      # 1-CTA product kernel
+    (64, "fp16", "c2"),         # batched small-n kernel: positions 0 and 3 are the two halves of a pair
+    (64, "fp16x3", "c2"),
+    (33, "fp16", "half"),       # small-n kernel, rows not a multiple of 4 (scalar loads)
+])
+def test_batch_position_determinism_and_inplace(pkg, n, prec, which):
+    """The same matrix at different batch positions gives bitwise-equal output; out == X works
+    and equals the out-of-place result bitwise."""
+    x = synth.goe(n, 11)
+    X = np.stack([x, synth.goe(n, 12), synth.goe(n, 13), x])
+    P, _, _ = _gpu(pkg, _product_filter(which, pkg), X, prec)
+    assert np.array_equal(P[0], P[3])
+    Pi, _, _ = _gpu(pkg, _product_filter(which, pkg), X, prec, inplace=True)
     assert np.array_equal(Pi, P)
 
 
