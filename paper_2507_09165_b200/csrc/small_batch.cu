@@ -31,7 +31,10 @@ namespace {
 
 constexpr int kN = 64;                  // padded matrix edge
 constexpr int kSlotBytes = kN * 128;    // 64 rows x 128 B (fp16), one SW128 atom wide
-constexpr int kThreadsS = 128;          // 4 warps: warp = TMEM lane quadrant, lane >> 4 = matrix
+// 4 warps (16-bit: 4 CTAs/SM at 128 registers) or 8 warps (split path: 2 CTAs/SM, two warps per
+// TMEM quadrant, each with half the columns and one matrix of the chain epilogue -- measured
+// 319 -> 277 us at c2 fp16x3; at fp16 the 8-warp layout needs 64 registers and spills: 139 -> 164 us)
+template <bool kSplit> constexpr int kWarpsS = kSplit ? 8 : 4;
 
 // byte offset of the 16-byte chunk `chunk` (8 fp16 columns) of row `row` in a SW128 K-major slot
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
@@ -47,7 +50,7 @@ struct SmallLayout {
     static constexpr int kY = kParts * kSlotBytes;
     static constexpr int kU = 2 * kParts * kSlotBytes;
     static constexpr int kPerMatrix = 3 * kParts * kSlotBytes;
-    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 128;   // + align slack, barrier, tmem slot, partial sums
+    static constexpr int kBytes = 2 * kPerMatrix + 1024 + 256;   // + align slack, barrier, tmem slot, partial sums
 };
 // resident CTAs per SM: 4 x 49 KB (16-bit), 2 x 97 KB (split)
 template <bool kSplit> constexpr int kSmallCtasPerSm = kSplit ? 2 : 4;
@@ -162,7 +165,7 @@ __device__ __forceinline__ void mirror_slot(uint8_t* smem, int slot_off, int war
     using L = SmallLayout<kSplit>;
     constexpr int kTasks = 2 * L::kParts * kMirrorGroups;
 #pragma unroll 1
-    for (int task = warp; task < kTasks; task += kThreadsS / 32) {
+    for (int task = warp; task < kTasks; task += kWarpsS<kSplit>) {
         const int mm = task / (L::kParts * kMirrorGroups);
         const int part = (task / kMirrorGroups) % L::kParts;
         mirror_group_warp(smem + mm * L::kPerMatrix + slot_off + part * kSlotBytes, task % kMirrorGroups, lane);
@@ -308,69 +311,89 @@ __device__ __forceinline__ void region_store(const uint32_t (&a)[8], uint32_t pd
         stsm_x2_trans(po + kSlotBytes + ot, g0.lo, g1.lo);
     }
 }
+// accumulator fragments of matrix mm for warp W's blocks (caller waits)
+template <int W>
+struct EpiFrags {
+    uint32_t aW[8], a0[8], a1[8], a2[8];
+};
+template <int W>
+__device__ __forceinline__ void epi_load(uint32_t tmem, int mm, EpiFrags<W>& f) {
+    const uint32_t tb = tmem + (static_cast<uint32_t>(32 * W + 16 * mm) << 16);
+    tmem_ld_16x256b_x2(tb + 16 * W, f.aW);
+    region_load<W, 0>(tb, f.a0);
+    region_load<W, 1>(tb, f.a1);
+    region_load<W, 2>(tb, f.a2);
+}
 template <bool kSplit, int W>
-__device__ __forceinline__ void chain_epilogue(uint32_t tmem, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
-                                               bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
+__device__ __forceinline__ void epi_store(const EpiFrags<W>& f, int mm, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
+                                          bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
     constexpr int R0 = 2 * W;
     const uint32_t lrow = lane & 7, lq = lane >> 3, lq1 = lq & 1;
     const uint32_t lrow128 = lrow * 128;
     // blocks inside the warp's rows, lane group q: [(R0,R0), (R1,R0), (R0,R1), (R1,R1)]
     const uint32_t offW = (8 * R0) * 128 + (lq & 1) * 1024 + lrow128 + (((R0 + (lq >> 1)) ^ lrow) << 4);
-    // both matrices' accumulator fragments in flight before the first wait
-    uint32_t aWs[2][8], a0s[2][8], a1s[2][8], a2s[2][8];
-#pragma unroll
-    for (int mm = 0; mm < 2; ++mm) {
-        const uint32_t tb = tmem + (static_cast<uint32_t>(32 * W + 16 * mm) << 16);
-        tmem_ld_16x256b_x2(tb + 16 * W, aWs[mm]);
-        region_load<W, 0>(tb, a0s[mm]);
-        region_load<W, 1>(tb, a1s[mm]);
-        region_load<W, 2>(tb, a2s[mm]);
-    }
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int mm = 0; mm < 2; ++mm) {
-        const uint32_t (&aW)[8] = aWs[mm];
-        const uint32_t (&a0)[8] = a0s[mm];
-        const uint32_t (&a1)[8] = a1s[mm];
-        const uint32_t (&a2)[8] = a2s[mm];
-        const uint32_t pd = pd0 + mm * mat_bytes, po = po0 + mm * mat_bytes;
-        {
-            uint32_t dh[4] = {0, 0, 0, 0}, dl[4] = {0, 0, 0, 0};
-            if (has_d) {
-                ldsm_x4(pd + offW, dh);
-                if constexpr (kSplit) ldsm_x4(pd + kSlotBytes + offW, dl);
-            }
-            const Frag<kSplit> f0 = combine<kSplit>(aW[0], aW[1], has_d, dh[0], dl[0], alpha, beta);
-            const Frag<kSplit> f2 = combine<kSplit>(aW[4], aW[5], has_d, dh[2], dl[2], alpha, beta);
-            const Frag<kSplit> f3 = combine<kSplit>(aW[6], aW[7], has_d, dh[3], dl[3], alpha, beta);
-            const uint32_t h[4] = {diag_upper(f0.hi, diag_mask), movmatrix_trans(f2.hi), f2.hi, diag_upper(f3.hi, diag_mask)};
-            stsm_x4(po + offW, h);
-            if constexpr (kSplit) {
-                const uint32_t l[4] = {diag_upper(f0.lo, diag_mask), movmatrix_trans(f2.lo), f2.lo, diag_upper(f3.lo, diag_mask)};
-                stsm_x4(po + kSlotBytes + offW, l);
-            }
+    const uint32_t pd = pd0 + mm * mat_bytes, po = po0 + mm * mat_bytes;
+    {
+        uint32_t dh[4] = {0, 0, 0, 0}, dl[4] = {0, 0, 0, 0};
+        if (has_d) {
+            ldsm_x4(pd + offW, dh);
+            if constexpr (kSplit) ldsm_x4(pd + kSlotBytes + offW, dl);
         }
-        region_store<kSplit, W, 0>(a0, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
-        region_store<kSplit, W, 1>(a1, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
-        region_store<kSplit, W, 2>(a2, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+        const Frag<kSplit> f0 = combine<kSplit>(f.aW[0], f.aW[1], has_d, dh[0], dl[0], alpha, beta);
+        const Frag<kSplit> f2 = combine<kSplit>(f.aW[4], f.aW[5], has_d, dh[2], dl[2], alpha, beta);
+        const Frag<kSplit> f3 = combine<kSplit>(f.aW[6], f.aW[7], has_d, dh[3], dl[3], alpha, beta);
+        const uint32_t h[4] = {diag_upper(f0.hi, diag_mask), movmatrix_trans(f2.hi), f2.hi, diag_upper(f3.hi, diag_mask)};
+        stsm_x4(po + offW, h);
+        if constexpr (kSplit) {
+            const uint32_t l[4] = {diag_upper(f0.lo, diag_mask), movmatrix_trans(f2.lo), f2.lo, diag_upper(f3.lo, diag_mask)};
+            stsm_x4(po + kSlotBytes + offW, l);
+        }
+    }
+    region_store<kSplit, W, 0>(f.a0, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+    region_store<kSplit, W, 1>(f.a1, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+    region_store<kSplit, W, 2>(f.a2, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+}
+// the chain-product epilogue of warp W: matrix `mm` (mm < 0: both matrices, their fragments loaded
+// before one wait)
+template <bool kSplit, int W>
+__device__ __forceinline__ void chain_epilogue(uint32_t tmem, int mm, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
+                                               bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
+    if (mm >= 0) {
+        EpiFrags<W> f;
+        epi_load<W>(tmem, mm, f);
+        ptx::tmem_ld_wait();
+        epi_store<kSplit, W>(f, mm, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
+    } else {
+        EpiFrags<W> f0, f1;
+        epi_load<W>(tmem, 0, f0);
+        epi_load<W>(tmem, 1, f1);
+        ptx::tmem_ld_wait();
+        epi_store<kSplit, W>(f0, 0, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
+        epi_store<kSplit, W>(f1, 1, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
     }
 }
 
 template <bool kSplit>
-__global__ void __launch_bounds__(kThreadsS, kSmallCtasPerSm<kSplit>)
+__global__ void __launch_bounds__(32 * kWarpsS<kSplit>, kSmallCtasPerSm<kSplit>)
 small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, int batch,
                    double* __restrict__ lambda_out, unsigned* __restrict__ status,
                    const __grid_constant__ SmallPlan plan) {
     using L = SmallLayout<kSplit>;
+    constexpr int kWarps = kWarpsS<kSplit>;
+    constexpr int kQW = kWarps / 4;              // warps per TMEM quadrant
+    constexpr int kCT = kN / kQW;                // columns per thread in the row-per-thread phases
+    constexpr int kRW = 16 / kQW;                // rows per warp in the coalesced load / store phases
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = ptx::align_smem_1024(smem_raw);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
-    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][4 warps]
+    double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][8 warps]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m = lane >> 4;                     // row-per-thread phases: matrix of the pair
-    const int row = 16 * warp + (lane & 15);     // its row (TMEM lane 32 warp + lane)
+    const int q = warp & 3;                      // TMEM lane quadrant (warp % 4, the hardware rule)
+    const int hw = warp >> 2;                    // 8 warps: column half (row-per-thread phases) / matrix (chain epilogue)
+    const int m = lane >> 4;                     // row-per-thread phases: matrix of the pair this thread serves
+    const int row = 16 * q + (lane & 15);        // its row (TMEM lane 32 q + lane)
     const int rx = row & 7;                      // its SW128 chunk swizzle
     const uint32_t rbase = static_cast<uint32_t>(row * 128);
     uint8_t* mat = smem + m * L::kPerMatrix;
@@ -390,8 +413,8 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tmem_row = tmem + (static_cast<uint32_t>(32 * warp) << 16);
-    const uint32_t tmem_x = tmem_row + 64;
+    const uint32_t tmem_row = tmem + (static_cast<uint32_t>(32 * q) << 16);
+    const uint32_t tmem_x = tmem_row + 64 + kCT * hw;     // this thread's input columns
     constexpr uint32_t kIdesc = ptx::make_idesc(0, 64, 64);   // f16 x f16 -> f32, M=64, N=64
     uint32_t mma_phase = 0;
 
@@ -401,18 +424,19 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
         const int b = 2 * pr + m;
         const bool valid = b < batch;
 
-        // X_0 = sym_upper(X) / lambda~ into a slot: this row's upper part (column chunks left of the
-        // warp's first row are below the diagonal for every lane: skipped), then the mirror
-        // X_0 in fp32: x * fl(1 / lambda~), the operand scale (a power of two) applied exactly
-        auto store_x0 = [&](const float (&xr)[kN], double inv, int slot_off) {
+        // X_0 = sym_upper(X) / lambda~ into a slot: this thread's 32 columns of its row (chunks
+        // left of the quadrant's first row are below the diagonal for every lane: skipped), then
+        // the mirror.  X_0 in fp32: x * fl(1 / lambda~), the operand scale (a power of two) exact.
+        auto store_x0 = [&](const float (&xr)[kCT], double inv, int slot_off) {
             const float is = static_cast<float>(inv) * plan.s_x0;
             const float2 invs = make_float2(is, is);
 #pragma unroll
-            for (int j = 0; j < kN / 8; ++j) {
-                if (j < 2 * warp) continue;
+            for (int jj = 0; jj < kCT / 8; ++jj) {
+                const int j = (kCT / 8) * hw + jj;
+                if (j < 2 * q) continue;
                 float2 v[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = mul2(make_float2(xr[8 * j + 2 * q], xr[8 * j + 2 * q + 1]), invs);
+                for (int e = 0; e < 4; ++e) v[e] = mul2(make_float2(xr[8 * jj + 2 * e], xr[8 * jj + 2 * e + 1]), invs);
                 store_operand8<kSplit>(mat + slot_off, rbase + ((j ^ rx) << 4), v);
             }
             __syncthreads();
@@ -421,41 +445,42 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             __syncthreads();
         };
         // the input rows kept in TMEM columns [64, 128) from the first read on (X is read once)
-        auto x_from_tmem = [&](float (&xr)[kN]) {
-            ptx::tmem_ld_32x32b_x32(tmem_x, *reinterpret_cast<uint32_t(*)[32]>(xr));
-            ptx::tmem_ld_32x32b_x32(tmem_x + 32, *reinterpret_cast<uint32_t(*)[32]>(xr + 32));
+        auto x_from_tmem = [&](float (&xr)[kCT]) {
+#pragma unroll
+            for (int h = 0; h < kCT / 32; ++h)
+                ptx::tmem_ld_32x32b_x32(tmem_x + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(xr + 32 * h));
             ptx::tmem_ld_wait();
         };
 
         // ---- bound: lambda~ = ||X||_F over the upper triangle, fp64, fixed reduction order
         double lam, inv;
         {
-            float xr[kN];
+            float xr[kCT];
             // the upper part (c >= r; whole 4-column groups that reach the diagonal) of the input
             // rows -- X, or the ADMM argument M = X - X_k / sigma - Diag(y) (R22); the lower
             // triangle is never read (R10).  Coalesced: per instruction, lanes 0-15 read one row of
-            // matrix 0 and lanes 16-31 the same row of matrix 1 (2 x 256 B); the rows are handed to
-            // the row-per-thread layout through fp32 staging in the (still free) Y and U slots.
+            // matrix 0 and lanes 16-31 the same row of matrix 1 (2 x 256 B); warp (q, h) reads rows
+            // 16q + 8h .. + 7; the rows reach the row-per-thread layout through fp32 staging in the
+            // (still free) Y and U slots.
             {
                 float4* xs = reinterpret_cast<float4*>(mat + L::kY);     // 64 x 16 float4, swizzled
                 const int cl = lane & 15;
                 const int c4 = 4 * cl;
-                // all 16 loads in flight before the first use (predicated, no branches between them)
-                float4 xv[16];
+                float4 xv[kRW];
                 const int64_t base = static_cast<int64_t>(b) * n * n + c4;
-                auto pred = [&](int i) { const int r = 16 * warp + i; return valid && r < n && c4 < n && c4 + 3 >= r; };
+                const int r0 = 16 * q + kRW * hw;
+                auto pred = [&](int i) { const int r = r0 + i; return valid && r < n && c4 < n && c4 + 3 >= r; };
                 if (vec) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        xv[i] = ldg4_pred(X + base + static_cast<int64_t>(16 * warp + i) * n, pred(i));
+                    for (int i = 0; i < kRW; ++i) xv[i] = ldg4_pred(X + base + static_cast<int64_t>(r0 + i) * n, pred(i));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) xv[i] = ldg4_tail(X + base + static_cast<int64_t>(16 * warp + i) * n, pred(i), n - c4);
+                    for (int i = 0; i < kRW; ++i) xv[i] = ldg4_tail(X + base + static_cast<int64_t>(r0 + i) * n, pred(i), n - c4);
                 }
                 if (plan.form.Xk) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = 16 * warp + i;
+                    for (int i = 0; i < kRW; ++i) {
+                        const int r = r0 + i;
                         const float* kp = plan.form.Xk + base + static_cast<int64_t>(r) * n;
                         const float4 k = vec ? ldg4_pred(kp, pred(i)) : ldg4_tail(kp, pred(i), n - c4);
                         float4& x = xv[i];
@@ -473,19 +498,20 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int r = 16 * warp + i;
+                for (int i = 0; i < kRW; ++i) {
+                    const int r = r0 + i;
                     xs[r * 16 + (cl ^ (r & 15))] = xv[i];
                 }
-                __syncwarp();                    // the warp reads back only the rows it wrote
+                __syncthreads();                 // the warps of a quadrant wrote its 16 rows
 #pragma unroll
-                for (int q = 0; q < kN / 4; ++q) {
+                for (int jq = 0; jq < kCT / 4; ++jq) {
+                    const int qq = (kCT / 4) * hw + jq;    // float4 column group
                     float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (q >= 4 * warp) x = xs[row * 16 + (q ^ (row & 15))];   // left of the warp's rows: lower
-                    xr[4 * q + 0] = x.x;
-                    xr[4 * q + 1] = x.y;
-                    xr[4 * q + 2] = x.z;
-                    xr[4 * q + 3] = x.w;
+                    if (qq >= 4 * q) x = xs[row * 16 + (qq ^ (row & 15))];   // left of the quadrant's rows: lower
+                    xr[4 * jq + 0] = x.x;
+                    xr[4 * jq + 1] = x.y;
+                    xr[4 * jq + 2] = x.z;
+                    xr[4 * jq + 3] = x.w;
                 }
             }
             const long long t_ld = kDebug ? clock64() : 0;
@@ -505,29 +531,33 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     }
                 }
             }
-            ptx::tmem_st_32x32b_x32(tmem_x, *reinterpret_cast<const uint32_t(*)[32]>(xr));
-            ptx::tmem_st_32x32b_x32(tmem_x + 32, *reinterpret_cast<const uint32_t(*)[32]>(xr + 32));
+#pragma unroll
+            for (int h = 0; h < kCT / 32; ++h)
+                ptx::tmem_st_32x32b_x32(tmem_x + 32 * h, *reinterpret_cast<const uint32_t(*)[32]>(xr + 32 * h));
             // sum of x^2 over c > row (counted twice) and the diagonal; four independent fp64
             // accumulators (fixed combination order: deterministic)
             double acc4[4] = {0.0, 0.0, 0.0, 0.0};
             double dg = 0.0;
 #pragma unroll
-            for (int g = 0; g < kN / 16; ++g) {
-                if (g < warp) continue;                          // left of the warp's first row
+            for (int g = 0; g < kCT / 16; ++g) {
+                if (kCT * hw + 16 * g + 15 < 16 * q) continue;         // left of the quadrant's first row
 #pragma unroll
-                for (int c = 16 * g; c < 16 * g + 16; ++c) {
-                    const double x = xr[c];
-                    if (c > row) acc4[c & 3] = fma(x, x, acc4[c & 3]);
+                for (int i = 0; i < 16; ++i) {
+                    const int cc = 16 * g + i, c = kCT * hw + cc;
+                    const double x = xr[cc];
+                    if (c > row) acc4[i & 3] = fma(x, x, acc4[i & 3]);
                     if (c == row) dg = x * x;
                 }
             }
             double ss = fma(2.0, (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]), dg);
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);   // within 16 lanes
-            if ((lane & 15) == 0) red[m * 4 + warp] = ss;
+            if ((lane & 15) == 0) red[m * kWarps + warp] = ss;
             ptx::tmem_st_wait();
             __syncthreads();
-            const double lsum = ((red[m * 4 + 0] + red[m * 4 + 1]) + red[m * 4 + 2]) + red[m * 4 + 3];
+            double lsum = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) lsum += red[m * kWarps + w];              // fixed order
             lam = sqrt(lsum);
             if (!isfinite(lam)) {
                 if (lane == 0 && warp == 0 && valid) atomicOr(status, 1u);
@@ -545,18 +575,18 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 atomicAdd(plan.dbg + 10, static_cast<unsigned long long>(clock64() - t_lam));   // X_0 + mirror
             }
         }
-
         if (kDebug && plan.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
             atomicAdd(plan.dbg + 5, static_cast<unsigned long long>(clock64() - t_pair));   // load, bound, X_0
             atomicAdd(plan.dbg + 7, 1ull);
         }
+
         // ---- the chain of products
 #pragma unroll 1
         for (int si = 0; si < plan.nsteps; ++si) {
             const SmallStep& st = plan.steps[si];
             if (st.reload_x0) {
                 // X_0 back into the Y slot for the reconstruction product (the Z slot holds S)
-                float xr[kN];
+                float xr[kCT];
                 x_from_tmem(xr);
                 store_x0(xr, inv, L::kY);
             }
@@ -597,22 +627,20 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             if (st.final_mode == 0) {
                 // chain product: (alpha acc + beta D) s, the operand scale s (a power of two,
                 // compute_scales) folded into alpha and beta exactly; in place (the MMA that read
-                // the slots has completed).  Only the upper 8x8 blocks are computed; each writes
-                // itself and its transpose (every product is exactly symmetric, R20).  Warp w owns
-                // the 9 unordered block pairs {P, Q} with P in its row blocks {2w, 2w+1}: the three
-                // inside them, and for every other warp b the two (2w, 2b), (2w, 2b+1) if b > w,
-                // else (2w, 2b+1), (2w+1, 2b+1) -- the same count for every warp (quadrant), and
-                // every pair exactly once.
+                // the slots has completed).  Warp (q, h) runs quadrant q's epilogue of matrix h: only
+                // the upper 8x8 blocks, each written with its transpose (every product exactly
+                // symmetric, R20); the quadrant's 9 block pairs are the same count for every SMSP.
                 const float2 alpha = make_float2(st.alpha * st.out_scale, st.alpha * st.out_scale);
                 const float2 beta = make_float2(st.beta * st.out_scale, st.beta * st.out_scale);
                 const bool has_d = st.slot_d >= 0;
                 const uint32_t pd = smem_base + static_cast<uint32_t>(has_d ? st.slot_d : 0);
                 const uint32_t po = smem_base + static_cast<uint32_t>(st.slot_out);
-                switch (warp) {
-                    case 0: chain_epilogue<kSplit, 0>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
-                    case 1: chain_epilogue<kSplit, 1>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
-                    case 2: chain_epilogue<kSplit, 2>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
-                    default: chain_epilogue<kSplit, 3>(tmem, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                const int mm = kQW == 2 ? hw : -1;       // 8 warps: one matrix per warp; 4 warps: both
+                switch (q) {
+                    case 0: chain_epilogue<kSplit, 0>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    case 1: chain_epilogue<kSplit, 1>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    case 2: chain_epilogue<kSplit, 2>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    default: chain_epilogue<kSplit, 3>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
                 }
                 const long long t_c = kDebug ? clock64() : 0;
                 ptx::tc_fence_before();
@@ -630,11 +658,12 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                 const long long t_f = kDebug ? clock64() : 0;
                 // final: P = lambda~ alpha acc + beta X  (mode 1, R5)  or
                 //        S = alpha acc + beta D          (mode 2; the sign output)
-                // computed on this row's upper part (row per thread, 32x32b loads), staged as fp32
-                // in the (consumed) operand region, and stored whole: the lower part is read back
-                // transposed (exact symmetry)
+                // computed on this row's upper part (row per thread, 32 columns, 32x32b loads), staged
+                // as fp32 in the (consumed) operand region, and stored whole: the lower part is read
+                // back transposed (exact symmetry)
                 float* stage = reinterpret_cast<float*>(mat);          // 64 x 64 fp32, float4-swizzled
                 float4* srow = reinterpret_cast<float4*>(stage + row * kN);
+                const bool live = kCT * hw + kCT - 1 >= 16 * q;       // columns at or right of the quadrant's rows
                 auto stage_at = [&](int r, int c) -> float {
                     return stage[r * kN + (((c >> 2) ^ (r & 15)) << 2) + (c & 3)];
                 };
@@ -645,8 +674,8 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     const int cl = lane & 15;
                     const int c4 = 4 * cl;
 #pragma unroll 4
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = 16 * warp + i;
+                    for (int i = 0; i < kRW; ++i) {
+                        const int r = 16 * q + kRW * hw + i;
                         if (r >= n) break;
                         float* orow = dst + static_cast<int64_t>(b) * n * n + static_cast<int64_t>(r) * n;
                         if (vec) {
@@ -672,23 +701,32 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                     const float lamf = static_cast<float>(lam);
 #pragma unroll 1
                     for (int pass = plan.out2 ? 1 : 0; pass >= 0; --pass) {
+                        if (live) {
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (32 * h + 31 < 16 * warp) continue;      // below the diagonal for the warp
-                            uint32_t r[32], xh[32];
-                            ptx::tmem_ld_32x32b_x32(tmem_row + 32 * h, r);
-                            ptx::tmem_ld_32x32b_x32(tmem_x + 32 * h, xh);
-                            ptx::tmem_ld_wait();
+                            for (int h = 0; h < kCT / 16; ++h) {
+                                uint32_t r[16], xh[16];
+                                asm volatile(
+                                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                                    : "r"(tmem_row + kCT * hw + 16 * h));
+                                asm volatile(
+                                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                    : "=r"(xh[0]), "=r"(xh[1]), "=r"(xh[2]), "=r"(xh[3]), "=r"(xh[4]), "=r"(xh[5]), "=r"(xh[6]), "=r"(xh[7]),
+                                      "=r"(xh[8]), "=r"(xh[9]), "=r"(xh[10]), "=r"(xh[11]), "=r"(xh[12]), "=r"(xh[13]), "=r"(xh[14]), "=r"(xh[15])
+                                    : "r"(tmem_x + 16 * h));
+                                ptx::tmem_ld_wait();
 #pragma unroll
-                            for (int qq = 0; qq < kN / 8; ++qq) {
-                                float o[4];
+                                for (int qq = 0; qq < 4; ++qq) {
+                                    float o[4];
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const float x = __uint_as_float(xh[4 * qq + e]);
-                                    const float p = lamf * (st.alpha * __uint_as_float(r[4 * qq + e])) + st.beta * x;
-                                    o[e] = pass == 1 ? plan.sigma2 * (p - x) : p;
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float x = __uint_as_float(xh[4 * qq + e]);
+                                        const float p = lamf * (st.alpha * __uint_as_float(r[4 * qq + e])) + st.beta * x;
+                                        o[e] = pass == 1 ? plan.sigma2 * (p - x) : p;
+                                    }
+                                    srow[((kCT / 4) * hw + 4 * h + qq) ^ (row & 15)] = make_float4(o[0], o[1], o[2], o[3]);
                                 }
-                                srow[((kN / 8) * h + qq) ^ (row & 15)] = make_float4(o[0], o[1], o[2], o[3]);
                             }
                         }
                         __syncthreads();
@@ -696,31 +734,35 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
                         __syncthreads();
                     }
                 } else {
-                    float v[kN];
+                    float v[kCT];
+                    if (live) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t r[32];
-                        ptx::tmem_ld_32x32b_x32(tmem_row + 32 * h, r);
-                        ptx::tmem_ld_wait();
+                        for (int h = 0; h < kCT / 32; ++h) {
+                            uint32_t r[32];
+                            ptx::tmem_ld_32x32b_x32(tmem_row + kCT * hw + 32 * h, r);
+                            ptx::tmem_ld_wait();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[32 * h + i] = st.alpha * __uint_as_float(r[i]);
-                    }
-                    if (st.slot_d >= 0) {
+                            for (int i = 0; i < 32; ++i) v[32 * h + i] = st.alpha * __uint_as_float(r[i]);
+                        }
+                        if (st.slot_d >= 0) {
 #pragma unroll
-                        for (int j = 0; j < kN / 8; ++j) {
-                            float2 d[4];
-                            load_operand8<kSplit>(mat + st.slot_d, rbase + ((j ^ rx) << 4), d);
+                            for (int jj = 0; jj < kCT / 8; ++jj) {
+                                float2 d[4];
+                                load_operand8<kSplit>(mat + st.slot_d, rbase + ((((kCT / 8) * hw + jj) ^ rx) << 4), d);
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                v[8 * j + 2 * q] += st.beta * d[q].x;
-                                v[8 * j + 2 * q + 1] += st.beta * d[q].y;
+                                for (int e = 0; e < 4; ++e) {
+                                    v[8 * jj + 2 * e] += st.beta * d[e].x;
+                                    v[8 * jj + 2 * e + 1] += st.beta * d[e].y;
+                                }
                             }
                         }
                     }
                     __syncthreads();             // every operand read is done: staging may overwrite
+                    if (live) {
 #pragma unroll
-                    for (int q = 0; q < kN / 4; ++q)
-                        srow[q ^ (row & 15)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        for (int qq = 0; qq < kCT / 4; ++qq)
+                            srow[((kCT / 4) * hw + qq) ^ (row & 15)] = make_float4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+                    }
                     __syncthreads();
                     store_staged(out);
                     __syncthreads();
@@ -755,7 +797,7 @@ cudaError_t launch_small_t(const float* X, float* out, int n, int batch, double*
     const int pairs = (batch + 1) / 2;
     int grid = kSmallCtasPerSm<kSplit> * num_sms;
     if (grid > pairs) grid = pairs;
-    small_batch_kernel<kSplit><<<grid, kThreadsS, L::kBytes, stream>>>(X, out, n, batch, lambda_out, status, plan);
+    small_batch_kernel<kSplit><<<grid, 32 * kWarpsS<kSplit>, L::kBytes, stream>>>(X, out, n, batch, lambda_out, status, plan);
     return cudaGetLastError();
 }
 
