@@ -64,6 +64,7 @@ struct Workspace {
 };
 
 constexpr int kMaxSteps = 1024;
+constexpr int kRowPanelChunks = 4;   // all-gathers per product on the NCCL row-panel path
 
 
 int op_bytes(OpType t) { return t == OpType::TF32 ? 4 : 2; }
@@ -87,9 +88,12 @@ struct psd_filter_s {
         OpType op = OpType::F16;
         float* xg = nullptr;            // gathered X, n x n fp32
         float* pfull = nullptr;         // unpacked final product, npad x npad fp32
-        void* packed_op = nullptr;      // [nranks * per][256 * 256] operand precision
-        float* packed_f32 = nullptr;    // [nranks * per][256 * 256] fp32 (final product)
-        uint32_t* codes = nullptr;      // [nranks][per] tile codes (gather order)
+        void* packed_op = nullptr;      // [chunks][nranks][ct][256 * 256] operand precision
+        float* packed_f32 = nullptr;    // [chunks][nranks][ct][256 * 256] fp32 (final product)
+        uint32_t* codes = nullptr;      // [nranks][per] tile codes (each rank's list, compute order)
+        uint32_t* codes_g = nullptr;    // [chunks][nranks][ct] tile codes in gathered-buffer order
+        int chunks = 1, ct = 0;         // gathers per product, tiles per rank per chunk
+        cudaStream_t cs = nullptr;      // communication stream (chunk c's all-gather under chunk c+1's MMAs)
         std::vector<int> counts;        // real tiles per rank
     } rp;
     // peer-memory row-panel path (multi-GPU without a collective on the data path): every rank
@@ -868,6 +872,8 @@ void free_rowpanel_ws(psd_filter_s::RowPanel& rp) {
     if (rp.packed_op) cudaFree(rp.packed_op);
     if (rp.packed_f32) cudaFree(rp.packed_f32);
     if (rp.codes) cudaFree(rp.codes);
+    if (rp.codes_g) cudaFree(rp.codes_g);
+    if (rp.cs) cudaStreamDestroy(rp.cs);
     rp = psd_filter_s::RowPanel();
 }
 
@@ -903,16 +909,35 @@ psd_status_t ensure_rowpanel(psd_filter_s* h, int n, int nranks) {
     std::vector<uint32_t> codes(static_cast<size_t>(nranks) * per);
     rp.counts.resize(nranks);
     for (int r = 0; r < nranks; ++r) rp.counts[r] = rowpanel_tiles(nt, nranks, r, codes.data() + r * per, per);
-    const size_t tiles = static_cast<size_t>(nranks) * per;
+    // each product's tiles are gathered in `chunks` all-gathers (SURVEY 8(e) "Overlap"): chunk c
+    // of every rank's list is computed, then gathered on the communication stream while chunk c+1
+    // is computed; the gathered buffer is [chunk][rank][ct] and codes_g maps it to tile codes
+    const int chunks = std::max(1, std::min(kRowPanelChunks, per));
+    const int ct = (per + chunks - 1) / chunks;
+    std::vector<uint32_t> codes_g(static_cast<size_t>(chunks) * nranks * ct, 0xFFFFFFFFu);
+    for (int c = 0; c < chunks; ++c)
+        for (int r = 0; r < nranks; ++r)
+            for (int i = 0; i < ct && c * ct + i < per; ++i)
+                codes_g[(static_cast<size_t>(c) * nranks + r) * ct + i] = codes[static_cast<size_t>(r) * per + c * ct + i];
+    const size_t tiles = codes_g.size();
     if (cudaMalloc(&rp.xg, static_cast<size_t>(n) * n * 4) != cudaSuccess ||
         cudaMalloc(&rp.pfull, static_cast<size_t>(npad) * npad * 4) != cudaSuccess ||
         cudaMalloc(&rp.packed_op, tiles * 65536 * op_bytes(op)) != cudaSuccess ||
         cudaMalloc(&rp.packed_f32, tiles * 65536 * 4) != cudaSuccess ||
-        cudaMalloc(&rp.codes, codes.size() * 4) != cudaSuccess) {
+        cudaMalloc(&rp.codes, codes.size() * 4) != cudaSuccess ||
+        cudaMalloc(&rp.codes_g, codes_g.size() * 4) != cudaSuccess) {
         free_rowpanel_ws(rp);
         return fail(PSD_ENOMEM, "cudaMalloc row-panel workspace failed");
     }
+    cudaError_t se = cudaStreamCreateWithFlags(&rp.cs, cudaStreamNonBlocking);
+    if (se != cudaSuccess) {
+        free_rowpanel_ws(rp);
+        return cuda_fail(se, "cudaStreamCreate");
+    }
     cudaMemcpy(rp.codes, codes.data(), codes.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(rp.codes_g, codes_g.data(), codes_g.size() * 4, cudaMemcpyHostToDevice);
+    rp.chunks = chunks;
+    rp.ct = ct;
     cudaMemset(rp.pfull, 0, static_cast<size_t>(npad) * npad * 4);
     rp.npad = npad;
     rp.n = n;
@@ -964,12 +989,15 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
     double sign_only = 0.0;
     std::vector<Step> steps = build_plan(h, want_sign, &sign_only);
     if (steps.empty()) return fail(PSD_EUNSUPPORTED, "row panels: filter without products");
-    if (steps.size() * nranks > static_cast<size_t>(kMaxSteps)) return fail(PSD_EUNSUPPORTED, "too many products");
-    e = cudaMemsetAsync(ws.counters, 0, steps.size() * nranks * sizeof(int), st);
+    const int C = rp.chunks, ct = rp.ct;
+    if (steps.size() * nranks * C > static_cast<size_t>(kMaxSteps)) return fail(PSD_EUNSUPPORTED, "too many products");
+    e = cudaMemsetAsync(ws.counters, 0, steps.size() * nranks * C * sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     const int ob = op_bytes(ws.op);
     const size_t tile_elems = 65536;
-    // (4) the products: each rank its upper tiles, packed; all-gather; unpack on every rank
+    std::vector<cudaEvent_t> used;
+    // (4) the products: each rank its upper tiles, packed, chunk by chunk; chunk c's all-gather runs
+    // on the communication stream while the compute stream does chunk c+1; unpack on every rank
     for (size_t si = 0; si < steps.size(); ++si) {
         const Step& s = steps[si];
         EpiParams ep{};
@@ -997,31 +1025,45 @@ psd_status_t run_rowpanel(psd_filter_s* h, const float* X, int64_t n64, int rank
         // mirror and the loader reads the left part of a panel transposed
         const bool upper_only = ws.op != OpType::TF32 && debug_env("PSD_NO_UPPER_ONLY") == nullptr;
         const int r0 = comm ? rank : 0, r1 = comm ? rank + 1 : nranks;
-        for (int vr = r0; vr < r1; ++vr) {
-            const size_t slot0 = static_cast<size_t>(vr) * rp.per * tile_elems;
-            ep.packed = s.outF ? static_cast<void*>(rp.packed_f32 + slot0)
-                               : static_cast<void*>(static_cast<uint8_t*>(rp.packed_op) + slot0 * ob);
-            GemmShape shape{npad, 1, rp.codes + static_cast<size_t>(vr) * rp.per, rp.counts[vr],
-                            ws.counters + si * nranks + vr};
-            shape.upper_only = upper_only ? 1 : 0;
-            if (rp.counts[vr] == 0) continue;
-            e = launch_sym_gemm_2cta(ws.op, false, m, shape, ep, st);
-            if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (row panel)");
-            h->kernel_launches += 1;
+        const size_t tbytes = tile_elems * (s.outF ? 4 : ob);             // one packed tile
+        uint8_t* gathered = s.outF ? reinterpret_cast<uint8_t*>(rp.packed_f32) : static_cast<uint8_t*>(rp.packed_op);
+        for (int c = 0; c < C; ++c) {
+            for (int vr = r0; vr < r1; ++vr) {
+                const int cnt = std::min(ct, rp.counts[vr] - c * ct);
+                if (cnt <= 0) continue;
+                ep.packed = gathered + (static_cast<size_t>(c) * nranks + vr) * ct * tbytes;
+                GemmShape shape{npad, 1, rp.codes + static_cast<size_t>(vr) * rp.per + c * ct, cnt,
+                                ws.counters + (si * C + c) * nranks + vr};
+                shape.upper_only = upper_only ? 1 : 0;
+                e = launch_sym_gemm_2cta(ws.op, false, m, shape, ep, st);
+                if (e != cudaSuccess) return cuda_fail(e, "sym_gemm_2cta (row panel)");
+                h->kernel_launches += 1;
+            }
+            if (comm) {
+                cudaEvent_t ready = take_event(h);
+                used.push_back(ready);
+                cudaEventRecord(ready, st);
+                cudaStreamWaitEvent(rp.cs, ready, 0);
+                uint8_t* slab = gathered + static_cast<size_t>(c) * nranks * ct * tbytes;
+                int r = nccl().all_gather(slab + static_cast<size_t>(rank) * ct * tbytes, slab, ct * tbytes, kNcclInt8,
+                                          comm, rp.cs);
+                if (r != 0) return nccl_fail(r, "ncclAllGather(tiles)");
+            }
         }
-        const size_t bytes_rank = static_cast<size_t>(rp.per) * tile_elems * (s.outF ? 4 : ob);
-        void* gathered = s.outF ? static_cast<void*>(rp.packed_f32) : rp.packed_op;
         if (comm) {
-            int r = nccl().all_gather(static_cast<uint8_t*>(gathered) + rank * bytes_rank, gathered, bytes_rank,
-                                      kNcclInt8, comm, st);
-            if (r != 0) return nccl_fail(r, "ncclAllGather(tiles)");
+            cudaEvent_t gathered_ev = take_event(h);
+            used.push_back(gathered_ev);
+            cudaEventRecord(gathered_ev, rp.cs);
+            cudaStreamWaitEvent(st, gathered_ev, 0);
         }
-        e = launch_unpack_tiles(s.outF ? 4 : ob, gathered, rp.codes, nranks * rp.per,
+        e = launch_unpack_tiles(s.outF ? 4 : ob, gathered, rp.codes_g, C * nranks * ct,
                                 s.outF ? static_cast<void*>(rp.pfull) : ws.op_buf[s.out_op], npad, st,
                                 s.outF || !upper_only);
         if (e != cudaSuccess) return cuda_fail(e, "unpack");
         h->kernel_launches += 1;
     }
+    // cudaStreamWaitEvent binds to the record made before it, so the events can be re-recorded
+    for (auto x : used) h->ev_pool.push_back(x);
     // (5) this rank's rows (all rows for the virtual ranks) of the result
     const int row0 = comm ? rank * rows : 0;
     const int nrows = comm ? rows : n;
