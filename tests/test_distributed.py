@@ -284,3 +284,25 @@ def test_bench_spawns_ranks_cpu():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["filter"] == "c3" and d["config"]["n"] == 1024
     assert d["cpu_baseline"]["cpu_model"] and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,batch,world,prec", [
+    (1024, 16, 2, "fp16"),     # CTA-pair kernel for the whole batch and for every shard
+    (1024, 24, 3, "fp16x3"),   # split path, K-chunked accumulation
+    (512, 6, 4, "fp16"),       # 1-CTA kernel, ragged shards (2, 2, 1, 1)
+    (64, 9, 2, "fp16"),        # batched small-n kernel, odd shards
+])
+def test_batch_shards_bitwise_equal_to_single_gpu(n, batch, world, prec):
+    """the c4 partition (contiguous shards of the batch, one per rank, no collective)
+    gives every matrix bitwise the result of the single-GPU run of the whole batch."""
+    import torch
+    from paper_2507_09165_b200 import Filter, filters, dist as pdist
+    X = torch.tensor(synth.batch("goe", n, batch, 77 + n), dtype=torch.float32, device="cuda")
+    stages = filters.single_filter() if prec.endswith("x3") else filters.half_filter()
+    f = Filter(stages, precision=prec)
+    full = f.project(X).cpu()
+    for rank in range(world):
+        first, count = pdist.shard_range(batch, world, rank)
+        part = Filter(stages, precision=prec).project(X[first:first + count].contiguous()).cpu()
+        assert torch.equal(part, full[first:first + count]), (rank, first, count)
