@@ -48,6 +48,7 @@ def _m32(C, K, y, sigma):
 
 @pytest.mark.parametrize("n,batch,prec,sigma", [
     (64, 5, "fp16x3", 1.0),       # batched small-n kernel
+    (37, 3, "fp16", 1.3),         # small-n kernel: rows not a multiple of 4 (scalar loads), odd batch
     (200, 2, "fp16", 2.0),        # ragged n, 1-CTA product kernel
     (512, 3, "fp16x3", 0.5),
     (1024, 8, "fp16", 1.0),       # CTA-pair kernel
@@ -72,7 +73,7 @@ def test_admm_update_parity(pkg, n, batch, prec, sigma):
         assert np.array_equal(S[b], S[b].T) and np.array_equal(X[b], X[b].T)
 
 
-@pytest.mark.parametrize("n,prec", [(64, "fp16"), (384, "fp16"), (1024, "fp16")])
+@pytest.mark.parametrize("n,prec", [(64, "fp16"), (37, "fp16x3"), (384, "fp16"), (1024, "fp16")])
 def test_admm_update_equals_projection_of_formed_argument(pkg, n, prec):
     """S is bitwise psd_project(M) of the fp32-formed M, and X_next is bitwise fl(sigma) (S - M):
     the fused formation in the bound, scale and epilogue stages changes nothing else; in place
