@@ -22,6 +22,10 @@
 // in the first version, profiles/r2_c2_small_v2.md).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <type_traits>
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -282,34 +286,24 @@ __device__ __forceinline__ void region_load(uint32_t tb, uint32_t (&a)[8]) {
     if constexpr (Rg::kRight) tmem_ld_16x256b_x2(tb + 16 * Rg::bq, a);
     else tmem_ld_16x256b_x1(tb + 16 * Rg::bq + 8, *reinterpret_cast<uint32_t(*)[4]>(a));
 }
-template <bool kSplit, int W, int K>
-__device__ __forceinline__ void region_store(const uint32_t (&a)[8], uint32_t pd, uint32_t po, bool has_d,
-                                             float2 alpha, float2 beta, uint32_t lrow128, uint32_t lrow, uint32_t lq1) {
+// normal and transposed block-row offsets (within a part) of this lane for region K of warp W
+template <int W, int K>
+__device__ __forceinline__ void region_offsets(uint32_t lrow128, uint32_t lrow, uint32_t lq1, uint32_t& on, uint32_t& ot) {
     using Rg = Region<W, K>;
     constexpr int R0 = 2 * W, bq = Rg::bq;
-    uint32_t on, ot, a0, a1, a2, a3;
     if constexpr (Rg::kRight) {
         on = (8 * R0) * 128 + lrow128 + (((2 * bq + lq1) ^ lrow) << 4);
         ot = (8 * 2 * bq) * 128 + lq1 * 1024 + lrow128 + ((R0 ^ lrow) << 4);
-        a0 = a[0]; a1 = a[1]; a2 = a[4]; a3 = a[5];
     } else {
         on = (8 * R0) * 128 + lq1 * 1024 + lrow128 + (((2 * bq + 1) ^ lrow) << 4);
         ot = (8 * (2 * bq + 1)) * 128 + lrow128 + (((R0 + lq1) ^ lrow) << 4);
-        a0 = a[0]; a1 = a[1]; a2 = a[2]; a3 = a[3];
     }
-    uint32_t dh[2] = {0, 0}, dl[2] = {0, 0};
-    if (has_d) {
-        ldsm_x2(pd + on, dh);
-        if constexpr (kSplit) ldsm_x2(pd + kSlotBytes + on, dl);
-    }
-    const Frag<kSplit> g0 = combine<kSplit>(a0, a1, has_d, dh[0], dl[0], alpha, beta);
-    const Frag<kSplit> g1 = combine<kSplit>(a2, a3, has_d, dh[1], dl[1], alpha, beta);
-    stsm_x2(po + on, g0.hi, g1.hi);
-    stsm_x2_trans(po + ot, g0.hi, g1.hi);
-    if constexpr (kSplit) {
-        stsm_x2(po + kSlotBytes + on, g0.lo, g1.lo);
-        stsm_x2_trans(po + kSlotBytes + ot, g0.lo, g1.lo);
-    }
+}
+// the accumulator registers of region K's two blocks
+template <int W, int K>
+__device__ __forceinline__ void region_acc(const uint32_t (&a)[8], uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    if constexpr (Region<W, K>::kRight) { a0 = a[0]; a1 = a[1]; a2 = a[4]; a3 = a[5]; }
+    else { a0 = a[0]; a1 = a[1]; a2 = a[2]; a3 = a[3]; }
 }
 // accumulator fragments of matrix mm for warp W's blocks (caller waits)
 template <int W>
@@ -324,24 +318,36 @@ __device__ __forceinline__ void epi_load(uint32_t tmem, int mm, EpiFrags<W>& f) 
     region_load<W, 1>(tb, f.a1);
     region_load<W, 2>(tb, f.a2);
 }
+// the addend's fragments at every block a warp writes (hi [, lo]): all shared-memory reads of the
+// epilogue are issued before its first store (the ldmatrix / stmatrix asm is ordered, so a read
+// after a store would wait for the store)
+struct EpiD {
+    uint32_t wh[4], wl[4], rh[3][2], rl[3][2];
+};
 template <bool kSplit, int W>
-__device__ __forceinline__ void epi_store(const EpiFrags<W>& f, int mm, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
-                                          bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
-    constexpr int R0 = 2 * W;
-    const uint32_t lrow = lane & 7, lq = lane >> 3, lq1 = lq & 1;
-    const uint32_t lrow128 = lrow * 128;
-    // blocks inside the warp's rows, lane group q: [(R0,R0), (R1,R0), (R0,R1), (R1,R1)]
-    const uint32_t offW = (8 * R0) * 128 + (lq & 1) * 1024 + lrow128 + (((R0 + (lq >> 1)) ^ lrow) << 4);
-    const uint32_t pd = pd0 + mm * mat_bytes, po = po0 + mm * mat_bytes;
+__device__ __forceinline__ void epi_load_d(uint32_t pd, bool has_d, uint32_t offW, const uint32_t (&on)[3], EpiD& d) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d.wh[i] = d.wl[i] = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d.rh[k][0] = d.rh[k][1] = d.rl[k][0] = d.rl[k][1] = 0;
+    if (!has_d) return;
+    ldsm_x4(pd + offW, d.wh);
+    if constexpr (kSplit) ldsm_x4(pd + kSlotBytes + offW, d.wl);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        ldsm_x2(pd + on[k], d.rh[k]);
+        if constexpr (kSplit) ldsm_x2(pd + kSlotBytes + on[k], d.rl[k]);
+    }
+}
+template <bool kSplit, int W>
+__device__ __forceinline__ void epi_store(const EpiFrags<W>& f, const EpiD& d, uint32_t po, uint32_t offW,
+                                          const uint32_t (&on)[3], const uint32_t (&ot)[3], bool has_d, float2 alpha,
+                                          float2 beta, uint32_t diag_mask) {
     {
-        uint32_t dh[4] = {0, 0, 0, 0}, dl[4] = {0, 0, 0, 0};
-        if (has_d) {
-            ldsm_x4(pd + offW, dh);
-            if constexpr (kSplit) ldsm_x4(pd + kSlotBytes + offW, dl);
-        }
-        const Frag<kSplit> f0 = combine<kSplit>(f.aW[0], f.aW[1], has_d, dh[0], dl[0], alpha, beta);
-        const Frag<kSplit> f2 = combine<kSplit>(f.aW[4], f.aW[5], has_d, dh[2], dl[2], alpha, beta);
-        const Frag<kSplit> f3 = combine<kSplit>(f.aW[6], f.aW[7], has_d, dh[3], dl[3], alpha, beta);
+        // blocks inside the warp's rows, lane group q: [(R0,R0), (R1,R0), (R0,R1), (R1,R1)]
+        const Frag<kSplit> f0 = combine<kSplit>(f.aW[0], f.aW[1], has_d, d.wh[0], d.wl[0], alpha, beta);
+        const Frag<kSplit> f2 = combine<kSplit>(f.aW[4], f.aW[5], has_d, d.wh[2], d.wl[2], alpha, beta);
+        const Frag<kSplit> f3 = combine<kSplit>(f.aW[6], f.aW[7], has_d, d.wh[3], d.wl[3], alpha, beta);
         const uint32_t h[4] = {diag_upper(f0.hi, diag_mask), movmatrix_trans(f2.hi), f2.hi, diag_upper(f3.hi, diag_mask)};
         stsm_x4(po + offW, h);
         if constexpr (kSplit) {
@@ -349,27 +355,53 @@ __device__ __forceinline__ void epi_store(const EpiFrags<W>& f, int mm, uint32_t
             stsm_x4(po + kSlotBytes + offW, l);
         }
     }
-    region_store<kSplit, W, 0>(f.a0, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
-    region_store<kSplit, W, 1>(f.a1, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
-    region_store<kSplit, W, 2>(f.a2, pd, po, has_d, alpha, beta, lrow128, lrow, lq1);
+    auto region = [&](const uint32_t (&a)[8], auto kc) {
+        constexpr int K = decltype(kc)::value;
+        uint32_t a0, a1, a2, a3;
+        region_acc<W, K>(a, a0, a1, a2, a3);
+        const Frag<kSplit> g0 = combine<kSplit>(a0, a1, has_d, d.rh[K][0], d.rl[K][0], alpha, beta);
+        const Frag<kSplit> g1 = combine<kSplit>(a2, a3, has_d, d.rh[K][1], d.rl[K][1], alpha, beta);
+        stsm_x2(po + on[K], g0.hi, g1.hi);
+        stsm_x2_trans(po + ot[K], g0.hi, g1.hi);
+        if constexpr (kSplit) {
+            stsm_x2(po + kSlotBytes + on[K], g0.lo, g1.lo);
+            stsm_x2_trans(po + kSlotBytes + ot[K], g0.lo, g1.lo);
+        }
+    };
+    region(f.a0, std::integral_constant<int, 0>{});
+    region(f.a1, std::integral_constant<int, 1>{});
+    region(f.a2, std::integral_constant<int, 2>{});
 }
-// the chain-product epilogue of warp W: matrix `mm` (mm < 0: both matrices, their fragments loaded
-// before one wait)
+// the chain-product epilogue of warp W: matrix `mm` (mm < 0: both matrices, their fragments and
+// addends loaded before the first store)
 template <bool kSplit, int W>
 __device__ __forceinline__ void chain_epilogue(uint32_t tmem, int mm, uint32_t pd0, uint32_t po0, uint32_t mat_bytes,
                                                bool has_d, float2 alpha, float2 beta, int lane, uint32_t diag_mask) {
+    constexpr int R0 = 2 * W;
+    const uint32_t lrow = lane & 7, lq = lane >> 3, lq1 = lq & 1;
+    const uint32_t lrow128 = lrow * 128;
+    const uint32_t offW = (8 * R0) * 128 + (lq & 1) * 1024 + lrow128 + (((R0 + (lq >> 1)) ^ lrow) << 4);
+    uint32_t on[3], ot[3];
+    region_offsets<W, 0>(lrow128, lrow, lq1, on[0], ot[0]);
+    region_offsets<W, 1>(lrow128, lrow, lq1, on[1], ot[1]);
+    region_offsets<W, 2>(lrow128, lrow, lq1, on[2], ot[2]);
     if (mm >= 0) {
         EpiFrags<W> f;
+        EpiD d;
         epi_load<W>(tmem, mm, f);
+        epi_load_d<kSplit, W>(pd0 + mm * mat_bytes, has_d, offW, on, d);
         ptx::tmem_ld_wait();
-        epi_store<kSplit, W>(f, mm, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
+        epi_store<kSplit, W>(f, d, po0 + mm * mat_bytes, offW, on, ot, has_d, alpha, beta, diag_mask);
     } else {
         EpiFrags<W> f0, f1;
+        EpiD d0, d1;
         epi_load<W>(tmem, 0, f0);
         epi_load<W>(tmem, 1, f1);
+        epi_load_d<kSplit, W>(pd0, has_d, offW, on, d0);
+        epi_load_d<kSplit, W>(pd0 + mat_bytes, has_d, offW, on, d1);
         ptx::tmem_ld_wait();
-        epi_store<kSplit, W>(f0, 0, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
-        epi_store<kSplit, W>(f1, 1, pd0, po0, mat_bytes, has_d, alpha, beta, lane, diag_mask);
+        epi_store<kSplit, W>(f0, d0, po0, offW, on, ot, has_d, alpha, beta, diag_mask);
+        epi_store<kSplit, W>(f1, d1, po0 + mat_bytes, offW, on, ot, has_d, alpha, beta, diag_mask);
     }
 }
 
@@ -795,7 +827,9 @@ cudaError_t launch_small_t(const float* X, float* out, int n, int batch, double*
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int pairs = (batch + 1) / 2;
-    int grid = kSmallCtasPerSm<kSplit> * num_sms;
+    int per_sm = kSmallCtasPerSm<kSplit>;
+    if (const char* v = debug_env("PSD_SMALL_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(v)));   // A/B only
+    int grid = per_sm * num_sms;
     if (grid > pairs) grid = pairs;
     small_batch_kernel<kSplit><<<grid, 32 * kWarpsS<kSplit>, L::kBytes, stream>>>(X, out, n, batch, lambda_out, status, plan);
     return cudaGetLastError();
