@@ -17,10 +17,41 @@ Readings (DESIGN.md):
   R10 only the upper triangle of X is read (X_ij := X_min(i,j),max(i,j));
   R14 the returned matrix is symmetrised 1/2 (P + P^T).
 
-Every matrix power here is a plain numpy float64 matmul; f_t(Z) is evaluated as
-the monomial sum of its definition, not by Horner, not fused.
+Every matrix power here is a plain float64 matrix product (``matmul``: numpy's BLAS product by
+default for speed; ``naive_matmul`` is the textbook i-k-j triple loop, and the pins check that the
+two agree on small inputs); f_t(Z) is evaluated as the monomial sum of its definition, not by
+Horner, not fused.
 """
 import numpy as np
+
+
+def naive_matmul(A, B):
+    """C = A B by the textbook i-k-j triple loop, float64 (the north star's "naive matmuls")."""
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    n, k = A.shape
+    k2, m = B.shape
+    assert k == k2
+    C = [[0.0] * m for _ in range(n)]
+    Bl = B.tolist()
+    for i in range(n):
+        Ci = C[i]
+        Ai = A[i].tolist()
+        for kk in range(k):
+            a = Ai[kk]
+            if a == 0.0:
+                continue
+            Bk = Bl[kk]
+            for j in range(m):
+                Ci[j] += a * Bk[j]
+    return np.array(C, dtype=np.float64)
+
+
+def blas_matmul(A, B):
+    return np.asarray(A, dtype=np.float64) @ np.asarray(B, dtype=np.float64)
+
+
+matmul = blas_matmul        # module-level hook: tests swap in naive_matmul
 
 
 def symmetric_from_upper(X):
@@ -42,10 +73,10 @@ def odd_poly_matrix(Z, coeffs):
     out = coeffs[0] * Z
     if len(coeffs) == 1:
         return out
-    Z2 = Z @ Z
+    Z2 = matmul(Z, Z)
     power = Z                        # Z^{2j+1}, starting at j = 0
     for j in range(1, len(coeffs)):
-        power = power @ Z2           # Z^{2j+1} = Z^{2j-1} Z^2
+        power = matmul(power, Z2)    # Z^{2j+1} = Z^{2j-1} Z^2
         out = out + coeffs[j] * power
     return out
 
@@ -79,7 +110,7 @@ def project(X, stages, kappas=None, lam=None):
         return np.zeros_like(Xs), 0.0
     X0 = Xs / lam
     S = sign_chain(X0, stages, kappas)
-    P = lam * 0.5 * (X0 @ (np.eye(n) + S))
+    P = lam * 0.5 * matmul(X0, np.eye(n) + S)
     return 0.5 * (P + P.T), lam                              # R14
 
 

@@ -337,3 +337,25 @@ def test_idempotence_bound(family, which):
     # and the method really is (nearly) idempotent at the paper's filter accuracy
     if which != "c1":
         assert np.linalg.norm(D) <= 1e-3 * np.linalg.norm(P)
+
+
+def test_naive_matmul_oracle_agrees_with_blas():
+    """The oracle's matrix products are plain float64 matmuls; with the textbook i-k-j triple loop
+    swapped in (the north star's "naive matmuls") Algorithm 2 gives the same P on the c1 input and on
+    a 24 x 24 GOE matrix with the half filter, to summation-order rounding."""
+    from oracle import chain as ch
+    X1 = synth.goe(8, synth.SEED_BASE + 1)
+    X2 = synth.goe(24, 5)
+    cases = [(X1, tables.F_HALF[:3], None), (X2, tables.F_HALF_REFINED, tables.half_kappas(7))]
+    ref = [ch.project(X, st, kap)[0] for X, st, kap in cases]
+    saved = ch.matmul
+    try:
+        ch.matmul = ch.naive_matmul
+        got = [ch.project(X, st, kap)[0] for X, st, kap in cases]
+    finally:
+        ch.matmul = saved
+    for r, g in zip(ref, got):
+        assert np.max(np.abs(r - g)) <= 1e-13 * np.max(np.abs(r))
+    A = np.arange(6.0).reshape(2, 3)
+    B = np.arange(12.0).reshape(3, 4) - 5.0
+    assert np.array_equal(ch.naive_matmul(A, B), A @ B)     # exact on small integers
