@@ -85,7 +85,6 @@ template <OpType T, bool kSplit, int KS, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const EpiParams e) {
     using Tr = OpTraits<T>;
-    static_assert(KS == 1 || BN == kTile, "cluster split-K uses 128-wide tiles");
     constexpr int kStages = Ring1<kSplit, BN>::kStages;
     constexpr int kStageBytes = Ring1<kSplit, BN>::kStageBytes;
     constexpr int kBBytes = Ring1<kSplit, BN>::kBBytes;
@@ -261,7 +260,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         // park this CTA's partial accumulator (all MMAs done -> the ring is free)
         const int r = warp * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kTile; c0 += 32) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
             uint32_t raw[32];
             ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
             ptx::tmem_ld_wait();
@@ -273,16 +272,17 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         ptx::cluster_sync();
         // CTA k reduces row groups [k * 4/KS, (k+1) * 4/KS) x 4 column chunks; warp w takes chunks w, w+4, ..
         constexpr int kGroups = 4 / KS;
+        constexpr int kCC = BN / 32;                 // 32-column chunks of the tile
         const uint32_t ring_u = ptx::smem_u32(ring);
         uint32_t peer[KS];
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) peer[kk] = ptx::mapa_shared(ring_u, static_cast<uint32_t>(kk));
 #pragma unroll 1
-        for (int ch = warp; ch < kGroups * 4; ch += 4) {
-            const int rg = krank * kGroups + ch / 4;
-            const int cc = ch % 4;
+        for (int ch = warp; ch < kGroups * kCC; ch += 4) {
+            const int rg = krank * kGroups + ch / kCC;
+            const int cc = ch % kCC;
             const int gi0 = I * kTile + rg * 32;
-            const int gj0 = J * kTile + cc * 32;
+            const int gj0 = J * BN + cc * 32;
             if (diag && gj0 + 31 < gi0) continue;
             const int row = rg * 32 + lane;
             float acc[32];
@@ -356,7 +356,7 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
 template <OpType T, bool kSplit>
 cudaError_t launch_ks(int ks, int bn, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
                       cudaStream_t stream) {
-    if (bn == 64) return launch_t<T, kSplit, 1, 64>(m, s, e, stream);
+    if (bn == 64) return ks == 2 ? launch_t<T, kSplit, 2, 64>(m, s, e, stream) : launch_t<T, kSplit, 1, 64>(m, s, e, stream);
     switch (ks) {
         case 4: return launch_t<T, kSplit, 4, kTile>(m, s, e, stream);
         case 2: return launch_t<T, kSplit, 2, kTile>(m, s, e, stream);
