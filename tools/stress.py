@@ -44,7 +44,10 @@ for c in range(cases):
         for b in b_check:
             M = admm.form_argument(C[b], K[b], y[b], 1.5)
             Sr, _, _ = admm.s_update(C[b], K[b], y[b], 1.5, *st_o, lam=chain.frobenius_bound(M))
-            errs.append(np.linalg.norm(S[b] - Sr) / np.linalg.norm(Sr))
+            # R12: relative to ||reference||, floored at 1% of ||M|| (a nearly negative-definite input
+            # has Pi(M) ~ 0 and its filter output is the method's residual: a relative error
+            # against ~0 measures nothing)
+            errs.append(np.linalg.norm(S[b] - Sr) / max(np.linalg.norm(Sr), 1e-2 * np.linalg.norm(M)))
     else:
         X = synth.batch(fam, n, batch, 1000 * c)
         Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
@@ -55,7 +58,8 @@ for c in range(cases):
         errs = []
         for b in b_check:
             ref, _ = (chain.sign if mode == "sign" else chain.project)(X[b], *st_o, lam=float(lam[b]))
-            errs.append(np.linalg.norm(P[b] - ref) / np.linalg.norm(ref))
+            # R12 floor, as above (projection of a nearly negative-definite X: ||Pi(X)|| ~ 0)
+            errs.append(np.linalg.norm(P[b] - ref) / max(np.linalg.norm(ref), 1e-2 * np.linalg.norm(X[b])))
             assert np.array_equal(P[b], P[b].T)
     e = max(errs)
     # n < 64: the test suite's small-n bar (4x, TOL_SMALL_N: the fp16 rounding model of this
