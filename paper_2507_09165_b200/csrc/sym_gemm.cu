@@ -12,7 +12,8 @@
 // A cluster of KS CTAs (KS = 1, 2, 4; cluster split-K) owns one 128x128 upper tile:
 //   warp 0 / elected lane : TMA producer over this CTA's K slice -> kStages smem ring
 //   warp 1 / elected lane : tcgen05.mma.cta_group::1 (M = N = 128) into TMEM
-//   KS = 1 : warps 0-3 run the epilogue straight from TMEM (tcgen05.ld 32x32b)
+//   KS = 1 : warps 0-7 run the epilogue straight from TMEM (tcgen05.ld 32x32b): warps w and w + 4
+//            share TMEM lane quadrant w % 4 and take alternate 32-column chunks
 //   KS > 1 : every CTA parks its partial accumulator in its own (now idle) ring smem; after a
 //            cluster barrier CTA k sums rows [k*128/KS, (k+1)*128/KS) over the KS partials with
 //            ld.shared::cluster (DSMEM) and runs the epilogue for those rows -- KS x more SMs
@@ -35,7 +36,8 @@ namespace psd {
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kWarps = 8;                       // producer, MMA issuer; all 8 run the epilogue
+constexpr int kThreads = 32 * kWarps;
 constexpr int kTileBytes = kTile * kBlockKBytes;                 // 16 KB per operand tile
 constexpr int kRingBytes1 = 128 * 1024;
 template <bool kSplit, int BN> struct Ring1 {
@@ -43,7 +45,7 @@ template <bool kSplit, int BN> struct Ring1 {
     static constexpr int kStageBytes = (kSplit ? 2 : 1) * (kTileBytes + kBBytes);   // A, B (+ A_lo, B_lo)
     static constexpr int kStages = kRingBytes1 / kStageBytes;
 };
-constexpr int kSmemBytes = kRingBytes1 + 1024 + 256 + 4 * kEpiWarpSmemBytes;  // ring, align, barriers, staging
+constexpr int kSmemBytes = kRingBytes1 + 1024 + 256 + kWarps * kEpiWarpSmemBytes;  // ring, align, barriers, staging
 
 // Row-major enumeration of the 128 x BN tiles (row block I, column block J) that hold any
 // upper-triangle element: J >= I * (128 / BN).
@@ -103,7 +105,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     uint64_t* empty = full + kStages;
     uint64_t* accum_full = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
-    uint8_t* epi_smem = smem + kRingBytes1 + 256;                   // 4 x kEpiWarpSmemBytes
+    uint8_t* epi_smem = smem + kRingBytes1 + 256;                   // kWarps x kEpiWarpSmemBytes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -234,13 +236,14 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     uint8_t* wsmem = epi_smem + warp * kEpiWarpSmemBytes;
 
     if constexpr (KS == 1) {
-        const int gi0 = I * kTile + warp * 32;      // this warp's first row (TMEM lanes 32w..)
+        const int quad = warp & 3;                  // TMEM lanes 32 quad .. (a warp reaches only its quadrant)
+        const int gi0 = I * kTile + quad * 32;      // this warp's first row
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = (warp >> 2) * 32; c0 < BN; c0 += 64) {
             const int gj0 = J * BN + c0;
             if (diag && gj0 + 31 < gi0) continue;   // chunk below the diagonal for the whole warp
             uint32_t raw[32];
-            const uint32_t tl = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0;
+            const uint32_t tl = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c0;
             ptx::tmem_ld_32x32b_x32(tl, raw);
             ptx::tmem_ld_wait();
             if constexpr (kRuns) {
@@ -258,11 +261,11 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         }
     } else {
         // park this CTA's partial accumulator (all MMAs done -> the ring is free)
-        const int r = warp * 32 + lane;
+        const int r = (warp & 3) * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = (warp >> 2) * 32; c0 < BN; c0 += 64) {
             uint32_t raw[32];
-            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c0, raw);
+            ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + c0, raw);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -270,7 +273,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                     make_uint4(raw[4 * q], raw[4 * q + 1], raw[4 * q + 2], raw[4 * q + 3]);
         }
         ptx::cluster_sync();
-        // CTA k reduces row groups [k * 4/KS, (k+1) * 4/KS) x 4 column chunks; warp w takes chunks w, w+4, ..
+        // CTA k reduces row groups [k * 4/KS, (k+1) * 4/KS) x BN/32 column chunks; warp w takes chunks w, w+8, ..
         constexpr int kGroups = 4 / KS;
         constexpr int kCC = BN / 32;                 // 32-column chunks of the tile
         const uint32_t ring_u = ptx::smem_u32(ring);
@@ -278,7 +281,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) peer[kk] = ptx::mapa_shared(ring_u, static_cast<uint32_t>(kk));
 #pragma unroll 1
-        for (int ch = warp; ch < kGroups * kCC; ch += 4) {
+        for (int ch = warp; ch < kGroups * kCC; ch += kWarps) {
             const int rg = krank * kGroups + ch / kCC;
             const int cc = ch % kCC;
             const int gi0 = I * kTile + rg * 32;
