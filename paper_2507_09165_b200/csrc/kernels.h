@@ -107,7 +107,7 @@ void make_tile_order(int nt, const char* order, uint32_t* out);
 bool make_operand_tmap(CUtensorMap* map, const void* base, OpType t, int npad, int batch, int box_rows = kTile);
 // 1-CTA product kernel tile width for (npad, batch): 128, or 64 for few-tile problems; its split-K.
 int sym_gemm_bn(int npad, int batch);
-int sym_gemm_split_k(int npad, int batch, OpType t);
+int sym_gemm_split_k(int npad, int batch, OpType t, bool split, int kchunk);
 
 // Operand tensor maps of one product: A, B (high parts) and, for split precision, their
 // low parts (A*B ~= Ahi Bhi + Ahi Blo + Alo Bhi, three tcgen05.mma passes, one accumulator).

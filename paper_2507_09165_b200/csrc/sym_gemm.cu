@@ -5,7 +5,7 @@
 // symmetric matrices (powers/polynomials of the same X), so C is symmetric: only
 // upper tiles (I <= J) are computed.  A and B are symmetric, so both operands are read as row
 // panels: K-major from the stored tiles, or -- with upper-only storage (GemmShape::upper_only,
-// 16-bit, KS = 1), where each tile is stored once and only the 128x128 diagonal blocks whole --
+// 16-bit operands), where each tile is stored once and only the 128x128 diagonal blocks whole --
 // transposed (MN-major, 64 x 64 TMA boxes) left of the row block's diagonal block.  Tiles
 // (128 x 128, or 128 x 64 for few-tile problems) meeting the diagonal are stored mirrored.
 //
@@ -161,7 +161,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 // panel is the stored upper block transposed -- 64 x 64 boxes read as an MN-major operand
                 auto load = [&](uint8_t* dst, const CUtensorMap* mk, const CUtensorMap* mt, int rows, int row0,
                                 int diag0, int row) {
-                    if (Tr::kBytes == 2 && KS == 1 && s.upper_only && kx < diag0) {
+                    if (Tr::kBytes == 2 && s.upper_only && kx < diag0) {
                         for (int c = 0; c < rows; c += 64)
                             ptx::tma_load_2d(dst + c * kBlockKBytes, mt, &full[st], row0 + c, b * s.npad + kx, pol);
                     } else {
@@ -187,7 +187,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 ptx::tc_fence_after();
                 const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
                 const int kx = (kb0 + kb) * kBK;
-                const bool up = Tr::kBytes == 2 && KS == 1 && s.upper_only;
+                const bool up = Tr::kBytes == 2 && s.upper_only;
                 const bool a_mn = up && kx < I * kTile;
                 const bool b_mn = up && kx < (J * BN / kTile) * kTile;
                 // MN-major (transposed) operands: 64-element MN chunks 8 KB apart, 8-row K groups 1 KB
@@ -369,19 +369,22 @@ cudaError_t launch_ks(int ks, int bn, const OperandMaps& m, const GemmShape& s, 
 
 }  // namespace
 
-// Split-K factor for a few-tile problem: fill the SMs (one wave), keep >= 4 k-blocks per CTA.
-int sym_gemm_split_k(int npad, int batch, OpType t) {
-    // measured (tools/latency_probe.py, n = 1024, 19 products): KS = 1 211 us, 2 229 us, 4 386 us --
-    // the cluster barriers / DSMEM reduction cost more than the extra SMs gain once the epilogue
-    // is vectorised, so split-K is off unless forced (PSD_SPLITK = 2 | 4)
-    static const int forced = debug_env("PSD_SPLITK") ? std::atoi(debug_env("PSD_SPLITK")) : 1;
+// Split-K factor for a few-tile problem.  Measured (n = 1024, 19 products, 8-warp epilogue,
+// profiles/r2_epi8/): single-pass fp16 KS = 1 154 us, KS = 2 175 us -- the cluster barriers and the
+// DSMEM reduction cost more than the extra SMs gain; the 3-pass split precisions (3 MMAs per K step,
+// a mainloop-bound chain) KS = 1 274 us, KS = 2 238 us.  KS = 2 is therefore taken for the split
+// precisions when it fills at most one wave AND the K range is exactly two accumulation chunks
+// (npad == 2 kchunk): each CTA of the pair then accumulates one chunk from zero and the reduction
+// adds the two in order -- the same arithmetic as the single-CTA K-run summation (bit-identical).
+int sym_gemm_split_k(int npad, int batch, OpType t, bool split, int kchunk) {
+    static const int forced = debug_env("PSD_SPLITK") ? std::atoi(debug_env("PSD_SPLITK")) : 0;
     if (forced == 1 || forced == 2 || forced == 4) return forced;
-    const int nt = npad / kTile;
-    const int tiles = nt * (nt + 1) / 2 * batch;
-    const int kblocks = npad / (kBlockKBytes / (t == OpType::TF32 ? 4 : 2));
-    int ks = 1;
-    while (ks < 4 && tiles * ks * 2 <= 148 && kblocks % (ks * 2) == 0 && kblocks / (ks * 2) >= 4) ks *= 2;
-    return ks;
+    (void)t;
+    if (!split || kchunk <= 0 || npad != 2 * kchunk) return 1;
+    const int bn = sym_gemm_bn(npad, batch);
+    const int nrb = npad / kTile, ncb = npad / bn;
+    const int tiles = (nrb * ncb - (kTile / bn) * nrb * (nrb - 1) / 2) * batch;
+    return tiles * 2 <= 148 ? 2 : 1;
 }
 
 // 128 x 64 tiles for few-tile problems: twice the CTAs, half the MMA and epilogue per CTA.
@@ -394,7 +397,7 @@ int sym_gemm_bn(int npad, int batch) {
 
 cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
                             cudaStream_t stream) {
-    const int ks = sym_gemm_split_k(s.npad, s.batch, t);
+    const int ks = sym_gemm_split_k(s.npad, s.batch, t, split, s.kchunk);
     const int bn = sym_gemm_bn(s.npad, s.batch);
     switch (t) {
         case OpType::F16: return split ? launch_ks<OpType::F16, true>(ks, bn, m, s, e, stream)

@@ -153,6 +153,25 @@ def test_batch_position_determinism_and_inplace(pkg, n, prec, which):
     assert np.array_equal(Pi, P)
 
 
+@pytest.mark.parametrize("prec", ["fp16x3", "tf32x3"])
+def test_split_k_cluster_matches_single_cta_runs(pkg, prec):
+    """n = 1024 on the 1-CTA kernel: batch 1 runs the split precisions as a CTA pair per 128 x 64
+    tile (cluster split-K, KS = 2: each CTA accumulates one 512-wide K chunk, a DSMEM reduction adds
+    the two), batch 3 as one CTA per 128 x 128 tile summing its two K runs in TMEM.  Same arithmetic
+    (sym_gemm_split_k): bitwise-equal products and projections."""
+    x = synth.goe(1024, 21)
+    X3 = np.stack([synth.goe(1024, 22), x, synth.goe(1024, 23)])
+    P1, _, _ = _gpu(pkg, _product_filter("c3", pkg), x[None], prec)
+    P3, _, _ = _gpu(pkg, _product_filter("c3", pkg), X3, prec)
+    assert np.array_equal(P1[0], P3[1])
+    f = pkg.Filter(pkg.filters.half_filter(), precision=prec)
+    t1 = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+    t3 = torch.tensor(X3, dtype=torch.float32, device="cuda")
+    C1 = f.sym_product(t1, t1).cpu().numpy()
+    C3 = f.sym_product(t3, t3).cpu().numpy()
+    assert np.array_equal(C1[0], C3[1])
+
+
 def test_zero_nan_and_upper_triangle(pkg):
     """lambda~ = 0 gives 0; a NaN input sets PSD_ENONFINITE; only the upper
     triangle of X is read (reading R10)."""
@@ -246,7 +265,8 @@ TOL_X3 = {"fp16x3": 1e-5, "tf32x3": 1e-5, "bf16x3": 1e-4}
     (300, 1, "goe", "half", "bf16x3"),
     (1024, 8, "goe", "single", "fp16x3"),     # CTA-pair kernel, split
     (1024, 8, "sdp_shaped", "single", "tf32x3"),
-    (1024, 1, "goe", "c3", "fp16x3"),         # config c3, FP32-class
+    (1024, 1, "goe", "c3", "fp16x3"),         # config c3, FP32-class (cluster split-K)
+    (1024, 1, "goe", "c3", "tf32x3"),
 ])
 def test_split_precision_parity(pkg, n, batch, family, which, prec):
     X = synth.batch(family, n, batch, synth.SEED_BASE + 5 * n)
