@@ -37,18 +37,25 @@ def build(verbose=False, force=False, debug=False):
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "psd_filter.h"))
-    objs = []
+    objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC] + ARCH + FLAGS + (["-DPSD_DEBUG"] if debug else []) + ["-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode != 0:
-                sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-            if r.returncode != 0:
-                raise RuntimeError("nvcc failed for " + src)
+            jobs.append((src, [NVCC] + ARCH + FLAGS + (["-DPSD_DEBUG"] if debug else []) + ["-c", s, "-o", o]))
+    # the translation units are independent: compile them concurrently
+    procs = [(src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+             for src, cmd in jobs]
+    failed = []
+    for src, cmd, p in procs:
+        out, err = p.communicate()
+        if verbose or p.returncode != 0:
+            sys.stderr.write(" ".join(cmd) + "\n" + out + err)
+        if p.returncode != 0:
+            failed.append(src)
+    if failed:
+        raise RuntimeError("nvcc failed for " + ", ".join(failed))
     if force or _stale(lib, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
