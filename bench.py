@@ -234,43 +234,56 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(cfg, stages_oracle, kappas, seconds_cap=30.0):
+def cpu_oracle_sample(cfg, stages_oracle, kappas, seconds_cap=30.0, seconds_min=10.0):
     """Time the float64 oracle (as it stands) on a bounded sample of the workload.
 
-    Sample: one matrix of the config; stages of Algorithm 2 are run one at a time until
-    ~seconds_cap is spent (at least one stage); the per-matrix time is extrapolated by the
-    GEMM count (each oracle stage costs (d+1)/2 matmuls, the return line one more)."""
+    Sample: whole matrices of the config (seeded like the GPU arm's inputs), one after another
+    until ~seconds_min of CPU work is done; when a matrix does not finish within seconds_cap, its
+    stages of Algorithm 2 are run one at a time until the cap (at least one stage) and the
+    per-matrix time is extrapolated by the GEMM count (each oracle stage costs (d+1)/2 matmuls,
+    the return line one more)."""
     import numpy as np
     from threadpoolctl import threadpool_info
 
     import synth
     from oracle import chain
     n = cfg["n"]
-    X = synth.make(cfg["family"], n, synth.SEED_BASE)
-    t0 = time.perf_counter()
-    lam = chain.frobenius_bound(X)
-    Z = X / lam
+    total_gemms = chain.gemm_count([2 * len(c) - 1 for c in stages_oracle])
+    t_start = time.perf_counter()
     done_gemms = 0
+    mats = 0
     stages_run = 0
-    for t, c in enumerate(stages_oracle):
-        Z = chain.odd_poly_matrix(Z, c)
-        if kappas is not None:
-            Z = kappas[t] * Z
-        done_gemms += len(c) if len(c) > 1 else 0
-        stages_run += 1
-        if time.perf_counter() - t0 > seconds_cap:
+    while True:
+        X = synth.make(cfg["family"], n, synth.SEED_BASE + mats)
+        lam = chain.frobenius_bound(X)
+        Z = X / lam
+        stages_run = 0
+        for t, c in enumerate(stages_oracle):
+            Z = chain.odd_poly_matrix(Z, c)
+            if kappas is not None:
+                Z = kappas[t] * Z
+            done_gemms += len(c) if len(c) > 1 else 0
+            stages_run += 1
+            if time.perf_counter() - t_start > seconds_cap:
+                break
+        if stages_run < len(stages_oracle):
             break
-    if stages_run == len(stages_oracle):
         P = lam * 0.5 * (X / lam @ (np.eye(n) + Z))
         done_gemms += 1
         del P
-    el = time.perf_counter() - t0
-    total_gemms = chain.gemm_count([2 * len(c) - 1 for c in stages_oracle])
+        mats += 1
+        if time.perf_counter() - t_start >= seconds_min:
+            break
+    el = time.perf_counter() - t_start
     per_matrix = el * total_gemms / max(done_gemms, 1)
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    sample = (f"oracle/chain.py float64 on 1 of the {cfg['batch']} matrices (n={n}), {stages_run} of "
-              f"{len(stages_oracle)} stages = {done_gemms} of {total_gemms} numpy matmuls in {el:.1f} s, "
-              f"extrapolated by GEMM count")
+    if mats:
+        sample = (f"oracle/chain.py float64 on {mats} whole matrices of this config (n={n}, seeded like the "
+                  f"GPU arm), {done_gemms} numpy matmuls ({total_gemms} per matrix) in {el:.1f} s")
+    else:
+        sample = (f"oracle/chain.py float64 on 1 of the {cfg['batch']} matrices (n={n}), {stages_run} of "
+                  f"{len(stages_oracle)} stages = {done_gemms} of {total_gemms} numpy matmuls in {el:.1f} s, "
+                  f"extrapolated by GEMM count")
     return 1.0 / per_matrix, threads, sample
 
 
@@ -292,11 +305,11 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     st, kap = oracle_filter(filter_name(cfg, args.precision))
-    per_step = max(5.0, 100.0 / max(args.steps + args.warmup, 1))
+    per_step = max(min(5.0, args.ref_seconds), args.ref_seconds / max(args.steps + args.warmup, 1))
     vals = []
     threads, sample = 1, ""
     for i in range(args.warmup + args.steps):
-        v, threads, sample = cpu_oracle_sample(cfg, st, kap, seconds_cap=per_step)
+        v, threads, sample = cpu_oracle_sample(cfg, st, kap, seconds_cap=per_step, seconds_min=per_step)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -539,6 +552,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=100.0,
+                    help="reference arm: CPU seconds for the whole --steps + --warmup run")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.precision is None:

@@ -150,9 +150,9 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     if (warp == 0) {
         if (ptx::elect_one()) {
             const uint64_t pol = ptx::policy_evict_last();
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int st = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
+            int st = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < num_kb; ++kb, st = (st + 1 == kStages) ? 0 : st + 1, ph ^= (st == 0)) {
                 ptx::mbar_wait(&empty[st], ph ^ 1);
                 uint8_t* sa = ring + st * kStageBytes;
                 const int kx = (kb0 + kb) * kBK;
@@ -180,16 +180,23 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         __syncwarp();
     } else if (warp == 1) {
         if (ptx::elect_one()) {
+            // the issue loop is the mainloop's critical path at N = 64 (4 MMAs = 192 tensor cycles per
+            // K block): ring position, run position and the MN-major switch are kept as counters and
+            // bounds instead of per-block divisions (tools/micro/tma_ingress.cu: the same pipeline with
+            // a lean issue loop runs a K block in ~280 cycles)
+            const bool up = Tr::kBytes == 2 && s.upper_only;
+            const int a_mn_end = up ? I * kTile : 0;                      // kx below: MN-major (transposed)
+            const int b_mn_end = up ? (J * BN / kTile) * kTile : 0;
+            const uint32_t ring0 = ptx::smem_u32(ring);
+            int st = 0, kr = 0, run = 0;
+            uint32_t ph = 0;
             for (int kb = 0; kb < num_kb; ++kb) {
-                const int st = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
                 ptx::mbar_wait(&full[st], ph);
                 ptx::tc_fence_after();
-                const uint32_t sa = ptx::smem_u32(ring + st * kStageBytes);
+                const uint32_t sa = ring0 + static_cast<uint32_t>(st * kStageBytes);
                 const int kx = (kb0 + kb) * kBK;
-                const bool up = Tr::kBytes == 2 && s.upper_only;
-                const bool a_mn = up && kx < I * kTile;
-                const bool b_mn = up && kx < (J * BN / kTile) * kTile;
+                const bool a_mn = kx < a_mn_end;
+                const bool b_mn = kx < b_mn_end;
                 // MN-major (transposed) operands: 64-element MN chunks 8 KB apart, 8-row K groups 1 KB
                 // apart, one K step of 16 = 2 KB (tools/micro/mn_major.cu)
                 auto desc = [&](uint32_t addr, bool mn) {
@@ -205,8 +212,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                     else
                         ptx::mma_f16(d, a, bb, idesc, accumulate);
                 };
-                const int kr = kb % run_kb;                   // position in its accumulation run
-                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>((kb / run_kb) * BN);
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(run * BN);
 #pragma unroll
                 for (int k = 0; k < kBK / kUmmaK; ++k) {
                     mma(d_tmem, adesc + k * astep, bdesc + k * bstep, (kr | k) != 0);
@@ -218,6 +224,8 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                     }
                 }
                 ptx::mma_commit(&empty[st]);
+                if (++st == kStages) { st = 0; ph ^= 1; }
+                if (++kr == run_kb) { kr = 0; ++run; }            // next accumulation run (split precisions)
             }
             ptx::mma_commit(accum_full);
         }

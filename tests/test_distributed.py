@@ -275,7 +275,7 @@ def test_bench_spawns_ranks_cpu():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
-                        "--config", "c3", "--steps", "1", "--warmup", "0"],
+                        "--config", "c3", "--steps", "1", "--warmup", "0", "--ref-seconds", "2"],
                        capture_output=True, text=True, timeout=600, env=env, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
