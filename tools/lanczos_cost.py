@@ -1,4 +1,5 @@
-"""Cost of the Lanczos/Theorem-2 bound at the c4 shape (n = 4096, batch 32), CUDA events, warm.
+"""Cost of the Lanczos/Theorem-2 bound (default: the c4 shape, n = 4096, batch 32; argv: n batch), CUDA
+events, warm.
 
 Times psd_project with the Frobenius and the Lanczos bound for f~*_half (T = 7, 22 products) and
 for a product-free filter (one degree-1 stage: the bound + scale + reconstruction only), so the
@@ -9,9 +10,11 @@ sys.path.insert(0, ".")
 import paper_2507_09165_b200 as pkg
 import synth
 
-n, batch = 4096, 32
-X = torch.tensor(synth.batch("goe", n, 4, 5), dtype=torch.float32, device="cuda")
-X = X.repeat(batch // 4, 1, 1).contiguous()
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+uniq = min(4, batch)
+X = torch.tensor(synth.batch("goe", n, uniq, 5), dtype=torch.float32, device="cuda")
+X = X.repeat(batch // uniq, 1, 1).contiguous()
 out = torch.empty_like(X)
 
 
