@@ -54,6 +54,7 @@ struct EpiParams {
     int packed_f32;
     // debug: CTA 0 thread 0 stores %globaltimer at kernel phases (NULL in production)
     unsigned long long* dbg;
+    unsigned long long* dbg_all;   // debug build: per-CTA %globaltimer stamps (PSD_DEBUG_TIMELINE, 1-CTA kernel)
     int dbg_nostore;          // debug experiment (PSD_DEBUG_NOSTORE): skip the epilogue's stores
     int upper_only;           // store off-diagonal tiles of the operand copy without their mirror
     // Peer-memory row-panel mode (the product and its all-gather in one kernel): the operand copy

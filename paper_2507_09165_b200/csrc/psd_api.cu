@@ -656,10 +656,48 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             cudaMemsetAsync(ep.dbg + 8, 0xFF, 8, st);
             cudaMemsetAsync(ep.dbg + 11, 0xFF, 8, st);
         }
+        // debug build: every CTA's phase stamps of the 1-CTA kernel (PSD_DEBUG_TIMELINE; synchronous)
+        static unsigned long long* tl_buf = nullptr;
+        constexpr int kTlSlots = 1 << 16;
+        const bool tl = !pair && !h->capturing && debug_env("PSD_DEBUG_TIMELINE") != nullptr;
+        if (tl) {
+            if (!tl_buf && cudaMalloc(&tl_buf, kTlSlots * sizeof(unsigned long long)) != cudaSuccess) tl_buf = nullptr;
+            if (tl_buf) {
+                cudaMemsetAsync(tl_buf, 0, kTlSlots * sizeof(unsigned long long), st);
+                ep.dbg_all = tl_buf;
+            }
+        }
         e = pair ? launch_sym_gemm_2cta(ws.op, split, maps(s.A, s.B), shape, ep, st)
                  : launch_sym_gemm(ws.op, split, maps(s.A, s.B), shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
+        if (tl && tl_buf) {
+            std::vector<unsigned long long> t(kTlSlots);
+            cudaStreamSynchronize(st);
+            cudaMemcpy(t.data(), tl_buf, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+            std::vector<double> wait, loop, epi;
+            unsigned long long t0 = ~0ull, s_max = 0, e_max = 0;
+            int ctas = 0;
+            for (int c = 0; c < kTlSlots / 4 && t[4 * c + 3]; ++c, ++ctas) {
+                t0 = std::min(t0, t[4 * c]);
+                s_max = std::max(s_max, t[4 * c]);
+                e_max = std::max(e_max, t[4 * c + 3]);
+                wait.push_back(double(t[4 * c + 1] - t[4 * c]));
+                loop.push_back(double(t[4 * c + 2] - t[4 * c + 1]));
+                epi.push_back(double(t[4 * c + 3] - t[4 * c + 2]));
+            }
+            auto med = [](std::vector<double> v) {
+                if (v.empty()) return 0.0;
+                std::sort(v.begin(), v.end());
+                return v[v.size() / 2] * 1e-3;
+            };
+            auto mx = [](const std::vector<double>& v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()) * 1e-3; };
+            if (ctas)
+                std::fprintf(stderr, "psd timeline step %zu: %d CTAs, starts spread %.2f us, prologue+wait med %.2f us, "
+                             "mainloop med %.2f max %.2f us, epilogue+exit med %.2f max %.2f us, first start -> last end "
+                             "%.2f us\n", si, ctas, (s_max - t0) * 1e-3, med(wait), med(loop), mx(loop), med(epi), mx(epi),
+                             (e_max - t0) * 1e-3);
+        }
         if (dbg) {           // debug only: per-product phase counters of the pair kernel
             unsigned long long t[13] = {};
             cudaStreamSynchronize(st);

@@ -66,6 +66,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 #define DBG_STAMP(i) do { if (kDebug && e.dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) e.dbg[i] = gtimer(); } while (0)
+// every CTA's thread 0: [0] start, [1] after griddepcontrol.wait, [2] accumulator complete, [3] end
+#define DBG_ALL(i) do { if (kDebug && e.dbg_all && threadIdx.x == 0) \
+    e.dbg_all[4 * (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) + (i)] = gtimer(); } while (0)
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -114,6 +117,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     int I, J;
     upper_tile_coords<BN>(blockIdx.x / KS, s.npad, I, J);
     DBG_STAMP(0);
+    DBG_ALL(0);
 
     if (warp == 0) {
         if (ptx::elect_one()) {
@@ -137,6 +141,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     DBG_STAMP(1);
     grid_dep_wait();                                  // the operands are the previous kernel's output
     DBG_STAMP(2);
+    DBG_ALL(1);
 
     const int num_kb = s.npad / kBK / KS;             // this CTA's K slice
     const int kb0 = krank * num_kb;
@@ -236,6 +241,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     ptx::mbar_wait(accum_full, 0);
     ptx::tc_fence_after();
     DBG_STAMP(3);
+    DBG_ALL(2);
     grid_dep_launch();                               // the next kernel may start its prologue
 
     const bool diag = (I * kTile < J * BN + BN) && (J * BN < I * kTile + kTile);   // tile meets the diagonal
@@ -326,6 +332,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
         ptx::tmem_dealloc<kCols>(tmem_base);
     }
     DBG_STAMP(5);
+    DBG_ALL(3);
 }
 
 template <OpType T, bool kSplit, int KS, int BN>
