@@ -402,6 +402,16 @@ std::vector<Step> build_plan(const psd_filter_s* h, bool want_sign, double* sign
 // Whether the per-product launches of run_body keep the operand copies upper-only (see
 // GemmShape::upper_only): 16-bit operands, on the CTA-pair kernel and on the 1-CTA kernel (with or
 // without cluster split-K).
+// K accumulation chunk of the product kernels: the split precisions restart the accumulator every
+// h->kchunk K elements (R23); single-pass products on the 1-CTA kernel at npad == 2 kchunk (c3,
+// n = 1024) accumulate the two K halves separately, the arithmetic of the KS = 2 cluster launch
+// (sym_gemm_split_k) -- faster at batch 1, and every batch size computes the same bits.
+int product_kchunk(const psd_filter_s* h, bool split, int n, int npad, int batch) {
+    if (split) return h->kchunk;
+    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+    return (!pair && h->kchunk > 0 && npad == 2 * h->kchunk) ? h->kchunk : 0;
+}
+
 bool upper_only_mode(const psd_filter_s* h, int n, int batch, int npad) {
     if (op_of(h->prec) == OpType::TF32 || debug_env("PSD_NO_UPPER_ONLY")) return false;
     (void)h; (void)n; (void)batch; (void)npad;
@@ -598,7 +608,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     e = cudaMemsetAsync(ws.counters, 0, steps.size() * sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
-    shape.kchunk = split ? h->kchunk : 0;
+    shape.kchunk = product_kchunk(h, split, n, npad, batch);
     std::pair<cudaEvent_t, cudaEvent_t> evp{nullptr, nullptr};
     if (h->profiling && !h->capturing && !steps.empty()) {
         evp = {take_event(h), take_event(h)};
@@ -1709,7 +1719,7 @@ psd_status_t psd_sym_product(psd_filter_t h, const float* A, const float* B, con
     e = cudaMemsetAsync(ws.counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
     GemmShape shape{npad, batch, ws.tiles, ws.tiles_per_matrix, ws.counters};
-    shape.kchunk = split ? h->kchunk : 0;
+    shape.kchunk = product_kchunk(h, split, n, npad, batch);
     const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
     const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     OperandMaps m;

@@ -46,6 +46,23 @@ template <bool kSplit, int BN> struct Ring1 {
     static constexpr int kStages = kRingBytes1 / kStageBytes;
 };
 constexpr int kSmemBytes = kRingBytes1 + 1024 + 256 + kWarps * kEpiWarpSmemBytes;  // ring, align, barriers, staging
+// cluster split-K with KS = 2: the peer's partial of this CTA's half of the tile rows (64 x BN fp32)
+template <int KS, int BN> constexpr int kRecvBytes = KS == 2 ? 64 * BN * 4 : 0;
+template <int KS, int BN> constexpr int kSmemBytesKs = kSmemBytes + kRecvBytes<KS, BN>;
+
+// receive-buffer layout: row r (0..63) of BN fp32, float4 column q stored at q ^ (r & 15) -- the 8 lanes
+// of a 128-bit access phase (8 consecutive rows, same q) hit 8 different 16-byte bank groups
+template <int BN>
+__device__ __forceinline__ uint32_t recv_off(int r, int q) {
+    return static_cast<uint32_t>((r * (BN / 4) + (q ^ (r & 15))) * 16);
+}
+
+// 16 bytes into a peer CTA's shared memory, completion counted on the peer's mbarrier (bytes)
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 :: "r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(cluster_bar) : "memory");
+}
 
 // Row-major enumeration of the 128 x BN tiles (row block I, column block J) that hold any
 // upper-triangle element: J >= I * (128 / BN).
@@ -98,7 +115,9 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     constexpr uint32_t kIdesc = ptx::make_idesc(Tr::kFmt, kTile, BN);
     // split precisions (KS = 1): the K range is cut into up to 512 / BN runs, each accumulated from
     // zero in its own TMEM columns and summed round-to-nearest in the epilogue (GemmShape::kchunk)
-    constexpr bool kRuns = kSplit && KS == 1;
+    // (single pass: two runs of npad / 2 when the planner sets kchunk = npad / 2, the K split of the
+    // KS = 2 cluster launch, so batch sizes that do and do not take the cluster agree bitwise)
+    constexpr bool kRuns = KS == 1;
     constexpr uint32_t kCols = kRuns ? 512 : BN;
 
     extern __shared__ uint8_t smem_raw[];
@@ -107,8 +126,10 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes1);
     uint64_t* empty = full + kStages;
     uint64_t* accum_full = empty + kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+    uint64_t* recv_bar = accum_full + 1;                          // KS == 2: the peer's partial landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
     uint8_t* epi_smem = smem + kRingBytes1 + 256;                   // kWarps x kEpiWarpSmemBytes
+    uint8_t* recv = epi_smem + kWarps * kEpiWarpSmemBytes;          // KS == 2: kRecvBytes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -128,6 +149,11 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                 ptx::mbar_init(&empty[i], 1);
             }
             ptx::mbar_init(accum_full, 1);
+            if constexpr (KS == 2) {
+                // phase 0 completes when the peer's kRecvBytes have landed (its st.async complete_tx)
+                ptx::mbar_init(recv_bar, 1);
+                ptx::mbar_arrive_expect_tx(recv_bar, kRecvBytes<KS, BN>);
+            }
             ptx::fence_barrier_init();
         }
         __syncwarp();
@@ -137,6 +163,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if constexpr (KS == 2) ptx::cluster_sync();      // both CTAs' recv_bar initialised before any st.async
     const uint32_t tmem_base = *tmem_slot;
     DBG_STAMP(1);
     grid_dep_wait();                                  // the operands are the previous kernel's output
@@ -273,6 +300,62 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
             }
             epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
         }
+    } else if constexpr (KS == 2) {
+        // Push reduction: CTA k finishes rows [64k, 64k + 64) of the tile (TMEM quadrants 2k, 2k + 1).
+        // The warps on the other two quadrants send this CTA's partial of the peer's rows straight into
+        // the peer's receive buffer (st.async, counted on the peer's recv_bar) while the warps on this
+        // CTA's own quadrants load their partial from TMEM, wait for the peer's, add the two in rank
+        // order -- p0 + p1, the arithmetic of the single-CTA K-run sum -- and run the epilogue.  No parking
+        // of the own partial, no cluster barrier after the mainloop, all 8 warps busy.
+        const int quad = warp & 3;
+        const int rr = (quad & 1) * 32 + lane;                 // row within a 64-row half
+        const bool mine = (quad >> 1) == krank;
+        if (!mine) {
+            const uint32_t peer = static_cast<uint32_t>(krank ^ 1);
+            const uint32_t rbuf = ptx::mapa_shared(ptx::smem_u32(recv), peer);
+            const uint32_t rbar = ptx::mapa_shared(ptx::smem_u32(recv_bar), peer);
+#pragma unroll 1
+            for (int c0 = (warp >> 2) * 32; c0 < BN; c0 += 64) {
+                uint32_t raw[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c0, raw);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    st_async_v4(rbuf + recv_off<BN>(rr, c0 / 4 + q), raw[4 * q], raw[4 * q + 1], raw[4 * q + 2],
+                                raw[4 * q + 3], rbar);
+            }
+        } else {
+            const int gi0 = I * kTile + quad * 32;
+            bool waited = false;
+#pragma unroll 1
+            for (int c0 = (warp >> 2) * 32; c0 < BN; c0 += 64) {
+                const int gj0 = J * BN + c0;
+                if (diag && gj0 + 31 < gi0) continue;
+                uint32_t own[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c0, own);
+                ptx::tmem_ld_wait();
+                if (!waited) {
+                    ptx::mbar_wait(recv_bar, 0);
+                    waited = true;
+                }
+                uint32_t raw[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(recv + recv_off<BN>(rr, c0 / 4 + q));
+                    const float pv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float mine_v = __uint_as_float(own[4 * q + i]);
+                        const float p0 = krank == 0 ? mine_v : pv[i];
+                        const float p1 = krank == 0 ? pv[i] : mine_v;
+                        raw[4 * q + i] = __float_as_uint(__fadd_rn(p0, p1));
+                    }
+                }
+                epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+            }
+            // a CTA must not exit while the peer's st.async into its receive buffer is in flight
+            if (!waited) ptx::mbar_wait(recv_bar, 0);
+        }
     } else {
         // park this CTA's partial accumulator (all MMAs done -> the ring is free)
         const int r = (warp & 3) * 32 + lane;
@@ -340,7 +423,7 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t err = cudaFuncSetAttribute(sym_gemm_kernel<T, kSplit, KS, BN>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesKs<KS, BN>);
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
@@ -349,7 +432,7 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(tiles * KS, s.batch);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = kSmemBytesKs<KS, BN>;
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
     int na = 0;
@@ -384,18 +467,20 @@ cudaError_t launch_ks(int ks, int bn, const OperandMaps& m, const GemmShape& s, 
 
 }  // namespace
 
-// Split-K factor for a few-tile problem.  Measured (n = 1024, 19 products, 8-warp epilogue,
-// profiles/r2_epi8/): single-pass fp16 KS = 1 154 us, KS = 2 175 us -- the cluster barriers and the
-// DSMEM reduction cost more than the extra SMs gain; the 3-pass split precisions (3 MMAs per K step,
-// a mainloop-bound chain) KS = 1 274 us, KS = 2 238 us.  KS = 2 is therefore taken for the split
-// precisions when it fills at most one wave AND the K range is exactly two accumulation chunks
-// (npad == 2 kchunk): each CTA of the pair then accumulates one chunk from zero and the reduction
-// adds the two in order -- the same arithmetic as the single-CTA K-run summation (bit-identical).
+// Split-K factor for a few-tile problem.  KS = 2 (a cluster of two CTAs per tile, each accumulating
+// one K half; the halves meet through the st.async push reduction) is taken when the CTA pairs fill
+// at most one wave AND the K range is exactly two accumulation chunks (npad == 2 kchunk), so each CTA
+// accumulates one chunk from zero and the reduction adds the two in order -- the arithmetic of the
+// single-CTA K-run sum (bit-identical; the planner sets kchunk = npad / 2 for the single-pass 1-CTA
+// path at npad = 1024).  Measured at c3 (n = 1024, 19 products; profiles/r2s3/push/): fp16 KS = 1 149
+// vs KS = 2 142 us (debug build), fp16x3 229 -> 197 us and tf32x3 328 -> 295 us with the push
+// reduction (the round-2 DSMEM pull reduction had made single-pass KS = 2 slower: 175 vs 154 us).
 int sym_gemm_split_k(int npad, int batch, OpType t, bool split, int kchunk) {
     static const int forced = debug_env("PSD_SPLITK") ? std::atoi(debug_env("PSD_SPLITK")) : 0;
     if (forced == 1 || forced == 2 || forced == 4) return forced;
     (void)t;
-    if (!split || kchunk <= 0 || npad != 2 * kchunk) return 1;
+    (void)split;
+    if (kchunk <= 0 || npad != 2 * kchunk) return 1;
     const int bn = sym_gemm_bn(npad, batch);
     const int nrb = npad / kTile, ncb = npad / bn;
     const int tiles = (nrb * ncb - (kTile / bn) * nrb * (nrb - 1) / 2) * batch;

@@ -153,11 +153,12 @@ def test_batch_position_determinism_and_inplace(pkg, n, prec, which):
     assert np.array_equal(Pi, P)
 
 
-@pytest.mark.parametrize("prec", ["fp16x3", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp16", "bf16", "fp16x3", "tf32x3"])
 def test_split_k_cluster_matches_single_cta_runs(pkg, prec):
-    """n = 1024 on the 1-CTA kernel: batch 1 runs the split precisions as a CTA pair per 128 x 64
-    tile (cluster split-K, KS = 2: each CTA accumulates one 512-wide K chunk, a DSMEM reduction adds
-    the two), batch 3 as one CTA per 128 x 128 tile summing its two K runs in TMEM.  Same arithmetic
+    """n = 1024 on the 1-CTA kernel: batch 1 runs as a CTA pair per 128 x 64 tile (cluster split-K,
+    KS = 2: each CTA accumulates one 512-wide K chunk, the st.async push reduction adds the two),
+    batch 3 as one CTA per 128 x 128 tile summing its two K runs in TMEM -- on the split precisions
+    (R23's chunks) and on the single-pass ones (K halves, product_kchunk).  Same arithmetic
     (sym_gemm_split_k): bitwise-equal products and projections."""
     x = synth.goe(1024, 21)
     X3 = np.stack([synth.goe(1024, 22), x, synth.goe(1024, 23)])
