@@ -685,16 +685,22 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             std::vector<unsigned long long> t(kTlSlots);
             cudaStreamSynchronize(st);
             cudaMemcpy(t.data(), tl_buf, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            std::vector<double> wait, loop, epi;
+            std::vector<double> wait, loop, epi, pre, chunk, post;
             unsigned long long t0 = ~0ull, s_max = 0, e_max = 0;
             int ctas = 0;
-            for (int c = 0; c < kTlSlots / 4 && t[4 * c + 3]; ++c, ++ctas) {
-                t0 = std::min(t0, t[4 * c]);
-                s_max = std::max(s_max, t[4 * c]);
-                e_max = std::max(e_max, t[4 * c + 3]);
-                wait.push_back(double(t[4 * c + 1] - t[4 * c]));
-                loop.push_back(double(t[4 * c + 2] - t[4 * c + 1]));
-                epi.push_back(double(t[4 * c + 3] - t[4 * c + 2]));
+            for (int c = 0; c < kTlSlots / 8 && t[8 * c + 3]; ++c, ++ctas) {
+                const unsigned long long* u = &t[8 * c];
+                t0 = std::min(t0, u[0]);
+                s_max = std::max(s_max, u[0]);
+                e_max = std::max(e_max, u[3]);
+                wait.push_back(double(u[1] - u[0]));
+                loop.push_back(double(u[2] - u[1]));
+                epi.push_back(double(u[3] - u[2]));
+                if (u[4] && u[5]) {
+                    pre.push_back(double(u[4] - u[2]));      // accumulator ready -> first chunk's epilogue
+                    chunk.push_back(double(u[5] - u[4]));    // one epilogue_chunk
+                    post.push_back(double(u[6] - u[5]));     // -> final barrier passed
+                }
             }
             auto med = [](std::vector<double> v) {
                 if (v.empty()) return 0.0;
@@ -704,20 +710,10 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             auto mx = [](const std::vector<double>& v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()) * 1e-3; };
             if (ctas)
                 std::fprintf(stderr, "psd timeline step %zu: %d CTAs, starts spread %.2f us, prologue+wait med %.2f us, "
-                             "mainloop med %.2f max %.2f us, epilogue+exit med %.2f max %.2f us, first start -> last end "
-                             "%.2f us\n", si, ctas, (s_max - t0) * 1e-3, med(wait), med(loop), mx(loop), med(epi), mx(epi),
-                             (e_max - t0) * 1e-3);
-        }
-        if (dbg) {           // debug only: per-product phase counters of the pair kernel
-            unsigned long long t[13] = {};
-            cudaStreamSynchronize(st);
-            cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);
-            const double tiles = t[4] ? double(t[4]) : 1.0;
-            std::fprintf(stderr, "psd step %zu (D %d, out %s): loop %.0f = tile %.0f + acc %.0f + operand %.0f + issue; "
-                         "epilogue acc-wait %.0f work %.0f cycles/tile; %llu clusters (tiles %llu..%llu), starts "
-                         "spread %.1f us, last end %.1f us after first start\n", si, s.D, s.outF ? "fp32" : "op",
-                         t[3] / tiles, t[0] / tiles, t[1] / tiles, t[2] / tiles, t[5] / (2 * tiles), t[6] / (2 * tiles),
-                         t[7], t[11], t[12], (t[9] - t[8]) * 1e-3, (t[10] - t[8]) * 1e-3);
+                             "mainloop med %.2f max %.2f us, epilogue+exit med %.2f max %.2f us (acc->chunk %.2f, "
+                             "chunk %.2f, chunk->barrier %.2f), first start -> last end %.2f us\n", si, ctas,
+                             (s_max - t0) * 1e-3, med(wait), med(loop), mx(loop), med(epi), mx(epi), med(pre), med(chunk),
+                             med(post), (e_max - t0) * 1e-3);
         }
     }
     if (evp.first) {

@@ -83,9 +83,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 #define DBG_STAMP(i) do { if (kDebug && e.dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) e.dbg[i] = gtimer(); } while (0)
-// every CTA's thread 0: [0] start, [1] after griddepcontrol.wait, [2] accumulator complete, [3] end
+// every CTA's thread 0: [0] start, [1] after griddepcontrol.wait, [2] accumulator complete, [3] end,
+// [4] / [5] before / after its first epilogue_chunk (0 if thread 0 runs none), [6] after the final barrier
 #define DBG_ALL(i) do { if (kDebug && e.dbg_all && threadIdx.x == 0) \
-    e.dbg_all[4 * (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) + (i)] = gtimer(); } while (0)
+    e.dbg_all[8 * (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) + (i)] = gtimer(); } while (0)
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -298,7 +299,9 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                         raw[i] = __float_as_uint(__fadd_rn(__uint_as_float(raw[i]), __uint_as_float(part[i])));
                 }
             }
+            if (c0 < 32) DBG_ALL(4);
             epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+            if (c0 < 32) DBG_ALL(5);
         }
     } else if constexpr (KS == 2) {
         // Push reduction: CTA k finishes rows [64k, 64k + 64) of the tile (TMEM quadrants 2k, 2k + 1).
@@ -351,7 +354,9 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
                         raw[4 * q + i] = __float_as_uint(__fadd_rn(p0, p1));
                     }
                 }
+                if (c0 < 32) DBG_ALL(4);
                 epilogue_chunk<T>(e, alpha, b, s.npad, gi0, gj0, diag, raw, wsmem);
+                if (c0 < 32) DBG_ALL(5);
             }
             // a CTA must not exit while the peer's st.async into its receive buffer is in flight
             if (!waited) ptx::mbar_wait(recv_bar, 0);
@@ -410,6 +415,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     DBG_STAMP(4);
     ptx::tc_fence_before();
     __syncthreads();
+    DBG_ALL(6);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<kCols>(tmem_base);

@@ -2,7 +2,7 @@
 synccheck): python tools/sanitize.py [quick]
 
 Covers: the batched small-n kernel (fp16 / fp16x3, ragged n, sign, ADMM), the 1-CTA product
-kernel (fp16, fp16x3, bf16, tf32), the CTA-pair kernel (fp16, fp16x3 with K-chunked accumulation),
+kernel (fp16, fp16x3, bf16, tf32; cluster split-K with the push reduction), the CTA-pair kernel (fp16, fp16x3 with K-chunked accumulation),
 the Lanczos bound, the row-panel paths (NCCL-free virtual ranks, peer-memory virtual ranks), the
 pipelined host path and psd_sym_product.  Each case is checked against nothing -- the sanitizer's
 report is the result; the parity suite covers correctness."""
@@ -44,6 +44,11 @@ run("small ADMM n=48", admm_small)
 for prec in ["fp16", "fp16x3", "bf16", "tf32"]:
     run(f"1-CTA {prec} n=300", lambda: Filter(single if prec.endswith("x3") else half, precision=prec).project(mats(300, 2)))
 run("1-CTA fp16 sign n=200", lambda: Filter(half).sign(mats(200, 2)))
+# cluster split-K (KS = 2, st.async push reduction) and the single-CTA two-run equivalent, n = 1024
+ns1 = [[1.5, -0.5]]          # one Newton-Schulz stage: 2 products + the reconstruction
+run("1-CTA cluster split-K fp16 n=1024 b=1", lambda: Filter(ns1).project(mats(1024, 1)))
+run("1-CTA cluster split-K fp16x3 n=1024 b=1", lambda: Filter(ns1, precision="fp16x3").project(mats(1024, 1)))
+run("1-CTA K halves fp16 n=1024 b=3", lambda: Filter(ns1).project(mats(1024, 3)))
 run("Lanczos fp16 n=300", lambda: Filter(half, bound="lanczos").project(mats(300, 2)))
 if not quick:
     run("pair fp16 n=1024 b=8", lambda: Filter(half).project(mats(1024, 8)))
