@@ -396,6 +396,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& e, float alpha, 
             store_f32_block(e.outF2 + static_cast<int64_t>(b) * e.strideF, e.ldF, e.nF, gi0, gj0, diag32, m, wsmem);
         }
     }
+    if (kDebug && e.dbg_all && threadIdx.x == 0) {       // debug timeline: addend loaded and added
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        // the compiler must not hoist the stamp above the addend's use: make it depend on v
+        if (v[0] == 1234.5f && v[31] == 1234.5f) t += 1;
+        e.dbg_all[8 * (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) + 7] = t;
+    }
     if (diag32) symmetrize_block(v, wsmem);
     if (kDebug && e.dbg_nostore) {                             // debug experiment only: keep v live, store nothing
         float acc = 0.0f;

@@ -685,7 +685,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             std::vector<unsigned long long> t(kTlSlots);
             cudaStreamSynchronize(st);
             cudaMemcpy(t.data(), tl_buf, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            std::vector<double> wait, loop, epi, pre, chunk, post;
+            std::vector<double> wait, loop, epi, pre, chunk, post, addend;
             unsigned long long t0 = ~0ull, s_max = 0, e_max = 0;
             int ctas = 0;
             for (int c = 0; c < kTlSlots / 8 && t[8 * c + 3]; ++c, ++ctas) {
@@ -700,6 +700,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
                     pre.push_back(double(u[4] - u[2]));      // accumulator ready -> first chunk's epilogue
                     chunk.push_back(double(u[5] - u[4]));    // one epilogue_chunk
                     post.push_back(double(u[6] - u[5]));     // -> final barrier passed
+                    if (u[7] > u[4]) addend.push_back(double(u[7] - u[4]));   // chunk start -> addend added
                 }
             }
             auto med = [](std::vector<double> v) {
@@ -711,9 +712,9 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             if (ctas)
                 std::fprintf(stderr, "psd timeline step %zu: %d CTAs, starts spread %.2f us, prologue+wait med %.2f us, "
                              "mainloop med %.2f max %.2f us, epilogue+exit med %.2f max %.2f us (acc->chunk %.2f, "
-                             "chunk %.2f, chunk->barrier %.2f), first start -> last end %.2f us\n", si, ctas,
-                             (s_max - t0) * 1e-3, med(wait), med(loop), mx(loop), med(epi), mx(epi), med(pre), med(chunk),
-                             med(post), (e_max - t0) * 1e-3);
+                             "chunk %.2f of which addend %.2f, chunk->barrier %.2f), first start -> last end %.2f us\n", si,
+                             ctas, (s_max - t0) * 1e-3, med(wait), med(loop), mx(loop), med(epi), mx(epi), med(pre),
+                             med(chunk), med(addend), med(post), (e_max - t0) * 1e-3);
         }
     }
     if (evp.first) {
