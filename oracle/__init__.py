@@ -21,6 +21,8 @@ certify   -- e_float certificate over every float32 in [-1,1],
 remez     -- Algorithm 1 sequential Remez + App. A.
 admm      -- the SDP consumer: three-step ADMM with the filter as Pi; the
              fused S/X update of psd_admm_update and the full iteration for the pins.
+polar     -- the polar factor of a general square matrix by the same composite odd filter
+             (f(A) = sum_j c_j A (A^T A)^j per stage).
 spectral  -- Higham closed form via numpy eigh, spectral operator
              (P:L381-399), Hadamard-conjugated structured oracle for large n.
 
