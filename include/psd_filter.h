@@ -158,6 +158,26 @@ psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t b
                             float* out, const double* lambda_in, double* lambda_out,
                             int want_sign, void* stream);
 
+/* Polar iterate of a general square matrix by the same composite filter (the
+ * polar factor generalises the matrix sign): with A = W diag(sigma) V^T,
+ *     out[b] = W diag(s(sigma / lambda~)) V^T = f_T o ... o f_1 (A[b] / lambda~),
+ *     f_t(Z) = sum_j c_{t,j} Z (Z^T Z)^j,
+ * which approaches the orthogonal polar factor W V^T for singular values in [eps, 1] * lambda~.
+ * Computed through the symmetric path: the upper triangle of H = [[0, A], [A^T, 0]] (2n x 2n) is
+ * written to a handle-owned workspace, psd_sign runs on H (f(H) = [[0, f(A)], [f(A)^T, 0]]), and
+ * the top-right block is copied to `out` -- every step in this library's kernels, about 6x the
+ * flops of a direct nonsymmetric chain.
+ *   A, out : device, batch x n x n fp32 row-major (all of A is read; out fully written; out == A
+ *            allowed), 16-byte aligned.
+ *   lambda~: ||A||_F (>= ||A||_2 = ||H||_2; fp64, deterministic) with PSD_BOUND_FROBENIUS, the
+ *            Lanczos/Theorem-2 bound of H with PSD_BOUND_LANCZOS, lambda_in with PSD_BOUND_USER.
+ *   lambda_in  device, `batch` doubles, used iff the bound is PSD_BOUND_USER (else may be NULL).
+ *   lambda_out device, `batch` doubles receiving the lambda~ used; may be NULL.
+ * Workspace: 2 x batch x (2n)^2 fp32 beside the product workspace of n' = 2n.  Non-finite input
+ * sets PSD_ENONFINITE (psd_status).  Errors: PSD_EINVAL for NULL pointers, n < 1, batch < 1. */
+psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch, float* out,
+                       const double* lambda_in, double* lambda_out, void* stream);
+
 /* One fused S- and X-update of the three-step ADMM for the SDP pair of Eq. (exp:sdp)
  * (Eq. exp:admm-three-step), for diagonal constraint operators (max-cut:
  * A_i = e_i e_i^T, so A* y = Diag(y)):

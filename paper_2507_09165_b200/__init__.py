@@ -132,6 +132,27 @@ class Filter:
         """S = X_T = f_T o ... o f_1 (X / lambda~)."""
         return self._run(X, out, lambda_in, lambda_out, True, stream)
 
+    def polar(self, A, out=None, lambda_in=None, lambda_out=None, stream=None):
+        """The filter's polar iterate of a general square A: f_T o ... o f_1 (A / lambda~) with
+        f_t(Z) = sum_j c_j Z (Z^T Z)^j, i.e. W diag(s(sigma / lambda~)) V^T for A = W diag(sigma) V^T
+        (psd_polar; all of A is read)."""
+        import torch
+        Ab = _check_matrix(A)
+        out = torch.empty_like(A) if out is None else out
+        outb = _check_matrix(out)
+        if outb.shape != Ab.shape:
+            raise ValueError("out shape mismatch")
+        B, n = Ab.shape[0], Ab.shape[-1]
+        for name, lam in (("lambda_in", lambda_in), ("lambda_out", lambda_out)):
+            if lam is not None and not (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64
+                                        and lam.is_contiguous() and lam.numel() == B):
+                raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of batch elements")
+        li = ctypes.c_void_p(lambda_in.data_ptr()) if lambda_in is not None else None
+        lo = ctypes.c_void_p(lambda_out.data_ptr()) if lambda_out is not None else None
+        check(self._lib.psd_polar(self._h, ctypes.c_void_p(Ab.data_ptr()), n, B, ctypes.c_void_p(outb.data_ptr()),
+                                  li, lo, _stream_ptr(stream)), "psd_polar")
+        return out
+
     def admm_update(self, C, Xk, y, sigma, S_out=None, X_out=None, stream=None):
         """One fused ADMM S/X update (Eq. exp:admm-three-step) for diagonal
         constraints (A* y = Diag(y)): S = P(C - Diag(y) - Xk / sigma) by this filter and

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libpsdfilter.so")
-SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "bound_scale.cu", "small_batch.cu", "rowpanel.cu", "certificate.cu"]
+SOURCES = ["psd_api.cu", "sym_gemm.cu", "sym_gemm_2cta.cu", "bound_scale.cu", "small_batch.cu", "rowpanel.cu", "certificate.cu", "polar.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -174,6 +174,13 @@ cudaError_t launch_peer_wait(const unsigned long long* my_flags, int nranks, uns
 // Frobenius partial sums: partial[b*nblk + k] = sum over rows i == k (mod nblk) of
 // x_ii^2 + 2 sum_{j>i} x_ij^2 (upper triangle of matrix b), fp64.
 int bound_blocks_per_matrix(int n, int batch);
+// psd_polar (polar.cu): the upper triangle of H = [[0, A], [A^T, 0]] (2n x 2n) from a general A, with
+// per-block fp64 partial sums of a^2 (finalised by launch_finalize_bound into lambda~ = ||A||_F),
+// and the top-right n x n block of the 2n x 2n sign output
+int polar_blocks_per_matrix(int n, int batch);
+cudaError_t launch_polar_embed(const float* A, int n, int batch, float* H, double* partial, int nblk,
+                               cudaStream_t stream);
+cudaError_t launch_polar_extract(const float* S, int n, int batch, float* out, cudaStream_t stream);
 cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
                                       cudaStream_t stream, const InputForm& form = InputForm());
 

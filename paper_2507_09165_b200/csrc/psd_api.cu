@@ -157,6 +157,14 @@ struct psd_filter_s {
     int64_t product_launches_profiled = 0;
     int64_t kernel_launches = 0;
     int64_t last_products = 0;     // product-carrying launches of the last run_body (graph accounting)
+    // psd_polar: the 2n x 2n embedding H, the sign output on it, lambda~ and the norm partials
+    struct Polar {
+        float* H = nullptr;
+        float* S = nullptr;
+        double* lam = nullptr;
+        double* part = nullptr;
+        int64_t n = 0, batch = 0;
+    } pol;
 };
 
 namespace {
@@ -1347,8 +1355,19 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
     return PSD_OK;
 }
 
+void free_polar(psd_filter_s* h) {
+    auto& p = h->pol;
+    if (p.H || p.S || p.lam || p.part) cudaDeviceSynchronize();
+    if (p.H) cudaFree(p.H);
+    if (p.S) cudaFree(p.S);
+    if (p.lam) cudaFree(p.lam);
+    if (p.part) cudaFree(p.part);
+    p = psd_filter_s::Polar{};
+}
+
 void psd_filter_destroy(psd_filter_t h) {
     if (!h) return;
+    free_polar(h);
     free_peerpath(h);
     free_rowpanel(h);
     free_hostpipe(h);
@@ -1439,6 +1458,60 @@ psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, co
     a.x_out = X_out;
     // no graph cache: sigma and the extra pointers are kernel arguments of every launch
     return run_body(h, C, n, batch, S_out, nullptr, nullptr, false, static_cast<cudaStream_t>(stream), &a);
+}
+
+psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch, float* out,
+                       const double* lambda_in, double* lambda_out, void* stream) {
+    if (!h) return fail(PSD_EINVAL, "null handle");
+    if (!A || !out) return fail(PSD_EINVAL, "null A or out");
+    if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+        return fail(PSD_EINVAL, "A and out must be 16-byte aligned");
+    if (n < 1 || batch < 1) return fail(PSD_EINVAL, "n and batch must be >= 1");
+    if (2 * n > (1 << 20) || batch > (1 << 24) || 4 * n * n * batch > (int64_t(1) << 40))
+        return fail(PSD_EINVAL, "polar problem too large");
+    if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto& p = h->pol;
+    const int64_t N = 2 * n;
+    const int nblk = polar_blocks_per_matrix(static_cast<int>(n), static_cast<int>(batch));
+    if (p.n != n || p.batch < batch) {
+        // stable buffers per (n, batch) -- the sign run on H is graph-cached on these pointers
+        free_graphs(h);
+        free_polar(h);
+        const size_t hb = static_cast<size_t>(batch) * N * N * sizeof(float);
+        if (cudaMalloc(&p.H, hb) != cudaSuccess || cudaMalloc(&p.S, hb) != cudaSuccess ||
+            cudaMalloc(&p.lam, batch * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&p.part, static_cast<size_t>(batch) * 512 * sizeof(double)) != cudaSuccess) {
+            free_polar(h);
+            return fail(PSD_ENOMEM, "cudaMalloc polar workspace failed");
+        }
+        p.n = n;
+        p.batch = batch;
+    }
+    // the product workspace of n' = 2n (its status word receives the non-finite flag of the norm)
+    psd_status_t rc = ensure_ws(h, static_cast<int>(padded_n(N, batch)), static_cast<int>(batch));
+    if (rc != PSD_OK) return rc;
+    cudaError_t e = launch_polar_embed(A, static_cast<int>(n), static_cast<int>(batch), p.H, p.part, nblk, st);
+    if (e != cudaSuccess) return cuda_fail(e, "polar_embed");
+    h->kernel_launches += 1;
+    const psd_bound_t bound = h->bound;
+    if (bound == PSD_BOUND_FROBENIUS) {
+        // lambda~ = ||A||_F (the Frobenius bound of A; ||H||_F would be sqrt(2) looser)
+        e = launch_finalize_bound(p.part, nblk, static_cast<int>(batch), p.lam, nullptr, h->ws.status, st);
+        if (e != cudaSuccess) return cuda_fail(e, "polar norm");
+        h->kernel_launches += 1;
+        h->bound = PSD_BOUND_USER;
+        rc = run(h, p.H, N, batch, p.S, p.lam, lambda_out, true, st);
+        h->bound = bound;
+    } else {
+        // USER: the caller's bound; LANCZOS: the Theorem-2 bound of H (||H||_2 = ||A||_2)
+        rc = run(h, p.H, N, batch, p.S, bound == PSD_BOUND_USER ? lambda_in : nullptr, lambda_out, true, st);
+    }
+    if (rc != PSD_OK) return rc;
+    e = launch_polar_extract(p.S, static_cast<int>(n), static_cast<int>(batch), out, st);
+    if (e != cudaSuccess) return cuda_fail(e, "polar_extract");
+    h->kernel_launches += 1;
+    return PSD_OK;
 }
 
 psd_status_t psd_filter_certificate(psd_filter_t h, double* sign_err, double* relu_err, double* sign_argmax,

@@ -40,6 +40,18 @@ def goe(n, seed):
     return _f32(0.5 * (A + A.T))
 
 
+def ginibre(n, seed):
+    """A general (nonsymmetric) square Gaussian matrix: the input of the polar path (psd_polar)."""
+    return _f32(rng(seed + 31337).standard_normal((n, n)))
+
+
+def svd_known(n, seed, sigma):
+    """A = W diag(sigma) V^T with Haar W, V: a general matrix whose polar factor W V^T is known."""
+    W = haar_orthogonal(n, seed)
+    V = haar_orthogonal(n, seed + 1)
+    return _f32((W * np.asarray(sigma)) @ V.T), W, V
+
+
 def haar_orthogonal(n, seed):
     g = rng(seed).standard_normal((n, n))
     Q, R = np.linalg.qr(g)
