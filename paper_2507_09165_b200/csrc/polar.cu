@@ -7,9 +7,11 @@
 // filter's polar iterate f_T o ... o f_1 (A / lambda~).  psd_polar therefore writes the upper
 // triangle of H (the sign path reads only the upper triangle, R10), computes lambda~ = ||A||_F
 // (>= ||A||_2 = ||H||_2; deterministic fp64 partials), runs psd_sign on H with that bound and copies
-// the top-right block out.  Cost: the chain runs on 2n (about 6x the flops of a direct
-// nonsymmetric chain, which needs general-output and Gram-product modes in the product kernels:
-// DESIGN.md, next).
+// the top-right block out.  H's structure is exploited in the product loop (psd_api.cu, R25): every
+// iterate is block off-diagonal and Y, U block diagonal, so each product runs only over its nonzero
+// block (Y, U: the bottom-right block = the A^T A side; Z': the top-right block) and its nonzero K
+// half -- the flops of a direct nonsymmetric chain.  A is zero-padded to m = a multiple of 128 so the
+// block boundary is a tile boundary (zero singular values map to 0).
 #include <cstdint>
 
 #include "kernels.h"
@@ -26,25 +28,28 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-// Block k of matrix b: rows [k * rows_per, ...) of A.  H row i (< n): [0 .. n) zeros, [n .. 2n) = A row i;
-// H row n + i: [n .. 2n) zeros (the lower-left block is never read).  partial[b][k] = sum of a^2 over the
-// block's rows (fp64, fixed order).
+// H = [[0, A'], [A'^T, 0]] of edge 2m, A' = A zero-padded to m x m (m >= n, a multiple of the tile edge:
+// the block boundary falls on a tile boundary).  Block k of matrix b covers rows [k * rows_per, ...) of
+// the top half: H row i < m gets zeros in [0, m) and A row i (zero-extended) in [m, 2m); H row m + i
+// gets zeros in [m, 2m) (the lower-left block is never read).  partial[b][k] = sum of a^2 (fp64, fixed
+// order).
 __global__ void __launch_bounds__(kPolarThreads)
-polar_embed_kernel(const float* __restrict__ A, int n, int rows_per, float* __restrict__ H, double* __restrict__ partial) {
+polar_embed_kernel(const float* __restrict__ A, int n, int m, int rows_per, float* __restrict__ H,
+                   double* __restrict__ partial) {
     const int b = blockIdx.y, k = blockIdx.x;
-    const int64_t N = 2 * static_cast<int64_t>(n);
+    const int64_t N = 2 * static_cast<int64_t>(m);
     const float* Ab = A + static_cast<int64_t>(b) * n * n;
     float* Hb = H + static_cast<int64_t>(b) * N * N;
-    const int r0 = k * rows_per, r1 = min(n, r0 + rows_per);
+    const int r0 = k * rows_per, r1 = min(m, r0 + rows_per);
     double s = 0.0;
     for (int i = r0; i < r1; ++i) {
         const float* arow = Ab + static_cast<int64_t>(i) * n;
         float* top = Hb + static_cast<int64_t>(i) * N;
-        float* bot = Hb + (static_cast<int64_t>(n) + i) * N + n;
-        for (int j = threadIdx.x; j < n; j += kPolarThreads) {
-            const float a = arow[j];
+        float* bot = Hb + (static_cast<int64_t>(m) + i) * N + m;
+        for (int j = threadIdx.x; j < m; j += kPolarThreads) {
+            const float a = (i < n && j < n) ? arow[j] : 0.0f;
             s = fma(static_cast<double>(a), static_cast<double>(a), s);
-            top[n + j] = a;
+            top[m + j] = a;
             top[j] = 0.0f;
             bot[j] = 0.0f;
         }
@@ -60,14 +65,14 @@ polar_embed_kernel(const float* __restrict__ A, int n, int rows_per, float* __re
     }
 }
 
-// out[b][i][j] = S[b][i][n + j]: one block per output row (blockIdx.x = b * n + i), float4 when rows
-// are 16-byte aligned
+// out[b][i][j] = S[b][i][m + j] for i, j < n: one block per output row (blockIdx.x = b * n + i), float4
+// when rows are 16-byte aligned
 __global__ void __launch_bounds__(kPolarThreads)
-polar_extract_kernel(const float* __restrict__ S, int n, float* __restrict__ out) {
-    const int64_t N = 2 * static_cast<int64_t>(n);
+polar_extract_kernel(const float* __restrict__ S, int n, int m, float* __restrict__ out) {
+    const int64_t N = 2 * static_cast<int64_t>(m);
     const int64_t row = blockIdx.x;                       // b * n + i
     const int64_t b = row / n, i = row - b * n;
-    const float* src = S + b * N * N + i * N + n;
+    const float* src = S + b * N * N + i * N + m;
     float* dst = out + row * n;
     if ((n & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(src);
@@ -80,23 +85,24 @@ polar_extract_kernel(const float* __restrict__ S, int n, float* __restrict__ out
 
 }  // namespace
 
-int polar_blocks_per_matrix(int n, int batch) {
-    int k = (n + 7) / 8;                                  // ~8 rows per block
+int polar_blocks_per_matrix(int m, int batch) {
+    int k = (m + 7) / 8;                                  // ~8 rows per block
     const int fill = (4 * 148 + batch - 1) / batch;      // a few blocks per SM over the batch
     if (k < fill) k = fill;
-    if (k > n) k = n;
+    if (k > m) k = m;
     return k < 1 ? 1 : (k > 512 ? 512 : k);
 }
 
-cudaError_t launch_polar_embed(const float* A, int n, int batch, float* H, double* partial, int nblk,
+cudaError_t launch_polar_embed(const float* A, int n, int m, int batch, float* H, double* partial, int nblk,
                                cudaStream_t stream) {
-    const int rows_per = (n + nblk - 1) / nblk;
-    polar_embed_kernel<<<dim3(nblk, batch), kPolarThreads, 0, stream>>>(A, n, rows_per, H, partial);
+    const int rows_per = (m + nblk - 1) / nblk;
+    polar_embed_kernel<<<dim3(nblk, batch), kPolarThreads, 0, stream>>>(A, n, m, rows_per, H, partial);
     return cudaGetLastError();
 }
 
-cudaError_t launch_polar_extract(const float* S, int n, int batch, float* out, cudaStream_t stream) {
-    polar_extract_kernel<<<static_cast<unsigned>(static_cast<int64_t>(batch) * n), kPolarThreads, 0, stream>>>(S, n, out);
+cudaError_t launch_polar_extract(const float* S, int n, int m, int batch, float* out, cudaStream_t stream) {
+    polar_extract_kernel<<<static_cast<unsigned>(static_cast<int64_t>(batch) * n), kPolarThreads, 0, stream>>>(S, n, m,
+                                                                                                            out);
     return cudaGetLastError();
 }
 

@@ -157,6 +157,9 @@ struct psd_filter_s {
     int64_t product_launches_profiled = 0;
     int64_t kernel_launches = 0;
     int64_t last_products = 0;     // product-carrying launches of the last run_body (graph accounting)
+    // psd_polar in progress: the block edge m of H = [[0, A], [A^T, 0]] (2m x 2m); the product loop
+    // then restricts every product to its nonzero block and K range (GemmShape::sub_mode, R25)
+    int polar_m = 0;
     // psd_polar: the 2n x 2n embedding H, the sign output on it, lambda~ and the norm partials
     struct Polar {
         float* H = nullptr;
@@ -591,7 +594,9 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         if (e != cudaSuccess) return cuda_fail(e, "Lanczos bound");
         h->kernel_launches += 1 + lanczos_launches(h->lz_steps, n);
     }
-    const bool bn64 = !(npad % 256 == 0 && use_pair_kernel(n, batch)) && sym_gemm_bn(npad, batch) == 64;
+    // psd_polar's block-restricted products run on the 1-CTA kernel (tile sub-blocks, K ranges)
+    const bool pair_ok = npad % 256 == 0 && use_pair_kernel(n, batch) && h->polar_m == 0;
+    const bool bn64 = !pair_ok && sym_gemm_bn(npad, batch) == 64;
     const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     auto maps = [&](int A, int B) {
         OperandMaps m;
@@ -624,7 +629,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     } else if (h->capturing && h->cap_ev[0] && !steps.empty()) {
         cudaEventRecordWithFlags(h->cap_ev[0], st, cudaEventRecordExternal);
     }
-    const bool pair = npad % 256 == 0 && use_pair_kernel(n, batch);
+    const bool pair = pair_ok;
     // the chain's operand copies hold only their upper tiles (16-bit operands)
     const bool upper_only = upper_only_mode(h, n, batch, npad);
     shape.upper_only = upper_only ? 1 : 0;
@@ -666,6 +671,26 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     for (size_t si = 0; si < steps.size(); ++si) {
         const Step& s = steps[si];
         shape.counter = ws.counters + si;
+        if (h->polar_m) {
+            // H = [[0, A], [A^T, 0]]: every iterate is block off-diagonal, Y = Z Z and the Horner
+            // products block diagonal; only the bottom-right block of Y / U (Z^T Z side) and the
+            // top-right block of Z' are needed, each over the one nonzero K half
+            const int m = h->polar_m;
+            if (s.out_op == B_Y && s.A == s.B) {          // Y_BR = Z_BL Z_TR: K in [0, m)
+                shape.sub_mode = 1;
+                shape.k_begin = 0;
+                shape.k_end = m;
+            } else if (s.out_op == B_UA || s.out_op == B_UB) {   // U_BR: K in [m, 2m)
+                shape.sub_mode = 1;
+                shape.k_begin = m;
+                shape.k_end = 2 * m;
+            } else {                                      // Z'_TR = c0 Z_TR + Z_TR (U or Y)_BR
+                shape.sub_mode = 2;
+                shape.k_begin = m;
+                shape.k_end = 2 * m;
+            }
+            shape.sub_m = m;
+        }
         EpiParams ep = make_ep(s);
         const bool dbg = pair && !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
         if (dbg) {
@@ -1472,8 +1497,9 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto& p = h->pol;
-    const int64_t N = 2 * n;
-    const int nblk = polar_blocks_per_matrix(static_cast<int>(n), static_cast<int>(batch));
+    const int64_t m = (n + kTile - 1) / kTile * kTile;      // block edge: a tile boundary
+    const int64_t N = 2 * m;
+    const int nblk = polar_blocks_per_matrix(static_cast<int>(m), static_cast<int>(batch));
     if (p.n != n || p.batch < batch) {
         // stable buffers per (n, batch) -- the sign run on H is graph-cached on these pointers
         free_graphs(h);
@@ -1488,17 +1514,22 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
         p.n = n;
         p.batch = batch;
     }
-    // the product workspace of n' = 2n (its status word receives the non-finite flag of the norm)
+    // the product workspace of n' = 2m (its status word receives the non-finite flag of the norm)
     psd_status_t rc = ensure_ws(h, static_cast<int>(padded_n(N, batch)), static_cast<int>(batch));
     if (rc != PSD_OK) return rc;
-    cudaError_t e = launch_polar_embed(A, static_cast<int>(n), static_cast<int>(batch), p.H, p.part, nblk, st);
+    cudaError_t e = launch_polar_embed(A, static_cast<int>(n), static_cast<int>(m), static_cast<int>(batch), p.H, p.part,
+                                       nblk, st);
     if (e != cudaSuccess) return cuda_fail(e, "polar_embed");
     h->kernel_launches += 1;
     const psd_bound_t bound = h->bound;
+    h->polar_m = static_cast<int>(m);
     if (bound == PSD_BOUND_FROBENIUS) {
         // lambda~ = ||A||_F (the Frobenius bound of A; ||H||_F would be sqrt(2) looser)
         e = launch_finalize_bound(p.part, nblk, static_cast<int>(batch), p.lam, nullptr, h->ws.status, st);
-        if (e != cudaSuccess) return cuda_fail(e, "polar norm");
+        if (e != cudaSuccess) {
+            h->polar_m = 0;
+            return cuda_fail(e, "polar norm");
+        }
         h->kernel_launches += 1;
         h->bound = PSD_BOUND_USER;
         rc = run(h, p.H, N, batch, p.S, p.lam, lambda_out, true, st);
@@ -1507,8 +1538,9 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
         // USER: the caller's bound; LANCZOS: the Theorem-2 bound of H (||H||_2 = ||A||_2)
         rc = run(h, p.H, N, batch, p.S, bound == PSD_BOUND_USER ? lambda_in : nullptr, lambda_out, true, st);
     }
+    h->polar_m = 0;
     if (rc != PSD_OK) return rc;
-    e = launch_polar_extract(p.S, static_cast<int>(n), static_cast<int>(batch), out, st);
+    e = launch_polar_extract(p.S, static_cast<int>(n), static_cast<int>(m), static_cast<int>(batch), out, st);
     if (e != cudaSuccess) return cuda_fail(e, "polar_extract");
     h->kernel_launches += 1;
     return PSD_OK;

@@ -77,6 +77,22 @@ __device__ __forceinline__ void upper_tile_coords(int t, int npad, int& I, int& 
     J = i * r + rem;
 }
 
+// Tile t of this launch (GemmShape::sub_mode) -> (I, J) in 128-row / BN-column units of the npad matrix
+template <int BN>
+__device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& I, int& J) {
+    if (s.sub_mode == 0) {
+        upper_tile_coords<BN>(t, s.npad, I, J);
+    } else if (s.sub_mode == 1) {                  // upper tiles of the bottom-right sub_m block
+        upper_tile_coords<BN>(t, s.sub_m, I, J);
+        I += s.sub_m / kTile;
+        J += s.sub_m / BN;
+    } else {                                       // every tile of the top-right sub_m block
+        const int ncb = s.sub_m / BN;
+        I = t / ncb;
+        J = ncb + t % ncb;
+    }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -137,7 +153,7 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     const int b = blockIdx.y;
     const int krank = (KS > 1) ? static_cast<int>(ptx::cluster_ctarank()) : 0;
     int I, J;
-    upper_tile_coords<BN>(blockIdx.x / KS, s.npad, I, J);
+    tile_coords<BN>(s, blockIdx.x / KS, I, J);
     DBG_STAMP(0);
     DBG_ALL(0);
 
@@ -171,12 +187,14 @@ sym_gemm_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, const
     DBG_STAMP(2);
     DBG_ALL(1);
 
-    const int num_kb = s.npad / kBK / KS;             // this CTA's K slice
-    const int kb0 = krank * num_kb;
+    const int kbeg = s.k_begin / kBK;                 // K range (whole npad unless sub_mode products)
+    const int kend = (s.k_end > 0 ? s.k_end : s.npad) / kBK;
+    const int num_kb = (kend - kbeg) / KS;            // this CTA's K slice
+    const int kb0 = kbeg + krank * num_kb;
     const int rowA = b * s.npad + I * kTile;
     const int rowB = b * s.npad + J * BN;
     int nruns = 1;
-    if (kRuns && s.kchunk > 0) nruns = min(static_cast<int>(kCols / BN), (s.npad + s.kchunk - 1) / s.kchunk);
+    if (kRuns && s.kchunk > 0) nruns = min(static_cast<int>(kCols / BN), ((kend - kbeg) * kBK + s.kchunk - 1) / s.kchunk);
     const int run_kb = (num_kb + nruns - 1) / nruns;    // K blocks per accumulation run
     nruns = (num_kb + run_kb - 1) / run_kb;
 
@@ -433,8 +451,9 @@ cudaError_t launch_t(const OperandMaps& m, const GemmShape& s, const EpiParams& 
         if (err != cudaSuccess) return err;
         attr_set = true;
     }
-    const int nrb = s.npad / kTile, ncb = s.npad / BN;
-    const int tiles = nrb * ncb - (kTile / BN) * nrb * (nrb - 1) / 2;
+    const int edge = s.sub_mode ? s.sub_m : s.npad;
+    const int nrb = edge / kTile, ncb = edge / BN;
+    const int tiles = s.sub_mode == 2 ? nrb * ncb : nrb * ncb - (kTile / BN) * nrb * (nrb - 1) / 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(tiles * KS, s.batch);
     cfg.blockDim = dim3(kThreads);
@@ -503,7 +522,7 @@ int sym_gemm_bn(int npad, int batch) {
 
 cudaError_t launch_sym_gemm(OpType t, bool split, const OperandMaps& m, const GemmShape& s, const EpiParams& e,
                             cudaStream_t stream) {
-    const int ks = sym_gemm_split_k(s.npad, s.batch, t, split, s.kchunk);
+    const int ks = s.sub_mode ? 1 : sym_gemm_split_k(s.npad, s.batch, t, split, s.kchunk);
     const int bn = sym_gemm_bn(s.npad, s.batch);
     switch (t) {
         case OpType::F16: return split ? launch_ks<OpType::F16, true>(ks, bn, m, s, e, stream)

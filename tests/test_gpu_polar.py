@@ -37,14 +37,14 @@ def _run(pkg, A, prec, bound="frobenius", lam_in=None):
 
 
 @pytest.mark.parametrize("n,batch,prec", [
-    (40, 3, "fp16"),        # 2n = 80: the 1-CTA kernel, ragged padding
+    (40, 3, "fp16"),        # A zero-padded to m = 128 (H is 256 x 256)
     (100, 2, "fp16"),
-    (257, 1, "bf16"),
+    (257, 1, "bf16"),       # m = 384: three 128-tile rows per block
     (300, 2, "tf32"),
     (160, 2, "fp16x3"),     # FP32-class
-    (512, 2, "fp16"),       # 2n = 1024: the K-half runs of the 1-CTA kernel
-    (512, 1, "tf32x3"),     # 2n = 1024, batch 1: cluster split-K
-    (2048, 2, "fp16"),      # 2n = 4096: the CTA-pair kernel
+    (512, 2, "fp16"),       # m = 512: 128 x 64 tiles (few-tile BN) in both block modes
+    (512, 1, "tf32x3"),     # FP32-class with a K range of one accumulation run
+    (2048, 2, "fp16"),      # m = 2048: 128 x 128 tiles, K ranges of 2048
 ])
 def test_polar_parity(pkg, n, batch, prec):
     A = np.stack([synth.ginibre(n, 7 * n + b) for b in range(batch)])
@@ -97,3 +97,17 @@ def test_polar_zero_nonfinite_and_user_bound(pkg):
     assert lam[0] == lam_user[0]
     ref, _ = polar.polar(A[0], *HALF, lam=float(lam_user[0]))
     assert np.linalg.norm(U[0] - ref) / np.linalg.norm(ref) < TOL["fp16"]
+
+
+def test_polar_lanczos_bound(pkg):
+    """PSD_BOUND_LANCZOS: the Theorem-2 bound of H (||H||_2 = ||A||_2) -- a valid bound, tighter than
+    ||A||_F, and the output is the oracle's polar iterate with that lambda~."""
+    A = np.stack([synth.ginibre(300, 21 + b) for b in range(2)])
+    U, lam, f = _run(pkg, A, "fp16", bound="lanczos")
+    assert f.status() == "PSD_OK"
+    for b in range(2):
+        s_max = np.linalg.norm(A[b], 2)
+        assert s_max <= lam[b] <= polar.frobenius(A[b]) * (1 + 1e-12)
+        assert lam[b] < 0.5 * polar.frobenius(A[b])                 # ~2 sigma_max / ||A||_F for Ginibre
+        ref, _ = polar.polar(A[b], *HALF, lam=float(lam[b]))
+        assert np.linalg.norm(U[b] - ref) / np.linalg.norm(ref) < TOL["fp16"]
