@@ -163,20 +163,27 @@ psd_status_t psd_project_ex(psd_filter_t h, const float* X, int64_t n, int64_t b
  *     out[b] = W diag(s(sigma / lambda~)) V^T = f_T o ... o f_1 (A[b] / lambda~),
  *     f_t(Z) = sum_j c_{t,j} Z (Z^T Z)^j,
  * which approaches the orthogonal polar factor W V^T for singular values in [eps, 1] * lambda~.
- * Computed through the symmetric path: the upper triangle of H = [[0, A], [A^T, 0]] (2n x 2n) is
- * written to a handle-owned workspace, psd_sign runs on H (f(H) = [[0, f(A)], [f(A)^T, 0]]), and
- * the top-right block is copied to `out` -- every step in this library's kernels, about 6x the
- * flops of a direct nonsymmetric chain.
+ * Computed through the symmetric path: the upper triangle of H = [[0, A'], [A'^T, 0]] (2m x 2m, A'
+ * = A zero-padded to m = n rounded up to 128) is written to a handle-owned workspace and the sign
+ * chain runs on H (f(H) = [[0, f(A')], [f(A')^T, 0]]) with every product restricted to its nonzero
+ * block and K half -- the Gram product Z^T Z, the Horner products and the general product Z U of a
+ * direct nonsymmetric chain (reading R25); the top-right block is copied to `out`.
  *   A, out : device, batch x n x n fp32 row-major (all of A is read; out fully written; out == A
  *            allowed), 16-byte aligned.
  *   lambda~: ||A||_F (>= ||A||_2 = ||H||_2; fp64, deterministic) with PSD_BOUND_FROBENIUS, the
  *            Lanczos/Theorem-2 bound of H with PSD_BOUND_LANCZOS, lambda_in with PSD_BOUND_USER.
  *   lambda_in  device, `batch` doubles, used iff the bound is PSD_BOUND_USER (else may be NULL).
  *   lambda_out device, `batch` doubles receiving the lambda~ used; may be NULL.
- * Workspace: 2 x batch x (2n)^2 fp32 beside the product workspace of n' = 2n.  Non-finite input
+ * Workspace: 2 x batch x (2m)^2 fp32 (m = n rounded up to 128) beside the product workspace of n' = 2m.  Non-finite input
  * sets PSD_ENONFINITE (psd_status).  Errors: PSD_EINVAL for NULL pointers, n < 1, batch < 1. */
 psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch, float* out,
                        const double* lambda_in, double* lambda_out, void* stream);
+
+/* psd_polar for a rectangular rows x cols A (batch x rows x cols fp32 in and out): the same
+ * iterate f(A) = sum_j c_j A (A^T A)^j per stage; A is zero-padded to a square edge (zero singular
+ * values map to 0).  psd_polar(h, A, n, ...) is psd_polar_rect(h, A, n, n, ...). */
+psd_status_t psd_polar_rect(psd_filter_t h, const float* A, int64_t rows, int64_t cols, int64_t batch,
+                            float* out, const double* lambda_in, double* lambda_out, void* stream);
 
 /* One fused S- and X-update of the three-step ADMM for the SDP pair of Eq. (exp:sdp)
  * (Eq. exp:admm-three-step), for diagonal constraint operators (max-cut:

@@ -133,24 +133,30 @@ class Filter:
         return self._run(X, out, lambda_in, lambda_out, True, stream)
 
     def polar(self, A, out=None, lambda_in=None, lambda_out=None, stream=None):
-        """The filter's polar iterate of a general square A: f_T o ... o f_1 (A / lambda~) with
-        f_t(Z) = sum_j c_j Z (Z^T Z)^j, i.e. W diag(s(sigma / lambda~)) V^T for A = W diag(sigma) V^T
-        (psd_polar; all of A is read)."""
+        """The filter's polar iterate of a general (rows, cols) or (batch, rows, cols) A:
+        f_T o ... o f_1 (A / lambda~) with f_t(Z) = sum_j c_j Z (Z^T Z)^j, i.e. W diag(s(sigma / lambda~)) V^T
+        for A = W diag(sigma) V^T (psd_polar_rect; all of A is read)."""
         import torch
-        Ab = _check_matrix(A)
+        if not isinstance(A, torch.Tensor) or not A.is_cuda or A.dtype != torch.float32:
+            raise TypeError("A must be a float32 CUDA tensor")
+        if A.dim() not in (2, 3):
+            raise ValueError("A must be (rows, cols) or (batch, rows, cols)")
+        Ab = A.unsqueeze(0) if A.dim() == 2 else A
+        if not Ab.is_contiguous():
+            raise ValueError("A must be contiguous")
         out = torch.empty_like(A) if out is None else out
-        outb = _check_matrix(out)
-        if outb.shape != Ab.shape:
-            raise ValueError("out shape mismatch")
-        B, n = Ab.shape[0], Ab.shape[-1]
+        if not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or not out.is_cuda or \
+                out.shape != A.shape or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float32 CUDA tensor shaped like A")
+        B, rows, cols = Ab.shape
         for name, lam in (("lambda_in", lambda_in), ("lambda_out", lambda_out)):
             if lam is not None and not (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64
                                         and lam.is_contiguous() and lam.numel() == B):
                 raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of batch elements")
         li = ctypes.c_void_p(lambda_in.data_ptr()) if lambda_in is not None else None
         lo = ctypes.c_void_p(lambda_out.data_ptr()) if lambda_out is not None else None
-        check(self._lib.psd_polar(self._h, ctypes.c_void_p(Ab.data_ptr()), n, B, ctypes.c_void_p(outb.data_ptr()),
-                                  li, lo, _stream_ptr(stream)), "psd_polar")
+        check(self._lib.psd_polar_rect(self._h, ctypes.c_void_p(Ab.data_ptr()), rows, cols, B,
+                                       ctypes.c_void_p(out.data_ptr()), li, lo, _stream_ptr(stream)), "psd_polar_rect")
         return out
 
     def admm_update(self, C, Xk, y, sigma, S_out=None, X_out=None, stream=None):

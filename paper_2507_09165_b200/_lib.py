@@ -35,6 +35,8 @@ SIGNATURES = [
     ("psd_sign", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p]),
     ("psd_polar", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p,
                              _c.c_void_p, _c.c_void_p]),
+    ("psd_polar_rect", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int64, _c.c_void_p,
+                                  _c.c_void_p, _c.c_void_p, _c.c_void_p]),
     ("psd_project_ex", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p,
                                   _c.c_void_p, _c.c_int, _c.c_void_p]),
     ("psd_admm_update", _c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_void_p, _c.c_double, _c.c_int64,

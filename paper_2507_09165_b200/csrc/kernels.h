@@ -99,8 +99,8 @@ struct GemmShape {
     // round-to-nearest fp32 adds in the epilogue warps.  0: one accumulation over the whole K.
     int kchunk;
     // 1-CTA kernel only (psd_polar's block-structured products on H = [[0, A], [A^T, 0]], R25):
-    // sub_mode 0 = the upper tiles of the whole npad matrix; 1 = the upper tiles of the sub_m x sub_m
-    // bottom-right block; 2 = every tile of the sub_m x sub_m top-right block.  K runs over
+    // sub_mode 0 = the upper tiles of the whole npad matrix; 1 / 3 = the upper tiles of the sub_m x sub_m
+    // bottom-right / top-left block; 2 = every tile of the sub_m x sub_m top-right block.  K runs over
     // [k_begin, k_end) (k_end 0: npad).  Zero-initialised = the symmetric product.
     int sub_mode;
     int sub_m;
@@ -185,9 +185,9 @@ int bound_blocks_per_matrix(int n, int batch);
 // per-block fp64 partial sums of a^2 (finalised by launch_finalize_bound into lambda~ = ||A||_F),
 // and the top-right n x n block of the 2n x 2n sign output
 int polar_blocks_per_matrix(int m, int batch);
-cudaError_t launch_polar_embed(const float* A, int n, int m, int batch, float* H, double* partial, int nblk,
-                               cudaStream_t stream);
-cudaError_t launch_polar_extract(const float* S, int n, int m, int batch, float* out, cudaStream_t stream);
+cudaError_t launch_polar_embed(const float* A, int rows, int cols, int m, int batch, float* H, double* partial,
+                               int nblk, cudaStream_t stream);
+cudaError_t launch_polar_extract(const float* S, int rows, int cols, int m, int batch, float* out, cudaStream_t stream);
 cudaError_t launch_frobenius_partials(const float* X, int n, int batch, double* partial, int nblk,
                                       cudaStream_t stream, const InputForm& form = InputForm());
 

@@ -11,7 +11,8 @@
 // iterate is block off-diagonal and Y, U block diagonal, so each product runs only over its nonzero
 // block (Y, U: the bottom-right block = the A^T A side; Z': the top-right block) and its nonzero K
 // half -- the flops of a direct nonsymmetric chain.  A is zero-padded to m = a multiple of 128 so the
-// block boundary is a tile boundary (zero singular values map to 0).
+// block boundary is a tile boundary (zero singular values map to 0); a rectangular rows x cols A is
+// padded the same way (f(A) = A q(A^T A) is rows x cols).
 #include <cstdint>
 
 #include "kernels.h"
@@ -34,20 +35,20 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // gets zeros in [m, 2m) (the lower-left block is never read).  partial[b][k] = sum of a^2 (fp64, fixed
 // order).
 __global__ void __launch_bounds__(kPolarThreads)
-polar_embed_kernel(const float* __restrict__ A, int n, int m, int rows_per, float* __restrict__ H,
+polar_embed_kernel(const float* __restrict__ A, int rows, int cols, int m, int rows_per, float* __restrict__ H,
                    double* __restrict__ partial) {
     const int b = blockIdx.y, k = blockIdx.x;
     const int64_t N = 2 * static_cast<int64_t>(m);
-    const float* Ab = A + static_cast<int64_t>(b) * n * n;
+    const float* Ab = A + static_cast<int64_t>(b) * rows * cols;
     float* Hb = H + static_cast<int64_t>(b) * N * N;
     const int r0 = k * rows_per, r1 = min(m, r0 + rows_per);
     double s = 0.0;
     for (int i = r0; i < r1; ++i) {
-        const float* arow = Ab + static_cast<int64_t>(i) * n;
+        const float* arow = Ab + static_cast<int64_t>(i) * cols;
         float* top = Hb + static_cast<int64_t>(i) * N;
         float* bot = Hb + (static_cast<int64_t>(m) + i) * N + m;
         for (int j = threadIdx.x; j < m; j += kPolarThreads) {
-            const float a = (i < n && j < n) ? arow[j] : 0.0f;
+            const float a = (i < rows && j < cols) ? arow[j] : 0.0f;
             s = fma(static_cast<double>(a), static_cast<double>(a), s);
             top[m + j] = a;
             top[j] = 0.0f;
@@ -65,21 +66,21 @@ polar_embed_kernel(const float* __restrict__ A, int n, int m, int rows_per, floa
     }
 }
 
-// out[b][i][j] = S[b][i][m + j] for i, j < n: one block per output row (blockIdx.x = b * n + i), float4
-// when rows are 16-byte aligned
+// out[b][i][j] = S[b][i][m + j] for i < rows, j < cols: one block per output row (blockIdx.x =
+// b * rows + i), float4 when rows are 16-byte aligned
 __global__ void __launch_bounds__(kPolarThreads)
-polar_extract_kernel(const float* __restrict__ S, int n, int m, float* __restrict__ out) {
+polar_extract_kernel(const float* __restrict__ S, int rows, int cols, int m, float* __restrict__ out) {
     const int64_t N = 2 * static_cast<int64_t>(m);
-    const int64_t row = blockIdx.x;                       // b * n + i
-    const int64_t b = row / n, i = row - b * n;
+    const int64_t row = blockIdx.x;                       // b * rows + i
+    const int64_t b = row / rows, i = row - b * rows;
     const float* src = S + b * N * N + i * N + m;
-    float* dst = out + row * n;
-    if ((n & 3) == 0) {
+    float* dst = out + row * cols;
+    if ((cols & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(src);
         float4* d4 = reinterpret_cast<float4*>(dst);
-        for (int j = threadIdx.x; j < n / 4; j += kPolarThreads) d4[j] = s4[j];
+        for (int j = threadIdx.x; j < cols / 4; j += kPolarThreads) d4[j] = s4[j];
     } else {
-        for (int j = threadIdx.x; j < n; j += kPolarThreads) dst[j] = src[j];
+        for (int j = threadIdx.x; j < cols; j += kPolarThreads) dst[j] = src[j];
     }
 }
 
@@ -93,16 +94,16 @@ int polar_blocks_per_matrix(int m, int batch) {
     return k < 1 ? 1 : (k > 512 ? 512 : k);
 }
 
-cudaError_t launch_polar_embed(const float* A, int n, int m, int batch, float* H, double* partial, int nblk,
-                               cudaStream_t stream) {
+cudaError_t launch_polar_embed(const float* A, int rows, int cols, int m, int batch, float* H, double* partial,
+                               int nblk, cudaStream_t stream) {
     const int rows_per = (m + nblk - 1) / nblk;
-    polar_embed_kernel<<<dim3(nblk, batch), kPolarThreads, 0, stream>>>(A, n, m, rows_per, H, partial);
+    polar_embed_kernel<<<dim3(nblk, batch), kPolarThreads, 0, stream>>>(A, rows, cols, m, rows_per, H, partial);
     return cudaGetLastError();
 }
 
-cudaError_t launch_polar_extract(const float* S, int n, int m, int batch, float* out, cudaStream_t stream) {
-    polar_extract_kernel<<<static_cast<unsigned>(static_cast<int64_t>(batch) * n), kPolarThreads, 0, stream>>>(S, n, m,
-                                                                                                            out);
+cudaError_t launch_polar_extract(const float* S, int rows, int cols, int m, int batch, float* out, cudaStream_t stream) {
+    polar_extract_kernel<<<static_cast<unsigned>(static_cast<int64_t>(batch) * rows), kPolarThreads, 0, stream>>>(
+        S, rows, cols, m, out);
     return cudaGetLastError();
 }
 

@@ -160,6 +160,7 @@ struct psd_filter_s {
     // psd_polar in progress: the block edge m of H = [[0, A], [A^T, 0]] (2m x 2m); the product loop
     // then restricts every product to its nonzero block and K range (GemmShape::sub_mode, R25)
     int polar_m = 0;
+    bool polar_wide = false;       // rows < cols: the Gram products on the A A^T side (top-left block)
     // psd_polar: the 2n x 2n embedding H, the sign output on it, lambda~ and the norm partials
     struct Polar {
         float* H = nullptr;
@@ -167,6 +168,7 @@ struct psd_filter_s {
         double* lam = nullptr;
         double* part = nullptr;
         int64_t n = 0, batch = 0;
+        bool wide = false;         // the plan the cached graphs on H were captured with
     } pol;
 };
 
@@ -671,23 +673,28 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     for (size_t si = 0; si < steps.size(); ++si) {
         const Step& s = steps[si];
         shape.counter = ws.counters + si;
+        Step sw = steps[si];
         if (h->polar_m) {
             // H = [[0, A], [A^T, 0]]: every iterate is block off-diagonal, Y = Z Z and the Horner
-            // products block diagonal; only the bottom-right block of Y / U (Z^T Z side) and the
-            // top-right block of Z' are needed, each over the one nonzero K half
+            // products block diagonal; only one diagonal block of Y / U -- the Gram side of the
+            // smaller dimension: A^T A (bottom-right) for rows >= cols, A A^T (top-left) for wide A,
+            // whose other side is numerically rank-deficient -- and the top-right block of Z' are
+            // needed, each over the one nonzero K half
             const int m = h->polar_m;
-            if (s.out_op == B_Y && s.A == s.B) {          // Y_BR = Z_BL Z_TR: K in [0, m)
-                shape.sub_mode = 1;
-                shape.k_begin = 0;
-                shape.k_end = m;
-            } else if (s.out_op == B_UA || s.out_op == B_UB) {   // U_BR: K in [m, 2m)
-                shape.sub_mode = 1;
-                shape.k_begin = m;
-                shape.k_end = 2 * m;
-            } else {                                      // Z'_TR = c0 Z_TR + Z_TR (U or Y)_BR
+            const bool wide = h->polar_wide;
+            if (s.out_op == B_Y && s.A == s.B) {          // Y = Z Z: Z_BL Z_TR (K [0, m)) or Z_TR Z_BL (K [m, 2m))
+                shape.sub_mode = wide ? 3 : 1;
+                shape.k_begin = wide ? m : 0;
+                shape.k_end = wide ? 2 * m : m;
+            } else if (s.out_op == B_UA || s.out_op == B_UB) {   // U in the Y block
+                shape.sub_mode = wide ? 3 : 1;
+                shape.k_begin = wide ? 0 : m;
+                shape.k_end = wide ? m : 2 * m;
+            } else {                                      // Z'_TR = c0 Z_TR + Z_TR U_BR  or  + U_TL Z_TR
                 shape.sub_mode = 2;
-                shape.k_begin = m;
-                shape.k_end = 2 * m;
+                shape.k_begin = wide ? 0 : m;
+                shape.k_end = wide ? m : 2 * m;
+                if (wide) std::swap(sw.A, sw.B);          // Z U = U Z (polynomials in H commute)
             }
             shape.sub_m = m;
         }
@@ -710,8 +717,8 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
                 ep.dbg_all = tl_buf;
             }
         }
-        e = pair ? launch_sym_gemm_2cta(ws.op, split, maps(s.A, s.B), shape, ep, st)
-                 : launch_sym_gemm(ws.op, split, maps(s.A, s.B), shape, ep, st);
+        e = pair ? launch_sym_gemm_2cta(ws.op, split, maps(sw.A, sw.B), shape, ep, st)
+                 : launch_sym_gemm(ws.op, split, maps(sw.A, sw.B), shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
         if (tl && tl_buf) {
@@ -1342,6 +1349,20 @@ psd_status_t run_rowpanel_p2p(psd_filter_s* h, const float* X, float* out, bool 
 
 }  // namespace
 
+namespace {
+
+void free_polar(psd_filter_s* h) {
+    auto& p = h->pol;
+    if (p.H || p.S || p.lam || p.part) cudaDeviceSynchronize();
+    if (p.H) cudaFree(p.H);
+    if (p.S) cudaFree(p.S);
+    if (p.lam) cudaFree(p.lam);
+    if (p.part) cudaFree(p.part);
+    p = psd_filter_s::Polar{};
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* psd_version(void) { return "psdfilter 0.1 sm_100a"; }
@@ -1378,16 +1399,6 @@ psd_status_t psd_filter_create(int T, const int* degrees, const double* coeffs, 
     *out = h;
     g_last_error.clear();
     return PSD_OK;
-}
-
-void free_polar(psd_filter_s* h) {
-    auto& p = h->pol;
-    if (p.H || p.S || p.lam || p.part) cudaDeviceSynchronize();
-    if (p.H) cudaFree(p.H);
-    if (p.S) cudaFree(p.S);
-    if (p.lam) cudaFree(p.lam);
-    if (p.part) cudaFree(p.part);
-    p = psd_filter_s::Polar{};
 }
 
 void psd_filter_destroy(psd_filter_t h) {
@@ -1487,11 +1498,17 @@ psd_status_t psd_admm_update(psd_filter_t h, const float* C, const float* Xk, co
 
 psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch, float* out,
                        const double* lambda_in, double* lambda_out, void* stream) {
+    return psd_polar_rect(h, A, n, n, batch, out, lambda_in, lambda_out, stream);
+}
+
+psd_status_t psd_polar_rect(psd_filter_t h, const float* A, int64_t rows, int64_t cols, int64_t batch, float* out,
+                            const double* lambda_in, double* lambda_out, void* stream) {
     if (!h) return fail(PSD_EINVAL, "null handle");
     if (!A || !out) return fail(PSD_EINVAL, "null A or out");
     if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
         return fail(PSD_EINVAL, "A and out must be 16-byte aligned");
-    if (n < 1 || batch < 1) return fail(PSD_EINVAL, "n and batch must be >= 1");
+    if (rows < 1 || cols < 1 || batch < 1) return fail(PSD_EINVAL, "rows, cols and batch must be >= 1");
+    const int64_t n = rows > cols ? rows : cols;
     if (2 * n > (1 << 20) || batch > (1 << 24) || 4 * n * n * batch > (int64_t(1) << 40))
         return fail(PSD_EINVAL, "polar problem too large");
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
@@ -1500,8 +1517,8 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
     const int64_t m = (n + kTile - 1) / kTile * kTile;      // block edge: a tile boundary
     const int64_t N = 2 * m;
     const int nblk = polar_blocks_per_matrix(static_cast<int>(m), static_cast<int>(batch));
-    if (p.n != n || p.batch < batch) {
-        // stable buffers per (n, batch) -- the sign run on H is graph-cached on these pointers
+    if (p.n != m || p.batch < batch) {
+        // stable buffers per (block edge, batch) -- the sign run on H is graph-cached on these pointers
         free_graphs(h);
         free_polar(h);
         const size_t hb = static_cast<size_t>(batch) * N * N * sizeof(float);
@@ -1511,23 +1528,29 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
             free_polar(h);
             return fail(PSD_ENOMEM, "cudaMalloc polar workspace failed");
         }
-        p.n = n;
+        p.n = m;
         p.batch = batch;
+    }
+    if (p.wide != (rows < cols)) {
+        free_graphs(h);            // the cached sign runs on H carry the other Gram side's plan
+        p.wide = rows < cols;
     }
     // the product workspace of n' = 2m (its status word receives the non-finite flag of the norm)
     psd_status_t rc = ensure_ws(h, static_cast<int>(padded_n(N, batch)), static_cast<int>(batch));
     if (rc != PSD_OK) return rc;
-    cudaError_t e = launch_polar_embed(A, static_cast<int>(n), static_cast<int>(m), static_cast<int>(batch), p.H, p.part,
-                                       nblk, st);
+    cudaError_t e = launch_polar_embed(A, static_cast<int>(rows), static_cast<int>(cols), static_cast<int>(m),
+                                       static_cast<int>(batch), p.H, p.part, nblk, st);
     if (e != cudaSuccess) return cuda_fail(e, "polar_embed");
     h->kernel_launches += 1;
     const psd_bound_t bound = h->bound;
     h->polar_m = static_cast<int>(m);
+    h->polar_wide = rows < cols;
     if (bound == PSD_BOUND_FROBENIUS) {
         // lambda~ = ||A||_F (the Frobenius bound of A; ||H||_F would be sqrt(2) looser)
         e = launch_finalize_bound(p.part, nblk, static_cast<int>(batch), p.lam, nullptr, h->ws.status, st);
         if (e != cudaSuccess) {
             h->polar_m = 0;
+            h->polar_wide = false;
             return cuda_fail(e, "polar norm");
         }
         h->kernel_launches += 1;
@@ -1539,8 +1562,10 @@ psd_status_t psd_polar(psd_filter_t h, const float* A, int64_t n, int64_t batch,
         rc = run(h, p.H, N, batch, p.S, bound == PSD_BOUND_USER ? lambda_in : nullptr, lambda_out, true, st);
     }
     h->polar_m = 0;
+    h->polar_wide = false;
     if (rc != PSD_OK) return rc;
-    e = launch_polar_extract(p.S, static_cast<int>(n), static_cast<int>(m), static_cast<int>(batch), out, st);
+    e = launch_polar_extract(p.S, static_cast<int>(rows), static_cast<int>(cols), static_cast<int>(m),
+                             static_cast<int>(batch), out, st);
     if (e != cudaSuccess) return cuda_fail(e, "polar_extract");
     h->kernel_launches += 1;
     return PSD_OK;

@@ -82,6 +82,8 @@ template <int BN>
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& I, int& J) {
     if (s.sub_mode == 0) {
         upper_tile_coords<BN>(t, s.npad, I, J);
+    } else if (s.sub_mode == 3) {                  // upper tiles of the top-left sub_m block
+        upper_tile_coords<BN>(t, s.sub_m, I, J);
     } else if (s.sub_mode == 1) {                  // upper tiles of the bottom-right sub_m block
         upper_tile_coords<BN>(t, s.sub_m, I, J);
         I += s.sub_m / kTile;

@@ -111,3 +111,31 @@ def test_polar_lanczos_bound(pkg):
         assert lam[b] < 0.5 * polar.frobenius(A[b])                 # ~2 sigma_max / ||A||_F for Ginibre
         ref, _ = polar.polar(A[b], *HALF, lam=float(lam[b]))
         assert np.linalg.norm(U[b] - ref) / np.linalg.norm(ref) < TOL["fp16"]
+
+
+@pytest.mark.parametrize("rows,cols,batch", [(300, 120, 2), (100, 257, 1), (1000, 130, 1)])
+def test_polar_rectangular(pkg, rows, cols, batch):
+    """Tall and wide A (psd_polar_rect): parity against the oracle's rectangular definition."""
+    import torch
+    A = np.stack([np.asarray(synth.ginibre(max(rows, cols), 3 + b), dtype=np.float64)[:rows, :cols]
+                  for b in range(batch)])
+    f = pkg.Filter(pkg.filters.half_filter())
+    lam = torch.zeros(batch, dtype=torch.float64, device="cuda")
+    U = f.polar(torch.tensor(A, dtype=torch.float32, device="cuda"), lambda_out=lam).double().cpu().numpy()
+    assert f.status() == "PSD_OK" and U.shape == A.shape
+    for b in range(batch):
+        ref, lam_o = polar.polar(A[b], *HALF)
+        assert float(lam[b]) == pytest.approx(lam_o, rel=1e-12)
+        assert np.linalg.norm(U[b] - ref) / np.linalg.norm(ref) < TOL["fp16"]
+
+
+def test_polar_tall_then_wide_same_handle(pkg):
+    """One handle, a tall and then a wide input of the same padded edge (the cached runs on H are
+    rebuilt for the other Gram side): both match the oracle."""
+    import torch
+    f = pkg.Filter(pkg.filters.half_filter())
+    for rows, cols in [(300, 120), (120, 300), (300, 120)]:
+        A = np.asarray(synth.ginibre(300, rows + 2 * cols), dtype=np.float64)[:rows, :cols][None]
+        U = f.polar(torch.tensor(A, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+        ref, _ = polar.polar(A[0], *HALF)
+        assert np.linalg.norm(U[0] - ref) / np.linalg.norm(ref) < TOL["fp16"], (rows, cols)

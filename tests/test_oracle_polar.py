@@ -101,3 +101,15 @@ def test_naive_and_blas_products_agree():
     finally:
         chain.matmul = old
     assert np.max(np.abs(U1 - U2)) < 1e-13
+
+
+@pytest.mark.parametrize("rows,cols", [(11, 5), (4, 9)])
+def test_rectangular_matches_svd(rows, cols):
+    """Tall and wide A: the same definition, f(A) = W diag(s(sigma / lambda~)) V^T with the thin SVD."""
+    A = np.random.default_rng(10 + rows).standard_normal((rows, cols))
+    st, kap = HALF
+    U, lam = polar.polar(A, st, kap)
+    assert U.shape == (rows, cols)
+    w, s, vt = np.linalg.svd(A, full_matrices=False)
+    ref = w @ np.diag(chain.scalar_chain(s / lam, st, kap)) @ vt
+    assert np.linalg.norm(U - ref) / np.linalg.norm(ref) < 1e-12
