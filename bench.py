@@ -48,6 +48,10 @@ CONFIGS = {
 # steps), seeded GOE inputs; the FP32-class row is the split precisions (fp16x3 / tf32x3).
 PAPER_B200_SECONDS = {5000: {"fp16": 14.8e-3, "x3": 55.9e-3}, 10000: {"fp16": 54.8e-3, "x3": 416e-3},
                       20000: {"fp16": 301e-3, "x3": 2.99}}
+# psd_polar: the polar iterate of general square matrices by the same filter
+CONFIGS["polar"] = dict(n=4096, batch=8, family="ginibre", filter="half", polar=True,
+                        workload="polar: batch 8 x 4096 x 4096 general (Ginibre) matrices, f~*_half+kappa polar "
+                                 "iterate (psd_polar: Gram + Horner + general product per stage)")
 for _n, _name in ((5000, "p5k"), (10000, "p10k"), (20000, "p20k")):
     CONFIGS[_name] = dict(n=_n, batch=1, family="goe", filter="half", bound="lanczos",
                           workload=f"paper Tables 3-5 size: single n={_n} symmetric matrix, f~*_half fp16 "
@@ -312,6 +316,10 @@ def oracle_filter(name):
 
 
 def run_reference(args, cfg):
+    if cfg.get("polar"):
+        print(json.dumps({"impl": "reference", "unavailable": "the polar config has no reference arm (the "
+                                                              "driver's workload is c4)"}), flush=True)
+        return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -505,6 +513,62 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_polar(args, cfg):
+    """psd_polar on one GPU: matrices/s, and the 1-CTA product kernel's fraction of the tensor peak
+    at the chain's algorithmic work (per stage with p = 2: Gram n^2 (n+1), one symmetric Horner
+    product n^2 (n+1), one general product 2 n^3)."""
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2507_09165_b200 import Filter
+    n, B = cfg["n"], cfg["batch"]
+    stages = product_filter(filter_name(cfg, args.precision))
+    f = Filter(stages, precision=args.precision)
+    host = torch.empty((B, n, n), dtype=torch.float32, pin_memory=True)
+    for b in range(B):
+        host[b].copy_(torch.from_numpy(synth.ginibre(n, synth.SEED_BASE + b).astype(np.float32)))
+    A = host.cuda()
+    out = torch.empty_like(A)
+    for _ in range(args.warmup):
+        f.polar(A, out=out)
+    torch.cuda.synchronize()
+    f.profile_read()
+    f.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            f.polar(A, out=out)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    prod_ms, prod_launches, kernel_launches = f.profile_read()
+    f.profile(False)
+    assert f.status() == "PSD_OK"
+    sym = float(n) * n * (n + 1)
+    alg = sum((len(c) - 1) * sym + 2.0 * n ** 3 for c in stages if len(c) > 1) * B
+    peaks, peak_src = load_peaks()
+    passes = 3 if args.precision.endswith("x3") else 1
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)) / passes
+    if not args.precision.startswith(("fp16", "bf16")):
+        peak /= 2.0
+    achieved = alg * args.steps / (prod_ms / 1e3) / 1e12 if prod_ms else None
+    line = {"metric": "polar_iterates_per_sec", "value": B * args.steps / (ms / 1e3), "unit": "matrices/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic", "config": {"workload": cfg["workload"], "n": n, "global_batch": B,
+                                            "family": "ginibre", "precision": args.precision,
+                                            "l2": "inputs > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if achieved else None,
+                         "kernel": "sym_gemm_kernel (1-CTA tcgen05 product, block-restricted on H = [[0,A],[A^T,0]])",
+                         "per_step_flops": alg, "product_launches": prod_launches,
+                         "peak_source": f"{peak_src} bf16 sustained"},
+            "gpu_launches": kernel_launches, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def run_rowpanel(args, cfg, world, rank, dev):
     """Config c5 on N GPUs: one n x n matrix, row panels, NCCL all-gathers (psd_project_rowpanel)."""
     import numpy as np
@@ -587,6 +651,8 @@ def main():
         sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("polar"):
+        run_polar(args, cfg)
     else:
         run_ours(args, cfg)
 

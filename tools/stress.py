@@ -7,7 +7,7 @@ sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 import synth
-from oracle import admm, chain, tables
+from oracle import admm, chain, polar, tables
 from paper_2507_09165_b200 import Filter, filters
 
 TOL = {"fp16": 5e-3, "bf16": 3e-2, "tf32": 5e-3, "fp16x3": 1e-5, "bf16x3": 1e-4}
@@ -27,13 +27,28 @@ for c in range(cases):
     prec = str(rng.choice(["fp16", "fp16x3", "fp16", "fp16x3", "bf16", "tf32"] if small else
                           ["fp16", "fp16", "bf16", "tf32", "fp16x3", "bf16x3"]))
     fam = str(rng.choice(["goe", "haar", "sdp_shaped", "dominant"]))
-    mode = str(rng.choice(["project", "project", "sign", "admm"]))
+    mode = str(rng.choice(["project", "project", "sign", "admm"] + ([] if small else ["polar"])))
     single = prec.endswith("x3")
     st_p = filters.single_filter() if single else filters.half_filter()
     st_o = (tables.F_SINGLE_REFINED, tables.single_kappas(10)) if single else (tables.F_HALF_REFINED, tables.half_kappas(7))
     f = Filter(st_p, precision=prec)
     b_check = sorted({0, batch - 1})
-    if mode == "admm":
+    if mode == "polar":
+        # a general rows x cols input (psd_polar_rect): the block-restricted products on H = [[0,A],[A^T,0]]
+        cols = int(rng.choice([n, max(1, n // 2), min(2048, n + 37)]))
+        A = np.stack([np.asarray(synth.ginibre(max(n, cols), 1000 * c + b), dtype=np.float64)[:n, :cols]
+                      for b in range(batch)])
+        Ad = torch.tensor(A, dtype=torch.float32, device="cuda")
+        lam = torch.zeros(batch, dtype=torch.float64, device="cuda")
+        U = f.polar(Ad, lambda_out=lam)
+        torch.cuda.synchronize()
+        U, lam = U.double().cpu().numpy(), lam.cpu().numpy()
+        errs = []
+        for b in b_check:
+            ref, _ = polar.polar(A[b], *st_o, lam=float(lam[b]))
+            errs.append(np.linalg.norm(U[b] - ref) / np.linalg.norm(ref))
+        fam = f"{n}x{cols}"
+    elif mode == "admm":
         Cs, Ks, ys = zip(*(synth.maxcut_admm(n, 1000 * c + b) for b in range(batch)))
         C, K, y = np.stack(Cs), np.stack(Ks), np.stack(ys)
         dev = lambda a: torch.tensor(a, dtype=torch.float32, device="cuda").contiguous()
