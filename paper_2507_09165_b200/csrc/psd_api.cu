@@ -721,6 +721,17 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
                  : launch_sym_gemm(ws.op, split, maps(sw.A, sw.B), shape, ep, st);
         if (e != cudaSuccess) return cuda_fail(e, "sym_gemm");
         h->kernel_launches += 1;
+        if (dbg) {           // debug only: per-product phase counters of the pair kernel
+            unsigned long long t[13] = {};
+            cudaStreamSynchronize(st);
+            cudaMemcpy(t, ep.dbg, sizeof(t), cudaMemcpyDeviceToHost);
+            const double tiles = t[4] ? double(t[4]) : 1.0;
+            std::fprintf(stderr, "psd step %zu (D %d, out %s): loop %.0f = tile %.0f + acc %.0f + operand %.0f + issue; "
+                         "epilogue acc-wait %.0f work %.0f cycles/tile; %llu clusters (tiles %llu..%llu), starts "
+                         "spread %.1f us, last end %.1f us after first start\n", si, s.D, s.outF ? "fp32" : "op",
+                         t[3] / tiles, t[0] / tiles, t[1] / tiles, t[2] / tiles, t[5] / (2 * tiles), t[6] / (2 * tiles),
+                         t[7], t[11], t[12], (t[9] - t[8]) * 1e-3, (t[10] - t[8]) * 1e-3);
+        }
         if (tl && tl_buf) {
             std::vector<unsigned long long> t(kTlSlots);
             cudaStreamSynchronize(st);
