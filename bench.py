@@ -550,9 +550,13 @@ def run_polar(args, cfg):
     alg = sum((len(c) - 1) * sym + 2.0 * n ** 3 for c in stages if len(c) > 1) * B
     peaks, peak_src = load_peaks()
     passes = 3 if args.precision.endswith("x3") else 1
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)) / passes
+    # a timed region well under a second does not reach the 1 kW cap: the BURST figure is the
+    # denominator there, the sustained one for long runs (bench contract)
+    long_run = ms > 500.0
+    peak = (peaks.get("bf16_tflops_sustained", 1400.0) if long_run else peaks.get("bf16_tflops", 1590.0)) / passes
     if not args.precision.startswith(("fp16", "bf16")):
         peak /= 2.0
+    peak_src = f"{peak_src} bf16 {'sustained' if long_run else 'burst'} (timed region {ms:.0f} ms)"
     achieved = alg * args.steps / (prod_ms / 1e3) / 1e12 if prod_ms else None
     line = {"metric": "polar_iterates_per_sec", "value": B * args.steps / (ms / 1e3), "unit": "matrices/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -562,9 +566,11 @@ def run_polar(args, cfg):
                                             "l2": "inputs > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if achieved else None,
-                         "kernel": "sym_gemm_kernel (1-CTA tcgen05 product, block-restricted on H = [[0,A],[A^T,0]])",
+                         "kernel": ("sym_gemm_2cta_kernel (CTA-pair tcgen05 product" if pair_kernel(2 * ((n + 255) // 256 * 256), B)
+                                    else "sym_gemm_kernel (1-CTA tcgen05 product") +
+                                   ", block-restricted on H = [[0,A],[A^T,0]])",
                          "per_step_flops": alg, "product_launches": prod_launches,
-                         "peak_source": f"{peak_src} bf16 sustained"},
+                         "peak_source": peak_src},
             "gpu_launches": kernel_launches, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 

@@ -169,6 +169,10 @@ struct psd_filter_s {
         double* part = nullptr;
         int64_t n = 0, batch = 0;
         bool wide = false;         // the plan the cached graphs on H were captured with
+        // CTA-pair kernel (block edge a multiple of 256): its 256-tile lists per block product --
+        // upper tiles of the top-left / bottom-right block, every tile of the top-right block
+        uint32_t* tiles = nullptr;         // [tl: nsym][br: nsym][tr: ntr]
+        int nsym = 0, ntr = 0;
     } pol;
 };
 
@@ -597,7 +601,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         h->kernel_launches += 1 + lanczos_launches(h->lz_steps, n);
     }
     // psd_polar's block-restricted products run on the 1-CTA kernel (tile sub-blocks, K ranges)
-    const bool pair_ok = npad % 256 == 0 && use_pair_kernel(n, batch) && h->polar_m == 0;
+    const bool pair_ok = npad % 256 == 0 && use_pair_kernel(n, batch) && (h->polar_m == 0 || h->pol.tiles);
     const bool bn64 = !pair_ok && sym_gemm_bn(npad, batch) == 64;
     const CUtensorMap* bmaps = bn64 ? ws.tmap64 : ws.tmap;
     auto maps = [&](int A, int B) {
@@ -697,6 +701,11 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
                 if (wide) std::swap(sw.A, sw.B);          // Z U = U Z (polynomials in H commute)
             }
             shape.sub_m = m;
+            if (pair) {                                   // the CTA-pair kernel takes tile lists
+                const auto& pl = h->pol;
+                shape.tiles = shape.sub_mode == 2 ? pl.tiles + 2 * pl.nsym : pl.tiles + (shape.sub_mode == 1 ? pl.nsym : 0);
+                shape.tiles_per_matrix = shape.sub_mode == 2 ? pl.ntr : pl.nsym;
+            }
         }
         EpiParams ep = make_ep(s);
         const bool dbg = pair && !h->capturing && debug_env("PSD_DEBUG_STAMPS") != nullptr;
@@ -1369,6 +1378,7 @@ void free_polar(psd_filter_s* h) {
     if (p.S) cudaFree(p.S);
     if (p.lam) cudaFree(p.lam);
     if (p.part) cudaFree(p.part);
+    if (p.tiles) cudaFree(p.tiles);
     p = psd_filter_s::Polar{};
 }
 
@@ -1525,10 +1535,14 @@ psd_status_t psd_polar_rect(psd_filter_t h, const float* A, int64_t rows, int64_
     if (h->bound == PSD_BOUND_USER && !lambda_in) return fail(PSD_EINVAL, "PSD_BOUND_USER needs lambda_in");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto& p = h->pol;
-    const int64_t m = (n + kTile - 1) / kTile * kTile;      // block edge: a tile boundary
+    // block edge m: a tile boundary of the kernel that will run H's products (256 for the CTA-pair
+    // kernel, whose tile lists are built below; 128 for the 1-CTA kernel)
+    const int64_t m256 = (n + 255) / 256 * 256;
+    const bool pair = use_pair_kernel(2 * m256, batch);
+    const int64_t m = pair ? m256 : (n + kTile - 1) / kTile * kTile;
     const int64_t N = 2 * m;
     const int nblk = polar_blocks_per_matrix(static_cast<int>(m), static_cast<int>(batch));
-    if (p.n != m || p.batch < batch) {
+    if (p.n != m || p.batch < batch || (p.tiles != nullptr) != pair) {
         // stable buffers per (block edge, batch) -- the sign run on H is graph-cached on these pointers
         free_graphs(h);
         free_polar(h);
@@ -1538,6 +1552,22 @@ psd_status_t psd_polar_rect(psd_filter_t h, const float* A, int64_t rows, int64_
             cudaMalloc(&p.part, static_cast<size_t>(batch) * 512 * sizeof(double)) != cudaSuccess) {
             free_polar(h);
             return fail(PSD_ENOMEM, "cudaMalloc polar workspace failed");
+        }
+        if (pair) {
+            const int mt = static_cast<int>(m / 256);
+            std::vector<uint32_t> sym(static_cast<size_t>(mt) * (mt + 1) / 2), all;
+            make_tile_order(mt, mt > 16 ? "grouped8" : "row", sym.data());
+            p.nsym = static_cast<int>(sym.size());
+            all = sym;                                                    // top-left block
+            for (uint32_t c : sym) all.push_back(c + ((static_cast<uint32_t>(mt) << 16) | static_cast<uint32_t>(mt)));  // bottom-right
+            for (int I = 0; I < mt; ++I)                                  // top-right block, row-major
+                for (int J = mt; J < 2 * mt; ++J) all.push_back((static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(J));
+            p.ntr = mt * mt;
+            if (cudaMalloc(&p.tiles, all.size() * sizeof(uint32_t)) != cudaSuccess ||
+                cudaMemcpy(p.tiles, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+                free_polar(h);
+                return fail(PSD_ENOMEM, "polar tile lists");
+            }
         }
         p.n = m;
         p.batch = batch;

@@ -85,7 +85,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = (rank == 0);
     const int total_tiles = s.tiles_per_matrix * s.batch;
-    const int num_kb = s.npad / kBK;
+    const int kbeg = s.k_begin / kBK;                 // K range (whole npad unless psd_polar's block products)
+    const int num_kb = (s.k_end > 0 ? s.k_end : s.npad) / kBK - kbeg;
     // K blocks per accumulation run: split precisions restart the accumulator every s.kchunk K
     // elements (GemmShape::kchunk); otherwise one run per tile
     const int chunk_kb = (kSplit && s.kchunk >= kBK) ? s.kchunk / kBK : num_kb;
@@ -162,7 +163,7 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     uint8_t* sa = ring + st * kStageBytes;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
                     else ptx::mbar_arrive_remote(full_leader);
-                    const int k0 = kb * kBK;
+                    const int k0 = (kbeg + kb) * kBK;
                     // upper-only storage: left of block `blk`'s diagonal tile the panel is the stored
                     // upper tile transposed -- two 64x64 boxes (rows k0.., this CTA's 128 columns) that
                     // the MMA reads as an MN-major operand
@@ -235,8 +236,8 @@ sym_gemm_2cta_kernel(const __grid_constant__ OperandMaps tm, const GemmShape s, 
                     // upper-only storage: operands left of their diagonal tile arrive transposed
                     // (MN-major: 64-element MN chunks 8 KB apart = LBO, 8-row K groups 1 KB apart = SBO;
                     // one K step of 16 = 2 KB); the instruction descriptor says which is which
-                    const bool a_mn = Tr::kBytes == 2 && s.upper_only && kb * kBK < tI * kT2;
-                    const bool b_mn = Tr::kBytes == 2 && s.upper_only && kb * kBK < tJ * kT2;
+                    const bool a_mn = Tr::kBytes == 2 && s.upper_only && (kbeg + kb) * kBK < tI * kT2;
+                    const bool b_mn = Tr::kBytes == 2 && s.upper_only && (kbeg + kb) * kBK < tJ * kT2;
                     const uint64_t adesc = a_mn ? ptx::smem_desc_sw128_mnmajor(sa, kTileBytes1 / 2, 1024)
                                                 : ptx::smem_desc_sw128_kmajor(sa);
                     const uint64_t bdesc = b_mn ? ptx::smem_desc_sw128_mnmajor(sa + kTileBytes1, kTileBytes1 / 2, 1024)

@@ -44,7 +44,8 @@ def _run(pkg, A, prec, bound="frobenius", lam_in=None):
     (160, 2, "fp16x3"),     # FP32-class
     (512, 2, "fp16"),       # m = 512: 128 x 64 tiles (few-tile BN) in both block modes
     (512, 1, "tf32x3"),     # FP32-class with a K range of one accumulation run
-    (2048, 2, "fp16"),      # m = 2048: 128 x 128 tiles, K ranges of 2048
+    (2048, 2, "fp16"),      # m = 2048: the CTA-pair kernel on its polar tile lists, K ranges of 2048
+    (1024, 4, "fp16x3"),    # CTA-pair kernel, split path: K range of two accumulation chunks
 ])
 def test_polar_parity(pkg, n, batch, prec):
     A = np.stack([synth.ginibre(n, 7 * n + b) for b in range(batch)])
@@ -113,7 +114,8 @@ def test_polar_lanczos_bound(pkg):
         assert np.linalg.norm(U[b] - ref) / np.linalg.norm(ref) < TOL["fp16"]
 
 
-@pytest.mark.parametrize("rows,cols,batch", [(300, 120, 2), (100, 257, 1), (1000, 130, 1)])
+@pytest.mark.parametrize("rows,cols,batch", [(300, 120, 2), (100, 257, 1), (1000, 130, 1),
+                                             (600, 1100, 2)])   # wide on the CTA-pair kernel (top-left tiles)
 def test_polar_rectangular(pkg, rows, cols, batch):
     """Tall and wide A (psd_polar_rect): parity against the oracle's rectangular definition."""
     import torch
