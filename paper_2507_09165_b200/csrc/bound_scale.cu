@@ -147,7 +147,7 @@ template <OpType T>
 __global__ void __launch_bounds__(256)
 scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double* __restrict__ lambda,
                      double scale, typename Cvt<T>::type* __restrict__ out_op, typename Cvt<T>::type* __restrict__ out_lo,
-                     float op_scale, float* __restrict__ outF, double post, const InputForm form) {
+                     float op_scale, float* __restrict__ outF, double post, const InputForm form, int mirror_block) {
     using op_t = typename Cvt<T>::type;
     __shared__ float S[kST][kST + 1];
     const int b = blockIdx.y;
@@ -227,7 +227,10 @@ scale_convert_kernel(const float* __restrict__ X, int n, int npad, const double*
             uint4* od = reinterpret_cast<uint4*>(dstb + base + static_cast<int64_t>(r0 + r) * npad + c0 + cs);
 #pragma unroll
             for (int q = 0; q < 16 / kVec; ++q) od[q] = *reinterpret_cast<const uint4*>(vd + q * kVec);
-            if (I != J) {
+            // upper-only operand storage (mirror_block > 0): the product kernels read the lower triangle
+            // only inside the diagonal mirror_block x mirror_block blocks, so the mirrored tile is
+            // written there alone (half the operand-copy writes of the scale pass)
+            if (I != J && (mirror_block == 0 || r0 / mirror_block == c0 / mirror_block)) {
                 uint4* ot = reinterpret_cast<uint4*>(dstb + base + static_cast<int64_t>(c0 + r) * npad + r0 + cs);
 #pragma unroll
                 for (int q = 0; q < 16 / kVec; ++q) ot[q] = *reinterpret_cast<const uint4*>(vt + q * kVec);
@@ -276,24 +279,24 @@ cudaError_t launch_finalize_bound(const double* partial, int nblk, int batch, do
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
                                  const double* lambda, double scale, void* out_op, void* out_lo,
                                  double op_scale, float* outF, double post, cudaStream_t stream,
-                                 const InputForm& form) {
+                                 const InputForm& form, int mirror_block) {
     const int nt = npad / kST;
     dim3 grid(nt * (nt + 1) / 2, batch);
     switch (t) {
         case OpType::F16:
             scale_convert_kernel<OpType::F16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__half*>(out_op), static_cast<__half*>(out_lo),
-                static_cast<float>(op_scale), outF, post, form);
+                static_cast<float>(op_scale), outF, post, form, mirror_block);
             break;
         case OpType::BF16:
             scale_convert_kernel<OpType::BF16><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<__nv_bfloat16*>(out_op),
-                static_cast<__nv_bfloat16*>(out_lo), static_cast<float>(op_scale), outF, post, form);
+                static_cast<__nv_bfloat16*>(out_lo), static_cast<float>(op_scale), outF, post, form, mirror_block);
             break;
         case OpType::TF32:
             scale_convert_kernel<OpType::TF32><<<grid, 256, 0, stream>>>(
                 X, n, npad, lambda, scale, static_cast<float*>(out_op), static_cast<float*>(out_lo),
-                static_cast<float>(op_scale), outF, post, form);
+                static_cast<float>(op_scale), outF, post, form, mirror_block);
             break;
     }
     return cudaGetLastError();

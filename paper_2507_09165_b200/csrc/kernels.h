@@ -212,6 +212,6 @@ void lanczos_prepare();   // kernel attributes (call once, outside graph capture
 cudaError_t launch_scale_convert(OpType t, const float* X, int n, int npad, int batch,
                                  const double* lambda, double scale, void* out_op, void* out_lo,
                                  double op_scale, float* outF, double post, cudaStream_t stream,
-                                 const InputForm& form = InputForm());
+                                 const InputForm& form = InputForm(), int mirror_block = 0);
 
 }  // namespace psd

@@ -587,13 +587,16 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
         sc[B_Y] = h->s_y;
         sc[B_UA] = sc[B_UB] = h->s_u;
     }
+    // upper-only operand storage: X0's lower triangle is read only inside the diagonal tiles (at most
+    // 256 x 256), so the scale pass writes the mirrored 64-tiles there alone
+    const int x0_mirror_block = upper_only_mode(h, n, batch, npad) ? 256 : 0;
     if (h->bound == PSD_BOUND_LANCZOS) {
         // X / lambda_F into the operand buffer, Lanczos on its square, then lambda~ <- the
         // Theorem-2 bound (never looser than lambda_F); the real scale below uses it
         rc = ensure_lz(h, npad, batch);
         if (rc != PSD_OK) return rc;
         e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0], nullptr, sc[B_X0], nullptr, 0.0, st,
-                                 form);
+                                 form, x0_mirror_block);
         if (e != cudaSuccess) return cuda_fail(e, "scale_convert (Lanczos bound)");
         e = launch_lanczos_bound(ws.op, ws.op_buf[B_X0], sc[B_X0], n, npad, batch, h->lz_steps, h->lz_safety,
                                  ws.lz_scratch, ws.lambda, lambda_out, st);
@@ -619,7 +622,7 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
     // (a2) scale + convert; the products-free sign chain finishes here
     e = launch_scale_convert(ws.op, X, n, npad, batch, lam, 1.0, ws.op_buf[B_X0],
                              split ? ws.op_buf[B_X0 + B_COUNT] : nullptr, sc[B_X0],
-                             (want_sign && steps.empty()) ? out : nullptr, sign_only, st, form);
+                             (want_sign && steps.empty()) ? out : nullptr, sign_only, st, form, x0_mirror_block);
     if (e != cudaSuccess) return cuda_fail(e, "scale_convert");
     h->kernel_launches += 1;
     // (a3-a6) products
