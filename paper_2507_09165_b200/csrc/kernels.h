@@ -154,6 +154,7 @@ struct SmallPlan {
     float* out2;              // ADMM: X_next = sigma2 (P - M), stored like out
     float sigma2;
     unsigned long long* dbg;  // debug: per-phase clock totals of CTA 0 (NULL in production)
+    int split_commit;         // chain products: one MMA commit per matrix, each matrix's epilogue starts on its own
     SmallStep steps[40];
 };
 int small_slot_offset(bool split, int slot);   // slot 0 Z, 1 Y, 2 U

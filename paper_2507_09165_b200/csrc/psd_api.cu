@@ -495,6 +495,9 @@ psd_status_t run_body(psd_filter_t h, const float* X, int64_t n64, int64_t batch
             sp_plan.sigma2 = admm->sigma;
         }
         sp_plan.s_x0 = static_cast<float>(sz);
+        // one MMA commit per matrix in the chain products (c2: 146 -> 135 us fp16, 295 -> 273 us fp16x3 in the
+        // debug build, profiles/r2s3/c2_split_commit/); PSD_SMALL_SPLIT_COMMIT=0 (debug build) for the A/B
+        sp_plan.split_commit = debug_env("PSD_SMALL_SPLIT_COMMIT") ? std::atoi(debug_env("PSD_SMALL_SPLIT_COMMIT")) : 1;
         for (size_t i = 0; i < steps.size(); ++i) {
             const Step& s = steps[i];
             SmallStep& q = sp_plan.steps[i];

@@ -17,7 +17,8 @@
 //     X_0 restaged for the last product, the result symmetrised through smem (exact symmetry) and
 //     stored to HBM.
 // 4 CTAs of 4 warps per SM on the 16-bit path (2 on the split path): while one CTA waits for its
-// MMAs, the others run their epilogues.  Only the issuing thread waits on the MMA barrier; the
+// MMAs, the others run their epilogues.  Chain products commit each matrix's MMAs separately, so
+// matrix 0's epilogue overlaps matrix 1's MMAs (SmallPlan::split_commit).  Only the issuing thread waits on the MMA barrier; the
 // other warps sleep in bar.sync (a 256-thread spin on the mbarrier took ~15% of the issue slots
 // in the first version, profiles/r2_c2_small_v2.md).
 #include <cuda_fp16.h>
@@ -420,6 +421,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * L::kPerMatrix);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
     double* red = reinterpret_cast<double*>(mma_bar + 2);     // [2 matrices][8 warps]
+    uint64_t* mma_bar1 = mma_bar + 2 + 16;                    // split commits: matrix 1's products
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = warp & 3;                      // TMEM lane quadrant (warp % 4, the hardware rule)
@@ -438,6 +440,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(mma_bar, 1);
+        ptx::mbar_init(mma_bar1, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 0) ptx::tmem_alloc<128>(tmem_slot);   // cols [0,64): accumulator, [64,128): the input rows
@@ -448,7 +451,7 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
     const uint32_t tmem_row = tmem + (static_cast<uint32_t>(32 * q) << 16);
     const uint32_t tmem_x = tmem_row + 64 + kCT * hw;     // this thread's input columns
     constexpr uint32_t kIdesc = ptx::make_idesc(0, 64, 64);   // f16 x f16 -> f32, M=64, N=64
-    uint32_t mma_phase = 0;
+    uint32_t mma_phase = 0, mma_phase1 = 0;
 
     const int pairs = (batch + 1) / 2;
     for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
@@ -624,6 +627,63 @@ small_batch_kernel(const float* __restrict__ X, float* __restrict__ out, int n, 
             }
             const long long t_a = kDebug ? clock64() : 0;
             long long t_i = t_a;
+            if (plan.split_commit && st.final_mode == 0) {
+                // one commit per matrix: matrix 0's epilogue runs while matrix 1's MMAs finish (the
+                // two matrices use disjoint operand slots and TMEM lane halves)
+                if (threadIdx.x == 0) {
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(smem + st.slot_a), b0 = ptx::smem_u32(smem + st.slot_b);
+                    const uint64_t ad0 = ptx::smem_desc_sw128_kmajor(a0), bd0 = ptx::smem_desc_sw128_kmajor(b0);
+                    constexpr uint64_t kMatDesc = static_cast<uint64_t>(L::kPerMatrix >> 4);
+                    constexpr uint64_t kLoDesc = static_cast<uint64_t>(kSlotBytes >> 4);
+#pragma unroll
+                    for (int mm = 0; mm < 2; ++mm) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t koff = static_cast<uint64_t>((k * 32) >> 4);
+                            const uint64_t ad = ad0 + mm * kMatDesc + koff, bd = bd0 + mm * kMatDesc + koff;
+                            const uint32_t d = tmem + (static_cast<uint32_t>(16 * mm) << 16);
+                            ptx::mma_f16(d, ad, bd, kIdesc, k != 0);
+                            if constexpr (kSplit) {
+                                ptx::mma_f16(d, ad, bd + kLoDesc, kIdesc, 1u);
+                                ptx::mma_f16(d, ad + kLoDesc, bd, kIdesc, 1u);
+                            }
+                        }
+                        ptx::mma_commit(mm == 0 ? mma_bar : mma_bar1);
+                    }
+                }
+                const float2 alpha = make_float2(st.alpha * st.out_scale, st.alpha * st.out_scale);
+                const float2 beta = make_float2(st.beta * st.out_scale, st.beta * st.out_scale);
+                const bool has_d = st.slot_d >= 0;
+                const uint32_t pd = smem_base + static_cast<uint32_t>(has_d ? st.slot_d : 0);
+                const uint32_t po = smem_base + static_cast<uint32_t>(st.slot_out);
+                auto epi = [&](int mm) {
+                    switch (q) {
+                        case 0: chain_epilogue<kSplit, 0>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                        case 1: chain_epilogue<kSplit, 1>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                        case 2: chain_epilogue<kSplit, 2>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                        default: chain_epilogue<kSplit, 3>(tmem, mm, pd, po, L::kPerMatrix, has_d, alpha, beta, lane, diag_mask); break;
+                    }
+                };
+                if (kQW == 2) {                          // 8 warps: warp half hw serves matrix hw
+                    ptx::mbar_wait(hw == 0 ? mma_bar : mma_bar1, hw == 0 ? mma_phase : mma_phase1);
+                    ptx::tc_fence_after();
+                    epi(hw);
+                } else {
+                    ptx::mbar_wait(mma_bar, mma_phase);
+                    ptx::tc_fence_after();
+                    epi(0);
+                    ptx::mbar_wait(mma_bar1, mma_phase1);
+                    ptx::tc_fence_after();
+                    epi(1);
+                }
+                mma_phase ^= 1;
+                mma_phase1 ^= 1;
+                ptx::tc_fence_before();
+                fence_proxy_async_smem();
+                __syncthreads();
+                continue;
+            }
             if (threadIdx.x == 0) {
                 ptx::tc_fence_after();
                 // the two matrices' K steps interleaved: two independent accumulation chains in
