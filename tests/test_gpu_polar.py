@@ -46,6 +46,7 @@ def _run(pkg, A, prec, bound="frobenius", lam_in=None):
     (512, 1, "tf32x3"),     # FP32-class with a K range of one accumulation run
     (2048, 2, "fp16"),      # m = 2048: the CTA-pair kernel on its polar tile lists, K ranges of 2048
     (1024, 4, "fp16x3"),    # CTA-pair kernel, split path: K range of two accumulation chunks
+    (1024, 4, "tf32"),      # CTA-pair kernel with full (mirrored) operand storage
 ])
 def test_polar_parity(pkg, n, batch, prec):
     A = np.stack([synth.ginibre(n, 7 * n + b) for b in range(batch)])
@@ -141,3 +142,14 @@ def test_polar_tall_then_wide_same_handle(pkg):
         U = f.polar(torch.tensor(A, dtype=torch.float32, device="cuda")).double().cpu().numpy()
         ref, _ = polar.polar(A[0], *HALF)
         assert np.linalg.norm(U[0] - ref) / np.linalg.norm(ref) < TOL["fp16"], (rows, cols)
+
+
+def test_polar_lanczos_bound_pair_kernel(pkg):
+    """The Lanczos bound of H on the CTA-pair path (n = 1024, batch 8: 2m = 2048, 288 tiles)."""
+    A = np.stack([synth.ginibre(1024, 61 + b) for b in range(8)])
+    U, lam, f = _run(pkg, A, "fp16", bound="lanczos")
+    assert f.status() == "PSD_OK"
+    for b in (0, 7):
+        assert np.linalg.norm(A[b], 2) <= lam[b] <= polar.frobenius(A[b]) * (1 + 1e-12)
+        ref, _ = polar.polar(A[b], *HALF, lam=float(lam[b]))
+        assert np.linalg.norm(U[b] - ref) / np.linalg.norm(ref) < TOL["fp16"]
